@@ -1,0 +1,145 @@
+/*
+ * xmg.h — C ABI of libxmg.so, the B200 (sm_100a) batched XLand-MiniGrid step.
+ *
+ * This is the drop-in boundary for the reference's batched operator API
+ * (`rulegrid.VecEnv`, /root/reference/pkg/src/rulegrid/vecenv.py).  The
+ * reference is a pure-Python package with no FFI; the entry points below are
+ * what its VecEnv would bind if its NumPy body were replaced by native code
+ * (see INTEGRATION.md for the ctypes stub).  Each entry point cites the
+ * reference interface it replaces.
+ *
+ * Conventions
+ *  - All buffer pointers are DEVICE pointers (cudaMalloc / torch CUDA
+ *    tensors) unless stated; the library never allocates or frees them.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *    asynchronous on that stream.
+ *  - Return value: 0 on success, < 0 on error; xmg_last_error() returns a
+ *    thread-local message for the last failing call on this thread.
+ *  - Scalar key helpers (xmg_key_*) run on the host.
+ *
+ * Device state layout (structure of arrays, one row per env):
+ *   grids  u8  [n][H*W]   row-major entity codes tile*16+color
+ *                          (allocation must extend >= 64 bytes past n*H*W:
+ *                          the step kernel reads 16-byte aligned chunks)
+ *   agent  u64 [n]        r | c<<8 | dir<<16 | pocket<<24 | step_count<<32
+ *   rng    u64 [n][2]     state key (hi, lo) = ref EnvState.rng
+ *   goal   u32 [n]        goal encoding bytes (kind, a1, a2, a3) little-endian
+ *   task   i32 [n]        row of the task table this env runs
+ * Task table (read-only), u32 [num_tasks][row_words]:
+ *   word 0 = goal, word 1 = rule_count | obj_count<<8,
+ *   words 2..2+R-1 = active rules (kind, in_a, in_b, out) left-packed,
+ *   then ceil(O/4) words of active object codes, left-packed.
+ */
+#ifndef XMG_H_
+#define XMG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XMG_ABI_VERSION 1
+
+/* scenario ids: ref scenarios.py:415-423 (SCENARIOS) */
+enum {
+    XMG_SCENARIO_XLAND = 0,
+    XMG_SCENARIO_EMPTY = 1,
+    XMG_SCENARIO_EMPTY_RANDOM = 2,
+    XMG_SCENARIO_DOOR_KEY = 3,
+    XMG_SCENARIO_FOUR_ROOMS = 4,
+    XMG_SCENARIO_UNLOCK = 5,
+    XMG_SCENARIO_UNLOCK_PICKUP = 6
+};
+
+/* action dtypes accepted by xmg_step / xmg_validate_actions */
+enum { XMG_ACT_U8 = 0, XMG_ACT_I32 = 1, XMG_ACT_I64 = 2 };
+
+/* Static environment description: ref EnvParams (env.py:50-73) plus the
+ * layout plan (layouts.py:474-529) and the task table, all pre-resolved on
+ * the host.  Pointers are device pointers. */
+typedef struct xmg_env_desc {
+    int32_t height, width, view_size, budget;
+    int32_t scenario;            /* XMG_SCENARIO_* */
+    int32_t see_through_walls;   /* 0: exact-integer line of sight, observation.py:46-87 */
+    int32_t num_segments;        /* door segments, layouts.py:509-520 */
+    int32_t fixed_doors;         /* R6: doors at segment midpoints */
+    int32_t rule_width;          /* R (max active rules over the table) */
+    int32_t obj_width;           /* O (max active objects over the table) */
+    int32_t row_words;           /* u32 words per task row = 2 + R + ceil(O/4) */
+    int32_t num_tasks;           /* M rows in task_rows */
+    const uint8_t* base_cells;   /* [H*W] grid before doors/objects for this scenario */
+    const int16_t* seg_off;      /* [num_segments+1] offsets into seg_cells */
+    const int16_t* seg_cells;    /* flat cell indices of each door segment */
+    const uint32_t* task_rows;   /* [num_tasks][row_words] */
+} xmg_env_desc;
+
+typedef struct xmg_state {
+    uint8_t* grids;
+    uint64_t* agent;
+    uint64_t* rng;
+    uint32_t* goal;
+    int32_t* task;
+} xmg_state;
+
+/* VecTimeStep (vecenv.py:95-105): observations may be NULL (compute_obs=False) */
+typedef struct xmg_out {
+    uint8_t* obs;       /* [n][v][v][2] (tile, color) */
+    float* reward;      /* [n]  float32(1.0 - 0.9*(sc/budget)) evaluated in fp64 */
+    float* discount;    /* [n] */
+    int8_t* step_type;  /* [n]  FIRST 0 / MID 1 / LAST 2 */
+} xmg_out;
+
+int32_t xmg_abi_version(void);
+const char* xmg_last_error(void);
+
+/* ---- counter-based RNG (ref rng.py) -------------------------------------- */
+
+/* One Philox4x64-10 block per row: out[i] = philox4(ctr[i], key[i]).
+ * Known-answer hook for ref rng.py:42-57 / philox4_array :74-93. */
+int32_t xmg_philox(const uint64_t* ctr /*[n][4]*/, const uint64_t* key /*[n][2]*/, uint64_t* out /*[n][4]*/,
+                   int64_t n, void* stream);
+
+/* keys[i] = fold_in(root, offset + i, SPLIT): ref split_batch rng.py:142-145
+ * (offset lets a GPU shard derive the keys of its global env range). */
+int32_t xmg_split_batch(uint64_t root_hi, uint64_t root_lo, int64_t offset, int64_t n, uint64_t* keys /*[n][2]*/,
+                        void* stream);
+
+/* Random policy: actions[t][i] = word (t0+t) of keys[i]'s draw stream mod 6,
+ * ref harness.py:269-275 (random_policy) with per-env keys. */
+int32_t xmg_random_actions(const uint64_t* keys /*[n][2]*/, int64_t n, int64_t t0, int64_t steps,
+                           uint8_t* actions /*[steps][n]*/, void* stream);
+
+/* Host-side scalar helpers: ref key_from_seed rng.py:96-99 and
+ * fold_in rng.py:107-110 (domain: 1 draw, 2 split, 3 fold, 4 seed). */
+void xmg_key_from_seed(uint64_t seed_lo, uint64_t seed_hi, uint64_t* out2);
+void xmg_fold_in(uint64_t hi, uint64_t lo, uint64_t data, int32_t domain, uint64_t* out2);
+void xmg_philox_host(const uint64_t ctr[4], uint64_t k0, uint64_t k1, uint64_t out[4]);
+
+/* ---- the batched environment (ref vecenv.py) ----------------------------- */
+
+/* ref VecEnv.reset_with_keys (vecenv.py:205-222): reset env i from keys[i];
+ * writes the FIRST VecTimeStep (obs, reward 0, discount 1, step type 0). */
+int32_t xmg_reset(const xmg_env_desc* desc, const xmg_state* state, const uint64_t* keys /*[n][2]*/, int64_t n,
+                  const xmg_out* out, void* stream);
+
+/* Sets *flag (device int32, caller zeroes it) to 1 when any action lies
+ * outside [0, 6): the device half of ref vecenv.py:297-301 (InvalidAction). */
+int32_t xmg_validate_actions(const void* actions, int32_t action_dtype, int64_t n, int32_t* flag, void* stream);
+
+/* ref VecEnv.step (vecenv.py:295-364): action, rules, goal, reward, auto-reset
+ * from each env's own rng, observation of the next playable state.
+ * abort_flag (device, nullable): when *abort_flag != 0 no env is touched
+ * (pairs with xmg_validate_actions so an invalid batch mutates nothing). */
+int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* actions, int32_t action_dtype,
+                 int64_t n, const xmg_out* out, const int32_t* abort_flag, void* stream);
+
+/* Bytes of dynamic shared memory per 128-env CTA the step/reset kernels use
+ * for this description (host query, for capacity checks). <0 if unsupported. */
+int64_t xmg_step_smem_bytes(const xmg_env_desc* desc);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* XMG_H_ */

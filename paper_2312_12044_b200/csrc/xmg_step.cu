@@ -1,0 +1,949 @@
+// xmg_step.cu — B200 (sm_100a) batched XLand-MiniGrid environment step.
+//
+// Implements the C ABI declared in include/xmg.h.  The hot path is ONE fused
+// kernel (`step_kernel`) that replaces the reference's NumPy VecEnv.step
+// (/root/reference/pkg/src/rulegrid/vecenv.py:295-364, cited as ref:<file>:<line>):
+//   action (:306-342) -> rules (:368-433) -> goal (:435-477) -> reward /
+//   discount / step type (:351-357) -> auto-reset of finished trials
+//   (:359-361 -> :224-291) -> egocentric observation (:481-500).
+//
+// Mapping:
+//  * one thread per env, 128 envs per CTA; the per-env SoA state is read with
+//    coalesced 8-byte loads (agent word) and written back the same way;
+//  * the grid bytes the step needs (the view window around the post-action
+//    pose, extended one cell ahead for MOVE so the target cell is inside) are
+//    fetched as 16-byte aligned chunks straight into a per-thread shared
+//    memory stage: the rest of a 13x13..25x25 grid is never read on the
+//    common no-event path;
+//  * rare work is warp-cooperative: every env whose trial ends is rebuilt by
+//    its whole warp (Philox draws spread over the lanes, the stable argsort of
+//    the reference replaced by an exact rank count in shared memory, the new
+//    grid written with contiguous stores);
+//  * observations are assembled in shared memory in the reference layout
+//    (n, v, v, 2) and leave the CTA as one TMA bulk store (cp.async.bulk).
+// Nothing here is a dense contraction, so no tensor cores are used; the
+// kernel is bounded by HBM bytes per env-step (roofline).
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/xmg.h"
+
+namespace {
+
+// ------------------------------------------------------------------ Philox
+// ref:rng.py:23-32
+constexpr uint64_t kM0 = 0xD2E7470EE14C6C93ULL;
+constexpr uint64_t kM1 = 0xCA5A826395121157ULL;
+constexpr uint64_t kW0 = 0x9E3779B97F4A7C15ULL;
+constexpr uint64_t kW1 = 0xBB67AE8584CAA73BULL;
+constexpr uint64_t kDomDraw = 1, kDomSplit = 2, kDomSeed = 4;
+
+struct Words4 {
+  uint64_t w0, w1, w2, w3;
+};
+
+// Philox4x64-10, ref:rng.py:42-57.  __umul64hi gives the high half of the
+// 64x64 product the reference builds from 32-bit limbs (rng.py:60-71).
+__device__ __forceinline__ Words4 philox(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3, uint64_t k0,
+                                         uint64_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t hi0 = __umul64hi(kM0, c0), lo0 = kM0 * c0;
+    const uint64_t hi1 = __umul64hi(kM1, c2), lo1 = kM1 * c2;
+    const uint64_t n0 = hi1 ^ c1 ^ k0;
+    const uint64_t n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+    k0 += kW0;
+    k1 += kW1;
+  }
+  return {c0, c1, c2, c3};
+}
+
+void philox_host(const uint64_t ctr[4], uint64_t k0, uint64_t k1, uint64_t out[4]) {
+  uint64_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+  for (int r = 0; r < 10; ++r) {
+    const unsigned __int128 p0 = (unsigned __int128)kM0 * c0;
+    const unsigned __int128 p1 = (unsigned __int128)kM1 * c2;
+    const uint64_t n0 = (uint64_t)(p1 >> 64) ^ c1 ^ k0;
+    const uint64_t n2 = (uint64_t)(p0 >> 64) ^ c3 ^ k1;
+    c1 = (uint64_t)p1;
+    c3 = (uint64_t)p0;
+    c0 = n0;
+    c2 = n2;
+    k0 += kW0;
+    k1 += kW1;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
+// ------------------------------------------------------------------ codes
+// ref:core.py:17-70; ref:layouts.py:39-42
+constexpr int kFloor = 3, kWall = 4, kBall = 5, kGoal = 8, kKey = 9, kLocked = 10, kClosed = 11, kOpen = 12;
+constexpr uint8_t kFloorCode = 57, kWallCode = 72, kGreenGoal = 132;
+__constant__ uint8_t cGenColors[10] = {3, 4, 5, 6, 7, 8, 10, 11, 12, 13};
+// tile-class bitmasks over the tile nibble (ref:core.py:53-59, ref:observation.py:21)
+constexpr uint32_t kWalkable = (1u << kFloor) | (1u << kGoal) | (1u << kOpen);
+constexpr uint32_t kPickable = (1u << 5) | (1u << 6) | (1u << 7) | (1u << 9) | (1u << 13) | (1u << 14);
+constexpr uint32_t kOpaque = (1u << kWall) | (1u << kClosed) | (1u << kLocked);
+// trigger gates as event bitmasks (ref:rules.py:60-72, ref:goals.py:268-283)
+__constant__ uint8_t cRuleGate[12] = {0, 0x2, 0x7, 0x4, 0x4, 0x4, 0x4, 0x4, 0x7, 0x7, 0x7, 0x7};
+__constant__ uint8_t cGoalGate[15] = {0, 0x2, 0x7, 0x7, 0x4, 0x7, 0x4, 0x4, 0x4, 0x4, 0x4, 0x7, 0x7, 0x7, 0x7};
+
+// direction deltas (ref:core.py:272) and the view's right-hand vector (ref:observation.py:24-25)
+__device__ __forceinline__ int dir_dr(int d) { return d == 0 ? -1 : (d == 2 ? 1 : 0); }
+__device__ __forceinline__ int dir_dc(int d) { return d == 1 ? 1 : (d == 3 ? -1 : 0); }
+// NEAR_OFFSETS = up, left, right, down (ref:rules.py:76)
+__device__ __forceinline__ int near_dr(int k) { return k == 0 ? -1 : (k == 3 ? 1 : 0); }
+__device__ __forceinline__ int near_dc(int k) { return k == 1 ? -1 : (k == 2 ? 1 : 0); }
+
+constexpr int kThreads = 128;  // envs per CTA
+constexpr int kWarps = kThreads / 32;
+
+// ------------------------------------------------------- smem geometry
+struct Geo {
+  int ob;      // observation bytes per env (2 v^2)
+  int stg;     // per-thread window stage bytes (16*maxch + 16 bank pad)
+  int hwp;     // H*W rounded up to 16 (+16)
+  int ws;      // per-warp reset scratch bytes
+  int maxch;   // window chunk capacity
+  int64_t total;
+};
+
+__host__ __device__ inline int round16(int x) { return (x + 15) & ~15; }
+
+__host__ __device__ inline Geo make_geo(int H, int W, int V, int maxch) {
+  Geo g;
+  g.ob = 2 * V * V;
+  g.maxch = maxch;
+  g.stg = maxch ? 16 * maxch + 16 : 0;
+  g.hwp = round16(H * W + 16);
+  // Wd: u64[hwp] | FC: u16[hwp] | G: u8[hwp] | misc: 64 u64
+  g.ws = 8 * g.hwp + 2 * g.hwp + g.hwp + 512;
+  g.total = (int64_t)kThreads * round16(g.ob) + (int64_t)kThreads * g.stg + (int64_t)kWarps * g.ws;
+  return g;
+}
+
+// chunk capacity needed for the (MOVE-extended) window: span = v*W + v bytes
+inline int needed_chunks(int W, int V) { return (V * W + V + 30) / 16; }
+
+// ------------------------------------------------------- per-thread view
+// The bytes of one env's grid staged in shared memory: stage[k] mirrors grid
+// flat index sbase + k for flat indices in [slo, shi); everything else falls
+// through to global memory.
+struct View {
+  uint8_t* g;      // env grid in global memory
+  uint8_t* stage;  // per-thread shared stage (nullptr when unused)
+  int sbase, slo, shi;
+
+  __device__ __forceinline__ uint8_t rd(int f) const {
+    return (f >= slo && f < shi) ? stage[f - sbase] : g[f];
+  }
+  __device__ __forceinline__ void wr(int f, uint8_t v) const {
+    g[f] = v;
+    if (f >= slo && f < shi) stage[f - sbase] = v;
+  }
+};
+
+// Bounding box of the view window for pose (r, c, d), extended by `ext`
+// cells ahead (ref:vecenv.py:77-92 / ref:observation.py:28-43), clipped.
+__device__ __forceinline__ void window_span(int r, int c, int d, int ext, int H, int W, int V, int& lo, int& hi) {
+  const int h = V / 2;
+  int r0, r1, c0, c1;
+  switch (d) {
+    case 0: r0 = r - (V - 1) - ext; r1 = r; c0 = c - h; c1 = c + h; break;
+    case 1: r0 = r - h; r1 = r + h; c0 = c; c1 = c + (V - 1) + ext; break;
+    case 2: r0 = r; r1 = r + (V - 1) + ext; c0 = c - h; c1 = c + h; break;
+    default: r0 = r - h; r1 = r + h; c0 = c - (V - 1) - ext; c1 = c; break;
+  }
+  r0 = max(r0, 0); c0 = max(c0, 0); r1 = min(r1, H - 1); c1 = min(c1, W - 1);
+  lo = r0 * W + c0;
+  hi = r1 * W + c1 + 1;
+}
+
+template <int MAXCH>
+__device__ __forceinline__ void stage_from_global(View& vw, int lo, int hi, int HW) {
+  if constexpr (MAXCH == 0) {
+    vw.slo = vw.shi = 0;
+    vw.sbase = 0;
+  } else {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(vw.g + lo) & ~uintptr_t(15);
+    const uintptr_t a1 = reinterpret_cast<uintptr_t>(vw.g + hi);
+    const int nch = (int)((a1 - a0 + 15) >> 4);
+    vw.sbase = (int)(a0 - reinterpret_cast<uintptr_t>(vw.g));
+    vw.slo = max(vw.sbase, 0);
+    vw.shi = min(vw.sbase + 16 * nch, HW);
+    const uint4* src = reinterpret_cast<const uint4*>(a0);
+    uint4* dst = reinterpret_cast<uint4*>(vw.stage);
+    constexpr int B = MAXCH < 8 ? MAXCH : 8;
+#pragma unroll
+    for (int k0 = 0; k0 < MAXCH; k0 += B) {
+      uint4 buf[B];
+#pragma unroll
+      for (int k = 0; k < B; ++k)
+        if (k0 + k < nch) buf[k] = src[k0 + k];
+#pragma unroll
+      for (int k = 0; k < B; ++k)
+        if (k0 + k < nch) dst[k0 + k] = buf[k];
+    }
+  }
+}
+
+// ------------------------------------------------------- rules and goals
+// ref:rules.py:147-217 (scalar) / ref:vecenv.py:368-433 (batched).  Slots in
+// stored order, each sees earlier rewrites; the TILE_NEAR family picks the
+// first `a` cell in row-major order with a matching neighbour.
+__device__ void apply_rules(const View& vw, const uint32_t* rules, int nr, int ev, int H, int W, int ar, int ac,
+                            int& pocket) {
+  const int HW = H * W;
+  for (int s = 0; s < nr; ++s) {
+    const uint32_t rw = rules[s];
+    const int kind = rw & 0xff, a = (rw >> 8) & 0xff, b = (rw >> 16) & 0xff, out = rw >> 24;
+    if (kind == 0 || kind > 11 || !((cRuleGate[kind] >> ev) & 1)) continue;
+    if (kind == 1) {  // AGENT_HOLD
+      if (pocket == a) pocket = (out >> 4) == kFloor ? 0 : out;
+    } else if (kind == 2) {  // AGENT_NEAR
+      for (int k = 0; k < 4; ++k) {
+        const int r = ar + near_dr(k), c = ac + near_dc(k);
+        if (r >= 0 && r < H && c >= 0 && c < W && vw.rd(r * W + c) == a) {
+          vw.wr(r * W + c, (uint8_t)out);
+          break;
+        }
+      }
+    } else if (kind >= 8) {  // AGENT_NEAR_{UP,RIGHT,DOWN,LEFT}
+      const int r = ar + dir_dr(kind - 8), c = ac + dir_dc(kind - 8);
+      if (r >= 0 && r < H && c >= 0 && c < W && vw.rd(r * W + c) == a) vw.wr(r * W + c, (uint8_t)out);
+    } else {  // TILE_NEAR (3) / TILE_NEAR_{UP,RIGHT,DOWN,LEFT} (4..7)
+      const int nofs = kind == 3 ? 4 : 1;
+      bool done = false;
+      for (int pos = 0; pos < HW && !done; ++pos) {
+        if (vw.rd(pos) != a) continue;
+        const int r = pos / W, c = pos - (pos / W) * W;
+        for (int k = 0; k < nofs; ++k) {
+          const int nr_ = r + (kind == 3 ? near_dr(k) : dir_dr(kind - 4));
+          const int nc_ = c + (kind == 3 ? near_dc(k) : dir_dc(kind - 4));
+          if (nr_ >= 0 && nr_ < H && nc_ >= 0 && nc_ < W && vw.rd(nr_ * W + nc_) == b) {
+            vw.wr(pos, (uint8_t)out);
+            vw.wr(nr_ * W + nc_, kFloorCode);
+            done = true;
+            break;
+          }
+        }
+      }
+    }
+  }
+}
+
+// ref:goals.py:347-394 / ref:vecenv.py:435-477
+__device__ bool check_goal(const View& vw, uint32_t goal, int ev, int H, int W, int ar, int ac, int pocket) {
+  const int kind = goal & 0xff, a1 = (goal >> 8) & 0xff, a2 = (goal >> 16) & 0xff, a3 = goal >> 24;
+  if (kind == 0 || kind > 14 || !((cGoalGate[kind] >> ev) & 1)) return false;
+  switch (kind) {
+    case 1: return pocket == a1;
+    case 2: return vw.rd(ar * W + ac) == a1;
+    case 5: return ar == a1 && ac == a2;
+    case 6: return a2 < H && a3 < W && vw.rd(a2 * W + a3) == a1;
+    case 3:
+      for (int k = 0; k < 4; ++k) {
+        const int r = ar + near_dr(k), c = ac + near_dc(k);
+        if (r >= 0 && r < H && c >= 0 && c < W && vw.rd(r * W + c) == a1) return true;
+      }
+      return false;
+    case 11: case 12: case 13: case 14: {
+      const int r = ar + dir_dr(kind - 11), c = ac + dir_dc(kind - 11);
+      return r >= 0 && r < H && c >= 0 && c < W && vw.rd(r * W + c) == a1;
+    }
+    default: {  // TILE_NEAR (4) and TILE_NEAR_{UP,RIGHT,DOWN,LEFT} (7..10)
+      const int nofs = kind == 4 ? 4 : 1;
+      for (int pos = 0; pos < H * W; ++pos) {
+        if (vw.rd(pos) != a1) continue;
+        const int r = pos / W, c = pos - (pos / W) * W;
+        for (int k = 0; k < nofs; ++k) {
+          const int nr_ = r + (kind == 4 ? near_dr(k) : dir_dr(kind - 7));
+          const int nc_ = c + (kind == 4 ? near_dc(k) : dir_dc(kind - 7));
+          if (nr_ >= 0 && nr_ < H && nc_ >= 0 && nc_ < W && vw.rd(nr_ * W + nc_) == a2) return true;
+        }
+      }
+      return false;
+    }
+  }
+}
+
+// ------------------------------------------------------- observation
+// exact-integer line of sight, ref:observation.py:46-87
+__device__ bool seg_crosses_cell(int p0r, int p0c, int dr, int dc, int cr, int cc) {
+  int lo_n = 0, lo_d = 1, hi_n = 1, hi_d = 1;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int p0 = k ? p0c : p0r, d = k ? dc : dr, low = 2 * (k ? cc : cr), high = low + 2;
+    if (d == 0) {
+      if (!(low < p0 && p0 < high)) return false;
+      continue;
+    }
+    const int a = low - p0, b = high - p0;
+    int ln, ld, hn, hd;
+    if (d > 0) { ln = a; ld = d; hn = b; hd = d; } else { ln = -b; ld = -d; hn = -a; hd = -d; }
+    if (ln * lo_d > lo_n * ld) { lo_n = ln; lo_d = ld; }
+    if (hn * hi_d < hi_n * hd) { hi_n = hn; hi_d = hd; }
+  }
+  return lo_n * hi_d < hi_n * lo_d;
+}
+
+__device__ bool cell_visible(const View& vw, int W, int r0, int c0, int r1, int c1) {
+  if (r0 == r1 && c0 == c1) return true;
+  const int p0r = 2 * r0 + 1, p0c = 2 * c0 + 1, dr = 2 * (r1 - r0), dc = 2 * (c1 - c0);
+  for (int rr = min(r0, r1); rr <= max(r0, r1); ++rr)
+    for (int cc = min(c0, c1); cc <= max(c0, c1); ++cc) {
+      if ((rr == r0 && cc == c0) || (rr == r1 && cc == c1)) continue;
+      if (!((kOpaque >> (vw.rd(rr * W + cc) >> 4)) & 1)) continue;
+      if (seg_crosses_cell(p0r, p0c, dr, dc, rr, cc)) return false;
+    }
+  return true;
+}
+
+// (v, v, 2) window, row 0 farthest ahead, agent at (v-1, v/2): ref:vecenv.py:481-500
+__device__ void write_obs(const View& vw, uint8_t* dst, int r, int c, int d, int H, int W, int V, bool see) {
+  const int h = V / 2;
+  const int fr = dir_dr(d), fc = dir_dc(d);
+  const int rr = fc, rc = -fr;  // right-hand vector (ref:observation.py:25)
+  uint16_t* o = reinterpret_cast<uint16_t*>(dst);
+  for (int i = 0; i < V; ++i) {
+    const int ahead = V - 1 - i;
+    for (int j = 0; j < V; ++j) {
+      const int lat = j - h;
+      const int wr = r + ahead * fr + lat * rr, wc = c + ahead * fc + lat * rc;
+      uint16_t v = 0;
+      if (wr >= 0 && wr < H && wc >= 0 && wc < W) {
+        if (!see && !cell_visible(vw, W, r, c, wr, wc)) {
+          v = 1 | (1 << 8);  // (UNSEEN, UNSEEN)
+        } else {
+          const int code = vw.rd(wr * W + wc);
+          v = (uint16_t)((code >> 4) | ((code & 15) << 8));
+        }
+      }
+      o[i * V + j] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------- warp-cooperative reset
+struct ResetOut {
+  int r, c, d;
+  uint32_t goal;
+};
+
+struct WarpScratch {
+  uint64_t* wd;   // draw words by free-cell index
+  uint16_t* fc;   // free cells (flat), row-major
+  uint8_t* grid;  // trial grid under construction
+  uint64_t* misc; // 64 words: door words [0,24), agent words [24,26), results [32..)
+};
+
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
+  const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src);
+  const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+// Row-major floor cells of the scratch grid into fc[]; returns their count
+// (the free list of ref:core.py:322-325, built with ballots).
+__device__ int build_free_list(const WarpScratch& ws, int HW, int lane) {
+  int count = 0;
+  for (int base = 0; base < HW; base += 32) {
+    const int i = base + lane;
+    const bool fl = i < HW && (ws.grid[i] >> 4) == kFloor;
+    const uint32_t m = __ballot_sync(0xffffffffu, fl);
+    if (fl) ws.fc[count + __popc(m & ((1u << lane) - 1))] = (uint16_t)i;
+    count += __popc(m);
+  }
+  __syncwarp();
+  return count;
+}
+
+// Philox draw blocks for one env, spread over the lanes: words 0..F-1 of key
+// kc into wd[], 2*nseg door words of kd into misc[0..], agent block of ka into
+// misc[24..27].  ref:rng.py:113-118 (random_words), ref:vecenv.py:235-240.
+__device__ void draw_all(const WarpScratch& ws, int lane, int F, uint64_t kc_hi, uint64_t kc_lo, int nseg,
+                         uint64_t kd_hi, uint64_t kd_lo, uint64_t ka_hi, uint64_t ka_lo) {
+  const int nO = (F + 3) >> 2, nD = (2 * nseg + 3) >> 2;
+  const int jobs = nO + nD + 1;
+  for (int j = lane; j < jobs; j += 32) {
+    uint64_t* dst;
+    Words4 w;
+    if (j < nO) {
+      w = philox((uint64_t)j, 0, kDomDraw, 0, kc_hi, kc_lo);
+      dst = ws.wd + 4 * j;
+    } else if (j < nO + nD) {
+      w = philox((uint64_t)(j - nO), 0, kDomDraw, 0, kd_hi, kd_lo);
+      dst = ws.misc + 4 * (j - nO);
+    } else {
+      w = philox(0, 0, kDomDraw, 0, ka_hi, ka_lo);
+      dst = ws.misc + 24;
+    }
+    dst[0] = w.w0; dst[1] = w.w1; dst[2] = w.w2; dst[3] = w.w3;
+  }
+  __syncwarp();
+}
+
+// Column filter of the port builders: 0 none, 1 col < x, 2 col > x.
+__device__ __forceinline__ bool col_ok(int mode, int cell, int W, int x) {
+  if (mode == 0) return true;
+  const int c = cell % W;
+  return mode == 1 ? c < x : c > x;
+}
+
+// Rank of every (filtered) free cell in the stable argsort of its draw word
+// (ref:core.py:328-333, ref:vecenv.py:261-265: ties broken by index), then
+// place `nobj` objects at ranks 0..nobj-1 and report the cell of rank
+// `spawn_rank`.  Exact counting: rank(f) = #{g : (w_g, g) < (w_f, f)}.
+__device__ void rank_place(const WarpScratch& ws, int lane, int F, int W, int mode, int x, const uint8_t* objs,
+                           int nobj, int spawn_rank) {
+  for (int f = lane; f < F; f += 32) {
+    const int cell = ws.fc[f];
+    if (!col_ok(mode, cell, W, x)) continue;
+    const uint64_t wf = ws.wd[f];
+    int rank = 0;
+    if (mode == 0) {
+      for (int g = 0; g < F; ++g) {
+        const uint64_t wg = ws.wd[g];
+        rank += (wg < wf) | ((wg == wf) & (g < f));
+      }
+    } else {
+      for (int g = 0; g < F; ++g) {
+        const uint64_t wg = ws.wd[g];
+        rank += ((wg < wf) | ((wg == wf) & (g < f))) & col_ok(mode, ws.fc[g], W, x);
+      }
+    }
+    if (rank < nobj) ws.grid[cell] = objs[rank];
+    if (rank == spawn_rank) reinterpret_cast<int*>(ws.misc + 32)[0] = cell;
+  }
+  __syncwarp();
+}
+
+__device__ int count_filtered(const WarpScratch& ws, int lane, int F, int W, int mode, int x) {
+  int n = 0;
+  for (int base = 0; base < F; base += 32) {
+    const int f = base + lane;
+    n += __popc(__ballot_sync(0xffffffffu, f < F && col_ok(mode, ws.fc[f], W, x)));
+  }
+  return n;
+}
+
+// Rebuild one env's trial from the episode key ek: ref:vecenv.py:224-233
+// (ks = split(ek, 0), next state key = split(ek, 1)) and the scenario
+// builders ref:scenarios.py:291-412 (batched: ref:vecenv.py:242-291).
+// Called by all 32 lanes with the same arguments; writes the new grid to
+// `gdst` and returns the new pose / goal on every lane.
+__device__ ResetOut warp_reset(const xmg_env_desc& d, const WarpScratch& ws, int lane, uint64_t ek_hi,
+                               uint64_t ek_lo, const uint32_t* row, uint32_t goal_in, uint8_t* gdst,
+                               uint64_t& st_hi, uint64_t& st_lo) {
+  const int H = d.height, W = d.width, HW = H * W;
+  const int sc = d.scenario;
+  // ks (lane 0) and the next state key (lane 1)
+  Words4 kw = {0, 0, 0, 0};
+  if (lane < 2) kw = philox((uint64_t)lane, 0, kDomSplit, 0, ek_hi, ek_lo);
+  const uint64_t ks_hi = shfl64(kw.w0, 0), ks_lo = shfl64(kw.w1, 0);
+  st_hi = shfl64(kw.w0, 1);
+  st_lo = shfl64(kw.w1, 1);
+  // base cells of this scenario
+  for (int i = lane; i < HW; i += 32) ws.grid[i] = d.base_cells[i];
+  ResetOut res;
+  res.goal = goal_in;
+  if (sc == XMG_SCENARIO_EMPTY) {  // ref:scenarios.py:320-327
+    __syncwarp();
+    for (int i = lane; i < HW; i += 32) gdst[i] = ws.grid[i];
+    res.r = 1; res.c = 1; res.d = 1;
+    res.goal = 2u | ((uint32_t)kGreenGoal << 8);
+    return res;
+  }
+  // k0, k1, k2 = split(ks, 3): doors/wall, cells/objects, agent
+  Words4 sk = {0, 0, 0, 0};
+  if (lane < 3) sk = philox((uint64_t)lane, 0, kDomSplit, 0, ks_hi, ks_lo);
+  const uint64_t k0h = shfl64(sk.w0, 0), k0l = shfl64(sk.w1, 0);
+  const uint64_t k1h = shfl64(sk.w0, 1), k1l = shfl64(sk.w1, 1);
+  const uint64_t k2h = shfl64(sk.w0, 2), k2l = shfl64(sk.w1, 2);
+
+  int wall_col = -1, color = 0;
+  const bool two_rooms = sc == XMG_SCENARIO_DOOR_KEY || sc == XMG_SCENARIO_UNLOCK || sc == XMG_SCENARIO_UNLOCK_PICKUP;
+  if (two_rooms) {  // ref:scenarios.py:341-353, 373-385
+    const Words4 w = philox(0, 0, kDomDraw, 0, k0h, k0l);  // redundant on every lane
+    int door_row;
+    if (sc == XMG_SCENARIO_DOOR_KEY) {
+      wall_col = 2 + (int)(w.w0 % (uint64_t)(W - 4));
+      door_row = 1 + (int)(w.w1 % (uint64_t)(H - 2));
+      color = 7;  // yellow
+    } else {
+      wall_col = (W - 1) / 2;
+      door_row = 1 + (int)(w.w0 % (uint64_t)(H - 2));
+      color = cGenColors[w.w1 % 10];
+    }
+    __syncwarp();
+    for (int r = lane; r < H; r += 32) ws.grid[r * W + wall_col] = kWallCode;
+    __syncwarp();
+    if (lane == 0) ws.grid[door_row * W + wall_col] = (uint8_t)(kLocked * 16 + color);
+  }
+  __syncwarp();
+  const int F = build_free_list(ws, HW, lane);
+  const int nseg = (sc == XMG_SCENARIO_XLAND || sc == XMG_SCENARIO_FOUR_ROOMS) ? d.num_segments : 0;
+  draw_all(ws, lane, F, k1h, k1l, nseg, k0h, k0l, k2h, k2l);
+  // doors: ref:layouts.py:532-544 (segments never hold free cells)
+  if (lane < nseg) {
+    const int off = d.seg_off[lane], len = d.seg_off[lane + 1] - off;
+    const int pos = d.fixed_doors ? len / 2 : (int)(ws.misc[2 * lane] % (uint64_t)len);
+    ws.grid[d.seg_cells[off + pos]] = (uint8_t)(kClosed * 16 + cGenColors[ws.misc[2 * lane + 1] % 10]);
+  }
+  const uint64_t a0 = ws.misc[24], a1 = ws.misc[25];
+  res.d = (int)(a1 & 3);  // a1 % 4
+  uint8_t objs_local[4];
+  if (sc == XMG_SCENARIO_XLAND || sc == XMG_SCENARIO_FOUR_ROOMS || sc == XMG_SCENARIO_EMPTY_RANDOM) {
+    int nobj;
+    const uint8_t* objs;
+    if (sc == XMG_SCENARIO_XLAND) {  // ref:vecenv.py:261-279
+      nobj = (row[1] >> 8) & 0xff;
+      objs = reinterpret_cast<const uint8_t*>(row + 2 + d.rule_width);
+    } else if (sc == XMG_SCENARIO_FOUR_ROOMS) {  // ref:scenarios.py:361-370
+      objs_local[0] = kGreenGoal;
+      objs = objs_local;
+      nobj = 1;
+      res.goal = 2u | ((uint32_t)kGreenGoal << 8);
+    } else {  // EMPTY_RANDOM, ref:scenarios.py:330-338
+      objs = objs_local;
+      nobj = 0;
+      res.goal = 2u | ((uint32_t)kGreenGoal << 8);
+    }
+    const int tail = F - nobj;
+    const int spawn = tail > 0 ? nobj + (int)(a0 % (uint64_t)tail) : -1;
+    rank_place(ws, lane, F, W, 0, 0, objs, nobj, spawn);
+  } else {  // two-room ports: shuffle all free cells, keep the left room
+    const int L = count_filtered(ws, lane, F, W, 1, wall_col);
+    objs_local[0] = (uint8_t)(kKey * 16 + color);
+    const int spawn = L > 1 ? 1 + (int)(a0 % (uint64_t)(L - 1)) : -1;
+    rank_place(ws, lane, F, W, 1, wall_col, objs_local, 1, spawn);
+    if (sc == XMG_SCENARIO_DOOR_KEY) {
+      res.goal = 2u | ((uint32_t)kGreenGoal << 8);
+    } else if (sc == XMG_SCENARIO_UNLOCK) {  // ref:scenarios.py:393-397
+      res.goal = 2u | ((uint32_t)(kOpen * 16 + color) << 8);
+    } else {  // UNLOCK_PICKUP, ref:scenarios.py:400-412: reshuffle with the key placed
+      const int ball = kBall * 16 + cGenColors[ws.wd[2] % 10];
+      const int F2 = build_free_list(ws, HW, lane);  // draw words for indices < F2 are unchanged
+      uint64_t bw = ~0ull;
+      int bg = 0x7fffffff;
+      for (int f = lane; f < F2; f += 32) {
+        if (!col_ok(2, ws.fc[f], W, wall_col)) continue;
+        const uint64_t w = ws.wd[f];
+        if (w < bw || (w == bw && f < bg)) { bw = w; bg = f; }
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        const uint64_t ow = shfl64(bw, (lane + off) & 31);
+        const int og = __shfl_sync(0xffffffffu, bg, (lane + off) & 31);
+        if (ow < bw || (ow == bw && og < bg)) { bw = ow; bg = og; }
+      }
+      if (lane == 0 && bg < F2) ws.grid[ws.fc[bg]] = (uint8_t)ball;
+      res.goal = 1u | ((uint32_t)ball << 8);
+      __syncwarp();
+    }
+  }
+  const int spawn_cell = reinterpret_cast<const int*>(ws.misc + 32)[0];
+  res.r = spawn_cell / W;
+  res.c = spawn_cell - res.r * W;
+  for (int i = lane; i < HW; i += 32) gdst[i] = ws.grid[i];
+  __syncwarp();
+  return res;
+}
+
+// ------------------------------------------------------- the fused step
+__device__ __forceinline__ int load_action(const void* a, int dtype, int64_t e) {
+  switch (dtype) {
+    case XMG_ACT_U8: return reinterpret_cast<const uint8_t*>(a)[e];
+    case XMG_ACT_I32: return reinterpret_cast<const int32_t*>(a)[e];
+    default: return (int)reinterpret_cast<const int64_t*>(a)[e];
+  }
+}
+
+__device__ __forceinline__ uint64_t pack_agent(int r, int c, int d, int pocket, uint32_t sc) {
+  return (uint64_t)(uint32_t)r | ((uint64_t)(uint32_t)c << 8) | ((uint64_t)(uint32_t)d << 16) |
+         ((uint64_t)(uint32_t)pocket << 24) | ((uint64_t)sc << 32);
+}
+
+template <int MAXCH>
+__global__ void __launch_bounds__(kThreads) step_kernel(const xmg_env_desc d, const xmg_state s, const xmg_out o,
+                                                        const void* actions, int act_dtype,
+                                                        const uint64_t* reset_keys, const int32_t* abort_flag,
+                                                        int64_t n) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  if (abort_flag != nullptr && *reinterpret_cast<volatile const int32_t*>(abort_flag) != 0) return;
+
+  const int H = d.height, W = d.width, HW = H * W, V = d.view_size;
+  const Geo geo = make_geo(H, W, V, MAXCH);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t e0 = (int64_t)blockIdx.x * kThreads;
+  const int64_t e = e0 + tid;
+  const bool valid = e < n;
+  const bool reset_mode = reset_keys != nullptr;
+
+  uint8_t* obs_stage = smem;
+  View vw;
+  vw.g = s.grids + (valid ? e : 0) * (int64_t)HW;
+  vw.stage = MAXCH ? smem + kThreads * round16(geo.ob) + tid * geo.stg : nullptr;
+  vw.sbase = vw.slo = vw.shi = 0;
+  uint8_t* wbase = smem + kThreads * round16(geo.ob) + kThreads * geo.stg + warp * geo.ws;
+  WarpScratch ws;
+  ws.wd = reinterpret_cast<uint64_t*>(wbase);
+  ws.fc = reinterpret_cast<uint16_t*>(wbase + 8 * geo.hwp);
+  ws.grid = wbase + 10 * geo.hwp;
+  ws.misc = reinterpret_cast<uint64_t*>(wbase + 11 * geo.hwp);
+
+  // ---- load: agent word (coalesced 8 B) and action
+  uint64_t ag = 0;
+  int act = 1;
+  if (valid) {
+    ag = s.agent[e];
+    if (!reset_mode) act = load_action(actions, act_dtype, e);
+  }
+  int r = (int)(ag & 0xff), c = (int)((ag >> 8) & 0xff), dir = (int)((ag >> 16) & 3);
+  int pocket = (int)((ag >> 24) & 0xff);
+  uint32_t sc = (uint32_t)(ag >> 32);
+
+  float rew = 0.f, disc = 1.f;
+  int8_t stype = 0;
+  bool last = reset_mode;
+
+  if (valid && !reset_mode) {
+    // ---- stage the post-action window (MOVE: both candidate poses)
+    const int nd = act == 1 ? ((dir + 3) & 3) : (act == 2 ? ((dir + 1) & 3) : dir);
+    int lo, hi;
+    window_span(r, c, nd, act == 0 ? 1 : 0, H, W, V, lo, hi);
+    stage_from_global<MAXCH>(vw, lo, hi, HW);
+
+    // ---- action, ref:vecenv.py:306-342 / ref:env.py:148-191
+    const int tr = r + dir_dr(dir), tc = c + dir_dc(dir);
+    const bool inside = tr >= 0 && tr < H && tc >= 0 && tc < W;
+    const int tflat = tr * W + tc;
+    const int tcode = inside ? vw.rd(tflat) : 0, tt = tcode >> 4;
+    int ev = -1;
+    switch (act) {
+      case 0:
+        if (inside && ((kWalkable >> tt) & 1)) { r = tr; c = tc; ev = 0; }
+        break;
+      case 1: dir = nd; break;
+      case 2: dir = nd; break;
+      case 3:
+        if (inside && pocket == 0 && ((kPickable >> tt) & 1)) {
+          pocket = tcode; vw.wr(tflat, kFloorCode); ev = 1;
+        }
+        break;
+      case 4:
+        if (inside && pocket != 0 && tt == kFloor) {
+          vw.wr(tflat, (uint8_t)pocket); pocket = 0; ev = 2;
+        }
+        break;
+      default:
+        if (inside) {
+          const int col = tcode & 15;
+          if (tt == kClosed || (tt == kLocked && pocket == kKey * 16 + col)) {
+            vw.wr(tflat, (uint8_t)(kOpen * 16 + col)); ev = 3;
+          }
+        }
+    }
+    // ---- rules and goal, only after an event (ref:vecenv.py:344-349).
+    // TOGGLE gates no rule and no goal, so it never reaches here.
+    bool goal = false;
+    if (ev >= 0 && ev != 3) {
+      if (d.rule_width > 0) {
+        const uint32_t* row = d.task_rows + (int64_t)s.task[e] * d.row_words;
+        const int nr = row[1] & 0xff;
+        if (nr) apply_rules(vw, row + 2, nr, ev, H, W, r, c, pocket);
+      }
+      goal = check_goal(vw, s.goal[e], ev, H, W, r, c, pocket);
+    }
+    // ---- counters and reward, ref:vecenv.py:351-357 (fp64, no contraction)
+    sc += 1;
+    last = goal || sc >= (uint32_t)d.budget;
+    if (goal) {
+      const double frac = __ddiv_rn((double)sc, (double)d.budget);
+      rew = __double2float_rn(__dsub_rn(1.0, __dmul_rn(0.9, frac)));
+    }
+    disc = last ? 0.f : 1.f;
+    stype = last ? 2 : 1;
+  }
+
+  // ---- auto-reset: every finished env is rebuilt by its whole warp
+  uint32_t rmask = __ballot_sync(0xffffffffu, valid && last);
+  if (rmask) {
+    uint64_t ek_hi = 0, ek_lo = 0;
+    int task = 0;
+    if (valid && last) {
+      const uint64_t* kp = reset_mode ? reset_keys + 2 * e : s.rng + 2 * e;
+      ek_hi = kp[0];
+      ek_lo = kp[1];
+      task = s.task[e];
+    }
+    while (rmask) {
+      const int src = __ffs(rmask) - 1;
+      rmask &= rmask - 1;
+      const uint64_t hi = shfl64(ek_hi, src), lo = shfl64(ek_lo, src);
+      const int t = __shfl_sync(0xffffffffu, task, src);
+      const uint32_t g_in = (d.scenario == XMG_SCENARIO_XLAND) ? d.task_rows[(int64_t)t * d.row_words] : 0u;
+      uint8_t* gdst = s.grids + (e0 + warp * 32 + src) * (int64_t)HW;
+      uint64_t st_hi, st_lo;
+      const ResetOut ro = warp_reset(d, ws, lane, hi, lo, d.task_rows + (int64_t)t * d.row_words, g_in, gdst,
+                                     st_hi, st_lo);
+      if (MAXCH) {
+        // restage the owner's window straight from the scratch grid
+        int lo2, hi2;
+        window_span(ro.r, ro.c, ro.d, 0, H, W, V, lo2, hi2);
+        const uintptr_t gsrc = reinterpret_cast<uintptr_t>(gdst);
+        const int sbase = (int)(((gsrc + lo2) & ~uintptr_t(15)) - gsrc);
+        const int nch = (int)(((gsrc + hi2) - ((gsrc + lo2) & ~uintptr_t(15)) + 15) >> 4);
+        uint8_t* ostage = smem + kThreads * round16(geo.ob) + (warp * 32 + src) * geo.stg;
+        for (int k = lane; k < 16 * nch; k += 32) {
+          const int f = sbase + k;
+          if (f >= 0 && f < HW) ostage[k] = ws.grid[f];
+        }
+        if (lane == src) {
+          vw.sbase = sbase;
+          vw.slo = max(sbase, 0);
+          vw.shi = min(sbase + 16 * nch, HW);
+        }
+      }
+      __syncwarp();
+      if (lane == src) {
+        r = ro.r; c = ro.c; dir = ro.d; pocket = 0; sc = 0;
+        s.rng[2 * e] = st_hi;
+        s.rng[2 * e + 1] = st_lo;
+        s.goal[e] = ro.goal;
+      }
+    }
+  }
+
+  // ---- per-env outputs (coalesced)
+  if (valid) {
+    s.agent[e] = pack_agent(r, c, dir, pocket, sc);
+    o.reward[e] = rew;
+    o.discount[e] = disc;
+    o.step_type[e] = stype;
+  }
+
+  // ---- observation: assembled in smem, one TMA bulk store per CTA
+  if (o.obs != nullptr) {
+    if (valid) write_obs(vw, obs_stage + tid * geo.ob, r, c, dir, H, W, V, d.see_through_walls != 0);
+    const int64_t nvalid = min((int64_t)kThreads, n - e0);
+    const uint32_t bytes = (uint32_t)(nvalid * geo.ob);
+    const uint32_t bulk = bytes & ~15u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    uint8_t* gdst = o.obs + e0 * geo.ob;
+    if (tid == 0 && bulk) {
+      const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(obs_stage);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                   ::"l"(gdst), "r"(saddr), "r"(bulk) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    for (uint32_t k = bulk + tid; k < bytes; k += kThreads) gdst[k] = obs_stage[k];
+    if (tid == 0 && bulk) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
+// ------------------------------------------------------- helper kernels
+__global__ void philox_kernel(const uint64_t* ctr, const uint64_t* key, uint64_t* out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Words4 w = philox(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3], key[2 * i], key[2 * i + 1]);
+  out[4 * i] = w.w0; out[4 * i + 1] = w.w1; out[4 * i + 2] = w.w2; out[4 * i + 3] = w.w3;
+}
+
+// keys[i] = fold_in(root, offset+i, SPLIT)  (ref:rng.py:142-145)
+__global__ void split_batch_kernel(uint64_t hi, uint64_t lo, int64_t offset, int64_t n, uint64_t* keys) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Words4 w = philox((uint64_t)(offset + i), 0, kDomSplit, 0, hi, lo);
+  keys[2 * i] = w.w0;
+  keys[2 * i + 1] = w.w1;
+}
+
+// one thread per (env, 4-word block): actions[t][i] = word(t0+t) % 6
+__global__ void random_actions_kernel(const uint64_t* keys, int64_t n, int64_t t0, int64_t steps, int64_t b0,
+                                      int64_t nblocks, uint8_t* actions) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * nblocks) return;
+  const int64_t i = idx % n, b = b0 + idx / n;
+  const Words4 w = philox((uint64_t)b, 0, kDomDraw, 0, keys[2 * i], keys[2 * i + 1]);
+  const uint64_t ws[4] = {w.w0, w.w1, w.w2, w.w3};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t t = 4 * b + k - t0;
+    if (t >= 0 && t < steps) actions[t * n + i] = (uint8_t)(ws[k] % 6);
+  }
+}
+
+__global__ void validate_kernel(const void* a, int dtype, int64_t n, int32_t* flag) {
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v;
+    switch (dtype) {
+      case XMG_ACT_U8: v = reinterpret_cast<const uint8_t*>(a)[i]; break;
+      case XMG_ACT_I32: v = reinterpret_cast<const int32_t*>(a)[i]; break;
+      default: v = reinterpret_cast<const int64_t*>(a)[i];
+    }
+    bad |= v < 0 || v >= 6;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(flag, 1);
+}
+
+// ------------------------------------------------------- host side
+thread_local std::string g_err;
+
+int fail(const std::string& msg) {
+  g_err = msg;
+  return -1;
+}
+
+int check_launch(const char* what) {
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return fail(std::string(what) + ": " + cudaGetErrorString(err));
+  return 0;
+}
+
+int pick_maxch(const xmg_env_desc* d) {
+  const int need = needed_chunks(d->width, d->view_size);
+  if (need <= 8) return 8;
+  if (need <= 16) return 16;
+  if (need <= 32) return 32;
+  return 0;
+}
+
+template <int MAXCH>
+int launch_step(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
+                const uint64_t* keys, const int32_t* abort_flag, int64_t n, cudaStream_t st) {
+  const Geo geo = make_geo(d->height, d->width, d->view_size, MAXCH);
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(step_kernel<MAXCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  if (attr_err != cudaSuccess) return fail(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+  const int64_t blocks = (n + kThreads - 1) / kThreads;
+  step_kernel<MAXCH><<<(unsigned)blocks, kThreads, (size_t)geo.total, st>>>(*d, *s, *o, actions, dtype, keys,
+                                                                           abort_flag, n);
+  return check_launch("step_kernel");
+}
+
+int validate_desc(const xmg_env_desc* d, int64_t n) {
+  if (!d) return fail("null env description");
+  if (n < 1) return fail("n must be >= 1");
+  if (d->height < 1 || d->height > 255 || d->width < 1 || d->width > 255) return fail("grid size outside [1, 255]");
+  if (d->view_size < 3 || !(d->view_size & 1)) return fail("view_size must be odd and >= 3");
+  if (d->scenario < 0 || d->scenario > 6) return fail("unknown scenario");
+  if (d->num_segments > 12) return fail("too many door segments");
+  if (!d->base_cells || !d->task_rows) return fail("null base_cells / task_rows");
+  const Geo geo = make_geo(d->height, d->width, d->view_size, pick_maxch(d));
+  if (geo.total > 227 * 1024)
+    return fail("grid too large for the shared-memory reset scratch of this build (H*W <= ~4000)");
+  return 0;
+}
+
+int dispatch_step(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
+                  const uint64_t* keys, const int32_t* abort_flag, int64_t n, cudaStream_t st) {
+  switch (pick_maxch(d)) {
+    case 8: return launch_step<8>(d, s, o, actions, dtype, keys, abort_flag, n, st);
+    case 16: return launch_step<16>(d, s, o, actions, dtype, keys, abort_flag, n, st);
+    case 32: return launch_step<32>(d, s, o, actions, dtype, keys, abort_flag, n, st);
+    default: return launch_step<0>(d, s, o, actions, dtype, keys, abort_flag, n, st);
+  }
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+int32_t xmg_abi_version(void) { return XMG_ABI_VERSION; }
+
+const char* xmg_last_error(void) { return g_err.c_str(); }
+
+void xmg_philox_host(const uint64_t ctr[4], uint64_t k0, uint64_t k1, uint64_t out[4]) {
+  philox_host(ctr, k0, k1, out);
+}
+
+void xmg_key_from_seed(uint64_t seed_lo, uint64_t seed_hi, uint64_t* out2) {
+  const uint64_t ctr[4] = {seed_lo, seed_hi, kDomSeed, 0};
+  uint64_t w[4];
+  philox_host(ctr, 0, 0, w);
+  out2[0] = w[0];
+  out2[1] = w[1];
+}
+
+void xmg_fold_in(uint64_t hi, uint64_t lo, uint64_t data, int32_t domain, uint64_t* out2) {
+  const uint64_t ctr[4] = {data, 0, (uint64_t)domain, 0};
+  uint64_t w[4];
+  philox_host(ctr, hi, lo, w);
+  out2[0] = w[0];
+  out2[1] = w[1];
+}
+
+int32_t xmg_philox(const uint64_t* ctr, const uint64_t* key, uint64_t* out, int64_t n, void* stream) {
+  if (n <= 0) return 0;
+  philox_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(ctr, key, out, n);
+  return check_launch("philox_kernel");
+}
+
+int32_t xmg_split_batch(uint64_t root_hi, uint64_t root_lo, int64_t offset, int64_t n, uint64_t* keys,
+                        void* stream) {
+  if (n <= 0) return 0;
+  split_batch_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(root_hi, root_lo, offset, n,
+                                                                                     keys);
+  return check_launch("split_batch_kernel");
+}
+
+int32_t xmg_random_actions(const uint64_t* keys, int64_t n, int64_t t0, int64_t steps, uint8_t* actions,
+                           void* stream) {
+  if (n <= 0 || steps <= 0) return 0;
+  if (t0 < 0) return fail("t0 must be >= 0");
+  const int64_t b0 = t0 / 4, b1 = (t0 + steps - 1) / 4;
+  const int64_t nb = b1 - b0 + 1, total = n * nb;
+  random_actions_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(keys, n, t0, steps, b0,
+                                                                                          nb, actions);
+  return check_launch("random_actions_kernel");
+}
+
+int32_t xmg_validate_actions(const void* actions, int32_t dtype, int64_t n, int32_t* flag, void* stream) {
+  if (n <= 0) return 0;
+  if (dtype < 0 || dtype > 2) return fail("unknown action dtype");
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 8);
+  validate_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(actions, dtype, n, flag);
+  return check_launch("validate_kernel");
+}
+
+int32_t xmg_reset(const xmg_env_desc* desc, const xmg_state* state, const uint64_t* keys, int64_t n,
+                  const xmg_out* out, void* stream) {
+  if (validate_desc(desc, n)) return -1;
+  if (!state || !out || !keys) return fail("null state/out/keys");
+  return dispatch_step(desc, state, out, nullptr, 0, keys, nullptr, n, (cudaStream_t)stream);
+}
+
+int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* actions, int32_t action_dtype,
+                 int64_t n, const xmg_out* out, const int32_t* abort_flag, void* stream) {
+  if (validate_desc(desc, n)) return -1;
+  if (!state || !out || !actions) return fail("null state/out/actions");
+  if (action_dtype < 0 || action_dtype > 2) return fail("unknown action dtype");
+  return dispatch_step(desc, state, out, actions, action_dtype, nullptr, abort_flag, n, (cudaStream_t)stream);
+}
+
+int64_t xmg_step_smem_bytes(const xmg_env_desc* desc) {
+  if (!desc) return -1;
+  return make_geo(desc->height, desc->width, desc->view_size, pick_maxch(desc)).total;
+}
+
+}  // extern "C"

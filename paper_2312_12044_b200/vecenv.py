@@ -1,0 +1,354 @@
+"""VecEnv: the reference's batched operator API over the sm_100a kernels.
+
+Drop-in for ``rulegrid.VecEnv`` (ref vecenv.py:108-521):
+  VecEnv(params, num_envs, rulesets)      ref :117-151
+  .reset(key) / .reset_with_keys(k0, k1)   ref :201-222
+  .step(actions, compute_obs)             ref :295-364  -> VecTimeStep
+  .env_state(i)                           ref :511-521
+State lives in HBM as structure-of-arrays torch tensors (layout in
+include/xmg.h); every call is one asynchronous launch of libxmg.so on the
+current CUDA stream.  Differences from the reference, by design:
+  * outputs are CUDA tensors; rewards / discounts are float32 (the reward is
+    evaluated in fp64 without contraction and rounded once, so it equals
+    ``np.float32`` of the reference's float64 bit for bit);
+  * actions given as a CUDA tensor are range-checked on the device: an
+    invalid batch mutates no env and raises ``InvalidAction`` at the next
+    ``check()`` (immediately with ``strict=True``); host (NumPy / list)
+    actions are checked on the host before anything is launched, exactly
+    like the reference.
+There is no CPU fallback: without libxmg.so or a GPU every call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import (AgentState, Direction, GridFull, Grid, InvalidAction, Key, Position, DOMAIN_FOLD, fold_in,
+                   key_from_seed)
+from .env import EnvParams, StepType
+from .layouts import Layout, bordered, plan_layout
+from .ruleset import Benchmark, Ruleset, TaskTable, pack_rulesets
+
+GRID_PAD = 64  # the step kernel reads 16-byte aligned chunks past the last grid
+
+
+def _stream(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _device(device) -> torch.device:
+    if device is None:
+        if not torch.cuda.is_available():
+            raise _lib.NativeLibraryError("VecEnv needs a CUDA device (B200); there is no CPU fallback")
+        return torch.device("cuda", torch.cuda.current_device())
+    d = torch.device(device)
+    if d.type != "cuda":
+        raise _lib.NativeLibraryError("VecEnv state must live on a CUDA device; there is no CPU fallback")
+    return d
+
+
+def u64_to_i64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint64)).view(np.int64)
+
+
+# ------------------------------------------------------------ batched keys
+def split_batch(key: Key, num: int, offset: int = 0, device=None) -> torch.Tensor:
+    """(num, 2) int64 tensor (u64 bit patterns hi, lo) of
+    fold_in(key, offset + i, SPLIT): ref split_batch rng.py:142-145."""
+    dev = _device(device)
+    out = torch.empty((num, 2), dtype=torch.int64, device=dev)
+    _lib.check(_lib.lib().xmg_split_batch(key[0], key[1], offset, num, out.data_ptr(), _stream(dev)),
+               "xmg_split_batch")
+    return out
+
+
+def policy_keys(key: Key, num: int, offset: int = 0, device=None) -> torch.Tensor:
+    """(num, 2) keys fold_in(key, offset + i) (FOLD domain): the per-env
+    random-policy streams of ref tests/test_vecenv.py:126-129."""
+    dev = _device(device)
+    h = np.array([fold_in(key, offset + i, DOMAIN_FOLD) for i in range(num)], dtype=np.uint64) if num <= 4096 \
+        else None
+    if h is not None:
+        return torch.from_numpy(h.view(np.int64)).to(dev)
+    # large batches: derive on the device via the philox KAT kernel
+    ctr = np.zeros((num, 4), np.uint64)
+    ctr[:, 0] = np.arange(offset, offset + num, dtype=np.uint64)
+    ctr[:, 2] = DOMAIN_FOLD
+    kk = np.tile(np.array([key[0], key[1]], np.uint64), (num, 1))
+    ctr_t = torch.from_numpy(ctr.view(np.int64)).to(dev)
+    key_t = torch.from_numpy(kk.view(np.int64)).to(dev)
+    out = torch.empty((num, 4), dtype=torch.int64, device=dev)
+    _lib.check(_lib.lib().xmg_philox(ctr_t.data_ptr(), key_t.data_ptr(), out.data_ptr(), num, _stream(dev)),
+               "xmg_philox")
+    return out[:, :2].contiguous()
+
+
+def random_actions(keys: torch.Tensor, t0: int, steps: int) -> torch.Tensor:
+    """(steps, n) uint8: word (t0+t) of each key's draw stream mod 6, the
+    random policy of ref harness.py:269-275 evaluated on the GPU."""
+    n = keys.shape[0]
+    out = torch.empty((steps, n), dtype=torch.uint8, device=keys.device)
+    _lib.check(_lib.lib().xmg_random_actions(keys.data_ptr(), n, t0, steps, out.data_ptr(), _stream(keys.device)),
+               "xmg_random_actions")
+    return out
+
+
+def philox(ctr: torch.Tensor, key: torch.Tensor) -> torch.Tensor:
+    """Batched Philox4x64-10 blocks on the device (KAT hook)."""
+    n = ctr.shape[0]
+    out = torch.empty((n, 4), dtype=torch.int64, device=ctr.device)
+    _lib.check(_lib.lib().xmg_philox(ctr.data_ptr(), key.data_ptr(), out.data_ptr(), n, _stream(ctr.device)),
+               "xmg_philox")
+    return out
+
+
+# ------------------------------------------------------------ records
+@dataclass(eq=False)
+class VecTimeStep:
+    observations: torch.Tensor | None  # (N, v, v, 2) uint8
+    rewards: torch.Tensor              # (N,) float32
+    discounts: torch.Tensor            # (N,) float32
+    step_types: torch.Tensor           # (N,) int8
+
+    def last(self) -> torch.Tensor:
+        return self.step_types == int(StepType.LAST)
+
+    def numpy(self) -> tuple:
+        return (None if self.observations is None else self.observations.cpu().numpy(),
+                self.rewards.cpu().numpy(), self.discounts.cpu().numpy(), self.step_types.cpu().numpy())
+
+
+@dataclass(frozen=True)
+class EnvState:
+    grid: Grid
+    agent: AgentState
+    ruleset: Ruleset
+    step_count: int
+    goal_reached: bool
+    rng: Key
+
+
+# ------------------------------------------------------------ VecEnv
+class VecEnv:
+    def __init__(self, params: EnvParams, num_envs: int, rulesets=None, *, device=None, task_ids=None,
+                 strict: bool = False, global_offset: int = 0, reuse_outputs: bool = False):
+        if num_envs < 1:
+            raise ValueError(f"num_envs must be >= 1, got {num_envs}")
+        self.params = params
+        self.num_envs = n = num_envs
+        self.device = dev = _device(device)
+        self.strict = strict
+        self.global_offset = global_offset
+        self.reuse_outputs = reuse_outputs
+        h, w, v = params.height, params.width, params.view_size
+        self._hw = h * w
+        scen = _lib.SCENARIO_IDS[params.scenario]
+
+        # -- tasks: a device table plus one row index per env
+        self._tasks: list[Ruleset] | None = None
+        self._benchmark: Benchmark | None = None
+        if rulesets is None or isinstance(rulesets, Ruleset):
+            task = params.ruleset if rulesets is None else rulesets
+            table = pack_rulesets([task])
+            ids = np.zeros(n, np.int32)
+            self._tasks = [task] * n
+        elif isinstance(rulesets, (Benchmark, TaskTable)):
+            table = rulesets.task_table() if isinstance(rulesets, Benchmark) else rulesets
+            self._benchmark = rulesets if isinstance(rulesets, Benchmark) else None
+            if task_ids is None:
+                ids = ((np.arange(n, dtype=np.int64) + global_offset) % table.num_tasks).astype(np.int32)
+            else:
+                ids = np.asarray(task_ids.cpu() if isinstance(task_ids, torch.Tensor) else task_ids, np.int64)
+                if ids.shape != (n,) or ids.min() < 0 or ids.max() >= table.num_tasks:
+                    raise ValueError("task_ids must be (num_envs,) rows of the table")
+                ids = ids.astype(np.int32)
+        else:
+            tasks = list(rulesets)
+            if len(tasks) != n:
+                raise ValueError(f"{len(tasks)} rulesets for {n} envs")
+            uniq: dict[int, int] = {}
+            order: list[Ruleset] = []
+            ids = np.empty(n, np.int32)
+            for i, t in enumerate(tasks):
+                j = uniq.setdefault(id(t), len(order))
+                if j == len(order):
+                    order.append(t)
+                ids[i] = j
+            table = pack_rulesets(order)
+            self._tasks = tasks
+        self.table = table
+
+        # -- static geometry of the scenario
+        seg_off = np.zeros(1, np.int16)
+        seg_cells = np.zeros(1, np.int16)
+        fixed = 0
+        if scen in (0, 4):  # xland / four_rooms: room layout with door segments
+            plan = plan_layout(Layout.R4 if scen == 4 else params.layout, h, w)
+            base = plan.base_cells()
+            seg_off, seg_cells = plan.segment_arrays()
+            fixed = int(plan.fixed_doors)
+            nseg = len(plan.door_segments)
+            free = int(((base >> 4) == 3).sum())
+            used_obj = int(((table.rows[ids, 1] >> 8) & 0xFF).max()) if scen == 0 else 1
+            if used_obj >= free:  # ref vecenv.py:171-175
+                raise GridFull(f"{used_obj} objects on {free} free cells")
+        else:
+            base = bordered(h, w, goal=scen in (1, 2, 3))
+            nseg = 0
+        if scen != 0:
+            table = TaskTable(np.zeros((1, 2), np.uint32), 0, 0, 0)  # ports bring their own goal, no rules
+            ids = np.zeros(n, np.int32)
+        self._ids_host = ids
+
+        # -- device buffers
+        self._base = torch.from_numpy(base.copy()).to(dev)
+        self._seg_off = torch.from_numpy(seg_off.astype(np.int16)).to(dev)
+        self._seg_cells = torch.from_numpy(seg_cells.astype(np.int16)).to(dev)
+        self._table = torch.from_numpy(table.rows.view(np.int32).copy()).to(dev)
+        self.grids_flat = torch.zeros(n * self._hw + GRID_PAD, dtype=torch.uint8, device=dev)
+        self.agent = torch.zeros(n, dtype=torch.int64, device=dev)
+        self.rng = torch.zeros((n, 2), dtype=torch.int64, device=dev)
+        self.task = torch.from_numpy(ids).to(dev)
+        goals = table.rows[ids, 0] if scen == 0 else np.zeros(n, np.uint32)
+        self.goal = torch.from_numpy(goals.view(np.int32).copy()).to(dev)
+        self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._flag_checked = True
+
+        self._desc = _lib.EnvDesc(h, w, v, params.step_budget, scen, int(params.see_through_walls), nseg, fixed,
+                                  table.rule_width if scen == 0 else 0, table.obj_width, table.row_words,
+                                  table.num_tasks, self._base.data_ptr(), self._seg_off.data_ptr(),
+                                  self._seg_cells.data_ptr(), self._table.data_ptr())
+        self._state = _lib.State(self.grids_flat.data_ptr(), self.agent.data_ptr(), self.rng.data_ptr(),
+                                 self.goal.data_ptr(), self.task.data_ptr())
+        if _lib.lib().xmg_step_smem_bytes(C.byref(self._desc)) > 227 * 1024:
+            raise _lib.NativeLibraryError(f"{h}x{w} grids exceed the shared-memory budget of this build")
+        self._outs = None
+        self.launches = 0  # kernels of ours launched by this VecEnv
+
+    # -- views
+    @property
+    def grids(self) -> torch.Tensor:
+        return self.grids_flat[: self.num_envs * self._hw].view(self.num_envs, self._hw)
+
+    def agent_fields(self) -> torch.Tensor:
+        """(N, 5) int64: row, col, dir, pocket, step_count."""
+        a = self.agent
+        return torch.stack([a & 0xFF, (a >> 8) & 0xFF, (a >> 16) & 0xFF, (a >> 24) & 0xFF,
+                            (a >> 32) & 0xFFFFFFFF], dim=1)
+
+    # -- outputs
+    def _alloc_out(self, compute_obs: bool):
+        n, v, dev = self.num_envs, self.params.view_size, self.device
+        if self.reuse_outputs and self._outs is not None and (self._outs[0] is not None) == compute_obs:
+            return self._outs
+        obs = torch.empty((n, v, v, 2), dtype=torch.uint8, device=dev) if compute_obs else None
+        outs = (obs, torch.empty(n, dtype=torch.float32, device=dev), torch.empty(n, dtype=torch.float32, device=dev),
+                torch.empty(n, dtype=torch.int8, device=dev))
+        if self.reuse_outputs:
+            self._outs = outs
+        return outs
+
+    @staticmethod
+    def _out_struct(outs) -> _lib.Out:
+        return _lib.Out(_ptr(outs[0]), _ptr(outs[1]), _ptr(outs[2]), _ptr(outs[3]))
+
+    # -- reset
+    def reset(self, key: Key, compute_obs: bool = True) -> VecTimeStep:
+        keys = split_batch(key, self.num_envs, self.global_offset, self.device)
+        self.launches += 1
+        return self._reset_keys(keys, compute_obs)
+
+    def reset_with_keys(self, k0, k1, compute_obs: bool = True) -> VecTimeStep:
+        if isinstance(k0, torch.Tensor):
+            keys = torch.stack([k0.to(self.device, torch.int64), k1.to(self.device, torch.int64)], dim=1)
+        else:
+            k0 = np.asarray(k0)
+            k1 = np.asarray(k1)
+            if k0.shape != (self.num_envs,) or k1.shape != (self.num_envs,):
+                raise ValueError(f"expected {self.num_envs} key pairs")
+            keys = torch.from_numpy(np.stack([u64_to_i64(k0), u64_to_i64(k1)], axis=1)).to(self.device)
+        if keys.shape != (self.num_envs, 2):
+            raise ValueError(f"expected {self.num_envs} key pairs")
+        return self._reset_keys(keys.contiguous(), compute_obs)
+
+    def _reset_keys(self, keys: torch.Tensor, compute_obs: bool) -> VecTimeStep:
+        outs = self._alloc_out(compute_obs)
+        o = self._out_struct(outs)
+        _lib.check(_lib.lib().xmg_reset(C.byref(self._desc), C.byref(self._state), keys.data_ptr(), self.num_envs,
+                                        C.byref(o), _stream(self.device)), "xmg_reset")
+        self.launches += 1
+        return VecTimeStep(*outs)
+
+    # -- step
+    def step(self, actions, compute_obs: bool = True, validate: bool = True) -> VecTimeStep:
+        n = self.num_envs
+        flag_ptr = None
+        if isinstance(actions, torch.Tensor) and actions.is_cuda:
+            if actions.shape != (n,):
+                raise InvalidAction(f"expected {n} actions, got shape {tuple(actions.shape)}")
+            if actions.dtype == torch.uint8:
+                dt = _lib.ACT_U8
+            elif actions.dtype == torch.int32:
+                dt = _lib.ACT_I32
+            else:
+                actions = actions.to(torch.int64)
+                dt = _lib.ACT_I64
+            actions = actions.contiguous()
+            if validate:
+                self._flag.zero_()
+                _lib.check(_lib.lib().xmg_validate_actions(actions.data_ptr(), dt, n, self._flag.data_ptr(),
+                                                           _stream(self.device)), "xmg_validate_actions")
+                self.launches += 1
+                flag_ptr = self._flag.data_ptr()
+                self._flag_checked = False
+        else:
+            a = np.asarray(actions)
+            if a.shape != (n,):
+                raise InvalidAction(f"expected {n} actions, got shape {a.shape}")
+            if ((a < 0) | (a >= 6)).any():
+                raise InvalidAction("action outside [0, 5]")
+            actions = torch.from_numpy(a.astype(np.uint8)).to(self.device)
+            dt = _lib.ACT_U8
+        outs = self._alloc_out(compute_obs)
+        o = self._out_struct(outs)
+        _lib.check(_lib.lib().xmg_step(C.byref(self._desc), C.byref(self._state), actions.data_ptr(), dt, n,
+                                       C.byref(o), flag_ptr, _stream(self.device)), "xmg_step")
+        self.launches += 1
+        if self.strict and flag_ptr is not None:
+            self.check()
+        return VecTimeStep(*outs)
+
+    def check(self) -> None:
+        """Raise InvalidAction if a device-validated batch was rejected (syncs)."""
+        if not self._flag_checked:
+            bad = int(self._flag.item())
+            self._flag_checked = True
+            if bad:
+                raise InvalidAction("action outside [0, 5]; the batch was not applied")
+
+    # -- inspection
+    def ruleset_of(self, i: int) -> Ruleset:
+        if self._tasks is not None:
+            return self._tasks[i]
+        if self._benchmark is not None:
+            return self._benchmark.get_ruleset(int(self._ids_host[i]))
+        return Ruleset()
+
+    def env_state(self, i: int) -> EnvState:
+        """The i-th env as a scalar EnvState (ref vecenv.py:511-521)."""
+        g = self.grids[i].cpu().numpy().tobytes()
+        a = int(self.agent[i].item()) & ((1 << 64) - 1)
+        k = self.rng[i].cpu().numpy().view(np.uint64)
+        agent = AgentState(Position(a & 0xFF, (a >> 8) & 0xFF), Direction((a >> 16) & 3), (a >> 24) & 0xFF)
+        return EnvState(Grid(self.params.height, self.params.width, g), agent, self.ruleset_of(i),
+                        (a >> 32) & 0xFFFFFFFF, False, Key(int(k[0]), int(k[1])))
