@@ -1,0 +1,360 @@
+"""Benchmark: env-steps/s of the batched XLand-MiniGrid step on B200.
+
+Contract (one JSON line on rank 0):
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3]
+Under torchrun (N > 1) each rank owns a contiguous global env range (weak
+scaling, no per-step communication); one NCCL all-reduce of the episode
+statistics runs after the timed window, and the reported time is the max over
+ranks of the device-timed window.
+
+Workload (default "c3", BASELINE.json configs[2]): XLand-MiniGrid-R4-13x13
+with medium-style rulesets (data/medium-65536.xmgb, reference generator,
+seed 42; env i runs row i mod M), 2^20 envs per GPU, random policy (Philox
+word t of fold_in(key_from_seed(1), i) mod 6), auto-reset on.  A step is one
+VecEnv.step over the whole batch (validate + fused step kernel).  Inputs
+(state 0.22 GB/GPU + actions) exceed the 126 MB L2.  The timed window always
+contains the synchronized budget auto-reset burst (t = 507): when K < 507 it
+is placed to straddle it, which weights resets MORE than steady state.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+WORKLOADS = {
+    # name: (env id, benchmark config or None, envs per GPU, BASELINE.json config text)
+    "c1": ("MiniGrid-Empty-8x8", None, 1024, "MiniGrid-Empty-8x8 random-policy rollout, 1024 envs"),
+    "c2": ("XLand-MiniGrid-R1-9x9", "trivial", 1 << 16, "XLand-MiniGrid-R1-9x9 trivial-style, 2^16 envs"),
+    "c3": ("XLand-MiniGrid-R4-13x13", "medium", 1 << 20, "XLand-MiniGrid-R4-13x13 medium-style, 2^20 envs/GPU"),
+    "c4": ("XLand-MiniGrid-R9-25x25", "high", 1 << 19, "XLand-MiniGrid-R9-25x25 high-style, 2^19 envs/GPU"),
+    "doorkey": ("MiniGrid-DoorKey-8x8", None, 1 << 20, "MiniGrid-DoorKey-8x8, 2^20 envs/GPU"),
+}
+METRIC = "env-steps/sec (random policy, auto-reset)"
+
+
+def algorithmic_bytes(h: int, w: int, rules: int, v: int) -> int:
+    """grid + agent in/out + goal + rule slots + action + obs
+    + reward + discount + step type, bytes per env-step."""
+    return h * w + 6 + 6 + 4 + 4 * rules + 1 + 2 * v * v + 4 + 4 + 1
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if "Active" in s[3 + k]
+                          and not s[3 + k].startswith("Not")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def make_workload(name: str, device, n: int, offset: int):
+    from helpers import benchmark_file
+    from paper_2312_12044_b200 import VecEnv, load_benchmark, make
+    env_id, config, _, _ = WORKLOADS[name]
+    _, params = make(env_id)
+    bm = load_benchmark(benchmark_file(config)) if config else None
+    vec = VecEnv(params, n, bm, device=device, global_offset=offset, reuse_outputs=True)
+    return params, bm, vec
+
+
+def cpu_reference(name: str, n_sample: int, steps: int, threads: int, budget_s: float = 20.0) -> dict:
+    """The oracle port (oracle/xmg_oracle.c, OpenMP) on host cores: the same
+    workload restricted to `n_sample` envs, stepping until `steps` steps or
+    `budget_s` seconds.  Returns env-steps/s."""
+    from helpers import benchmark_file, oracle_from_table
+    from oracle import oracle as O
+    from paper_2312_12044_b200 import make
+    from paper_2312_12044_b200.ruleset import TaskTable, load_benchmark
+    env_id, config, _, _ = WORKLOADS[name]
+    _, params = make(env_id)
+    if config:
+        table = load_benchmark(benchmark_file(config)).task_table()
+    else:
+        table = TaskTable(np.zeros((1, 4), np.uint32), 0, 0, 0)
+    ids = (np.arange(n_sample) % table.num_tasks).astype(np.int64)
+    ora = oracle_from_table(params, table, ids, threads)
+    root = O.key_from_seed(0)
+    ora.reset(root)
+    keys = [O.fold_in(O.key_from_seed(1), i) for i in range(n_sample)]
+    pk0 = np.array([k[0] for k in keys], np.uint64)
+    pk1 = np.array([k[1] for k in keys], np.uint64)
+    done, t0 = 0, time.perf_counter()
+    chunk = 16
+    while done < steps and time.perf_counter() - t0 < budget_s:
+        ora.rollout_random(pk0, pk1, done, min(chunk, steps - done), compute_obs=True)
+        done += min(chunk, steps - done)
+    el = time.perf_counter() - t0
+    return {"value": n_sample * done / el, "steps": done, "envs": n_sample, "seconds": el}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    env_id, config, n_gpu, desc = WORKLOADS[args.workload]
+    threads = os.cpu_count() or 1
+    n_sample = min(n_gpu, 1 << 16)
+    r = cpu_reference(args.workload, n_sample, max(args.steps, 1), threads, budget_s=30.0)
+    value = r["value"]
+    sample = f"{r['envs']} envs x {r['steps']} steps of the {desc} workload ({r['seconds']:.1f} s)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": args.gpus,
+        "steps": r["steps"], "warmup": 0, "ms_per_step": 1e3 * r["envs"] / value, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": desc, "env": env_id, "rulesets": config, "envs_per_gpu": n_gpu},
+        "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference arm = CPU oracle port of rulegrid.VecEnv (oracle/xmg_oracle.c, OpenMP over host "
+                "threads); the Python reference cannot travel to the GPU box",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def load_traffic(kernel_key: str):
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get(kernel_key)
+    except Exception:
+        return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2312_12044_b200 import key_from_seed, policy_keys, random_actions
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    env_id, config, n, desc = WORKLOADS[args.workload]
+    if args.envs:
+        n = args.envs
+    offset = rank * n
+    params, bm, vec = make_workload(args.workload, dev, n, offset)
+    budget = params.step_budget
+    K, W = args.steps, args.warmup
+    pre = max(0, (budget - 1) - K // 2 - W) if K < budget else 0
+    total = W + pre + K
+    stream = torch.cuda.current_stream(dev)
+
+    vec.reset(key_from_seed(0))
+    pkeys = policy_keys(key_from_seed(1), n, offset=offset, device=dev)
+    actions = random_actions(pkeys, 0, total)
+    stats = vec.enable_stats()
+    for t in range(W + pre):
+        vec.step(actions[t])
+    torch.cuda.synchronize(dev)
+
+    # ---- timed window: K public-API steps, device-resident inputs
+    l0 = vec.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index if dev.index is not None else 0) as clocks:
+        ev0.record(stream)
+        for t in range(W + pre, total):
+            vec.step(actions[t])
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = vec.launches - l0
+    ms = ev0.elapsed_time(ev1)
+    vec.check()
+    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms_max = float(t_max.item())
+    value = n * world * K / (ms_max / 1e3)
+
+    # ---- episode statistics: the single collective (NCCL all-reduce, ~24 B)
+    tot = vec.episode_stats()
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    tot = tot.cpu().numpy()
+
+    # ---- dominant kernel alone: per-launch CUDA events on the launching stream
+    # (a fresh env at the same phase, validate off so only step_kernel runs)
+    params2, _, vec2 = make_workload(args.workload, dev, n, offset)
+    vec2.reset(key_from_seed(0))
+    for t in range(W + pre):
+        vec2.step(actions[t], validate=False)
+    torch.cuda.synchronize(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for i, t in enumerate(range(W + pre, total)):
+        evs[i][0].record(stream)
+        vec2.step(actions[t], validate=False)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    kms = [a.elapsed_time(b) for a, b in evs]
+    kern_ms = sum(kms) / len(kms)
+    del vec2
+    rules = vec.table.rule_width if params.scenario == "xland" else 0
+    bpe = algorithmic_bytes(params.height, params.width, rules, params.view_size)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = bpe * n / (kern_ms / 1e3) / 1e9
+    traffic = load_traffic(f"{args.workload}:step_kernel")
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": (traffic * n if traffic is not None else None),
+                "kernel": "step_kernel", "kernel_ms": kern_ms, "bytes_per_env_step": bpe,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+                "traffic_note": "ncu dram__bytes_read.sum+write.sum per launch (profiles/ncu_summary.json)"}
+
+    # ---- e2e through the public API with HOST buffers (pinned), per step:
+    # H2D of the step's actions, the step, D2H of the whole VecTimeStep.
+    e2e = None
+    if not args.no_e2e:
+        params3, _, vec3 = make_workload(args.workload, dev, n, offset)
+        vec3.reset(key_from_seed(0))
+        ke = min(K, args.e2e_steps)
+        host_actions = actions[W + pre: W + pre + ke].cpu().pin_memory()
+        v = params3.view_size
+        slots = [(torch.empty((n, v, v, 2), dtype=torch.uint8).pin_memory(),
+                  torch.empty(n, dtype=torch.float32).pin_memory(), torch.empty(n, dtype=torch.float32).pin_memory(),
+                  torch.empty(n, dtype=torch.int8).pin_memory()) for _ in range(2)]
+        done_ev = [torch.cuda.Event(), torch.cuda.Event()]
+        dev_act = torch.empty(n, dtype=torch.uint8, device=dev)
+        checksum = 0.0
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for t in range(ke):
+            s = t & 1
+            if t >= 2:  # the host consumes step t-2's record before reusing its buffers
+                done_ev[s].synchronize()
+                checksum += float(slots[s][1][0])
+            dev_act.copy_(host_actions[t], non_blocking=True)
+            ts = vec3.step(dev_act)
+            slots[s][0].copy_(ts.observations, non_blocking=True)
+            slots[s][1].copy_(ts.rewards, non_blocking=True)
+            slots[s][2].copy_(ts.discounts, non_blocking=True)
+            slots[s][3].copy_(ts.step_types, non_blocking=True)
+            done_ev[s].record(stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = e0.elapsed_time(e1)
+        te = torch.tensor([ems], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n * world * ke / (float(te.item()) / 1e3), "unit": "env-steps/s",
+               "h2d_bytes_per_step": n, "d2h_bytes_per_step": n * (2 * v * v + 4 + 4 + 1), "steps": ke,
+               "api": "VecEnv.step with pinned host actions in, full VecTimeStep out (double-buffered)"}
+        del vec3
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r = cpu_reference(args.workload, min(n, 1 << 14), 1024, os.cpu_count() or 1, budget_s=15.0)
+        cpu = {"value": r["value"], "unit": "env-steps/s", "cores": os.cpu_count() or 1, "kind": "port",
+               "sample": f"{r['envs']} envs x {r['steps']} steps of the same workload on the host "
+                         f"({r['seconds']:.1f} s, OpenMP over all host threads)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic",
+            "config": {"workload": desc, "env": env_id, "rulesets": f"data/{config}-65536.xmgb" if config else None,
+                       "envs_per_gpu": n, "global_envs": n * world, "parallelism": f"env-shard x{world}",
+                       "timed_window": f"steps [{W + pre}, {total}) incl. budget reset burst at t={budget}",
+                       "l2": "inputs larger than L2" if n * params.height * params.width > 126e6
+                             else "state resident in L2 (small workload)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "episode_stats": {"return_sum": float(tot[0]), "trials": float(tot[1]), "length_sum": float(tot[2])},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1024)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--envs", type=int, default=0, help="override envs per GPU")
+    ap.add_argument("--e2e-steps", type=int, default=256)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

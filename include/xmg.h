@@ -28,7 +28,8 @@
  * Task table (read-only), u32 [num_tasks][row_words]:
  *   word 0 = goal, word 1 = rule_count | obj_count<<8,
  *   words 2..2+R-1 = active rules (kind, in_a, in_b, out) left-packed,
- *   then ceil(O/4) words of active object codes, left-packed.
+ *   then ceil(O/4) words of active object codes, left-packed; rows are
+ *   padded to a multiple of 4 words (16-byte aligned 128-bit loads).
  */
 #ifndef XMG_H_
 #define XMG_H_
@@ -66,7 +67,7 @@ typedef struct xmg_env_desc {
     int32_t fixed_doors;         /* R6: doors at segment midpoints */
     int32_t rule_width;          /* R (max active rules over the table) */
     int32_t obj_width;           /* O (max active objects over the table) */
-    int32_t row_words;           /* u32 words per task row = 2 + R + ceil(O/4) */
+    int32_t row_words;           /* u32 words per task row: 2 + R + ceil(O/4), rounded up to 4 */
     int32_t num_tasks;           /* M rows in task_rows */
     const uint8_t* base_cells;   /* [H*W] grid before doors/objects for this scenario */
     const int16_t* seg_off;      /* [num_segments+1] offsets into seg_cells */
@@ -88,6 +89,10 @@ typedef struct xmg_out {
     float* reward;      /* [n]  float32(1.0 - 0.9*(sc/budget)) evaluated in fp64 */
     float* discount;    /* [n] */
     int8_t* step_type;  /* [n]  FIRST 0 / MID 1 / LAST 2 */
+    /* nullable episode statistics, one slot per 128-env CTA (no atomics
+     * contention): stats[3*cta + 0] += sum of rewards, [+1] += finished
+     * trials, [+2] += their lengths (ref RolloutStats, harness.py:314-354) */
+    double* stats;
 } xmg_out;
 
 int32_t xmg_abi_version(void);

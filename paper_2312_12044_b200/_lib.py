@@ -15,7 +15,7 @@ import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB_PATH = os.path.join(PKG, "libxmg.so")
+LIB_PATH = os.environ.get("XMG_LIB") or os.path.join(PKG, "libxmg.so")
 SOURCES = [os.path.join(PKG, "csrc", "xmg_step.cu")]
 HEADER = os.path.join(ROOT, "include", "xmg.h")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -52,22 +52,23 @@ class State(C.Structure):
 
 class Out(C.Structure):
     _fields_ = [("obs", C.c_void_p), ("reward", C.c_void_p), ("discount", C.c_void_p),
-                ("step_type", C.c_void_p)]
+                ("step_type", C.c_void_p), ("stats", C.c_void_p)]
 
 
 _lock = threading.Lock()
 _lib = None
 
 
-def build(verbose: bool = False) -> str:
+def build(verbose: bool = False, out: str | None = None, defines: tuple[str, ...] = ()) -> str:
     """Compile libxmg.so for sm_100a in-tree (nvcc); returns its path."""
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, *SOURCES]
+    out = out or os.path.join(PKG, "libxmg.so")
+    cmd = ["nvcc", *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-o", out, *SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise NativeLibraryError(f"nvcc failed:\n{res.stderr}")
     if verbose:
         print(res.stderr)
-    return LIB_PATH
+    return out
 
 
 def _bind(L):

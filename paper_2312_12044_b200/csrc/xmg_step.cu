@@ -109,29 +109,39 @@ __device__ __forceinline__ int near_dr(int k) { return k == 0 ? -1 : (k == 3 ? 1
 __device__ __forceinline__ int near_dc(int k) { return k == 1 ? -1 : (k == 2 ? 1 : 0); }
 
 constexpr int kThreads = 128;  // envs per CTA
+#ifndef XMG_MINB
+#define XMG_MINB 6  // min resident CTAs per SM the register allocation targets
+#endif
 constexpr int kWarps = kThreads / 32;
 
 // ------------------------------------------------------- smem geometry
+// Per CTA: obs stage [128][2v^2] (warp w owns rows 32w..32w+31, stored with
+// one bulk copy per warp), per-thread window stage, per-thread rule-row
+// buffer, per-warp reset / event scratch.  No CTA-wide barrier is used.
 struct Geo {
   int ob;      // observation bytes per env (2 v^2)
   int stg;     // per-thread window stage bytes (16*maxch + 16 bank pad)
+  int rb;      // per-thread rule-row buffer bytes (header + R rules, 16-aligned)
   int hwp;     // H*W rounded up to 16 (+16)
-  int ws;      // per-warp reset scratch bytes
+  int ws;      // per-warp scratch bytes
   int maxch;   // window chunk capacity
   int64_t total;
 };
 
 __host__ __device__ inline int round16(int x) { return (x + 15) & ~15; }
 
-__host__ __device__ inline Geo make_geo(int H, int W, int V, int maxch) {
+__host__ __device__ inline Geo make_geo(int H, int W, int V, int maxch, int R) {
   Geo g;
   g.ob = 2 * V * V;
   g.maxch = maxch;
   g.stg = maxch ? 16 * maxch + 16 : 0;
+  g.rb = 16 * ((2 + R + 3) / 4);
   g.hwp = round16(H * W + 16);
   // Wd: u64[hwp] | FC: u16[hwp] | G: u8[hwp] | misc: 64 u64
   g.ws = 8 * g.hwp + 2 * g.hwp + g.hwp + 512;
-  g.total = (int64_t)kThreads * round16(g.ob) + (int64_t)kThreads * g.stg + (int64_t)kWarps * g.ws;
+  // the warp's observation stage (32 x 2v^2) reuses its scratch at the end
+  if (g.ws < 32 * g.ob) g.ws = round16(32 * g.ob);
+  g.total = (int64_t)kThreads * (g.stg + g.rb) + (int64_t)kWarps * g.ws;
   return g;
 }
 
@@ -202,18 +212,23 @@ __device__ __forceinline__ void stage_from_global(View& vw, int lo, int hi, int 
 
 // ------------------------------------------------------- rules and goals
 // ref:rules.py:147-217 (scalar) / ref:vecenv.py:368-433 (batched).  Slots in
-// stored order, each sees earlier rewrites; the TILE_NEAR family picks the
-// first `a` cell in row-major order with a matching neighbour.
-__device__ void apply_rules(const View& vw, const uint32_t* rules, int nr, int ev, int H, int W, int ar, int ac,
+// stored order, each sees earlier rewrites.
+//
+// MOVE and PICK_UP events gate only agent-relative rules (AGENT_HOLD,
+// AGENT_NEAR, AGENT_NEAR_{UP,RIGHT,DOWN,LEFT}) and agent-relative goals, so
+// they are resolved per lane from the staged window.  Every grid-wide
+// predicate (TILE_NEAR* rules, TILE_* goals) is gated on PUT_DOWN only
+// (ref:rules.py:60-72, ref:goals.py:268-283): PUT_DOWN events are resolved
+// by the whole warp (warp_put_event), one env at a time.
+__device__ __noinline__ void agent_rules(const View& vw, const uint32_t* rules, int nr, int ev, int H, int W, int ar, int ac,
                             int& pocket) {
-  const int HW = H * W;
   for (int s = 0; s < nr; ++s) {
     const uint32_t rw = rules[s];
-    const int kind = rw & 0xff, a = (rw >> 8) & 0xff, b = (rw >> 16) & 0xff, out = rw >> 24;
+    const int kind = rw & 0xff, a = (rw >> 8) & 0xff, out = rw >> 24;
     if (kind == 0 || kind > 11 || !((cRuleGate[kind] >> ev) & 1)) continue;
     if (kind == 1) {  // AGENT_HOLD
       if (pocket == a) pocket = (out >> 4) == kFloor ? 0 : out;
-    } else if (kind == 2) {  // AGENT_NEAR
+    } else if (kind == 2) {  // AGENT_NEAR: first NEAR_OFFSETS neighbour holding a
       for (int k = 0; k < 4; ++k) {
         const int r = ar + near_dr(k), c = ac + near_dc(k);
         if (r >= 0 && r < H && c >= 0 && c < W && vw.rd(r * W + c) == a) {
@@ -224,36 +239,19 @@ __device__ void apply_rules(const View& vw, const uint32_t* rules, int nr, int e
     } else if (kind >= 8) {  // AGENT_NEAR_{UP,RIGHT,DOWN,LEFT}
       const int r = ar + dir_dr(kind - 8), c = ac + dir_dc(kind - 8);
       if (r >= 0 && r < H && c >= 0 && c < W && vw.rd(r * W + c) == a) vw.wr(r * W + c, (uint8_t)out);
-    } else {  // TILE_NEAR (3) / TILE_NEAR_{UP,RIGHT,DOWN,LEFT} (4..7)
-      const int nofs = kind == 3 ? 4 : 1;
-      bool done = false;
-      for (int pos = 0; pos < HW && !done; ++pos) {
-        if (vw.rd(pos) != a) continue;
-        const int r = pos / W, c = pos - (pos / W) * W;
-        for (int k = 0; k < nofs; ++k) {
-          const int nr_ = r + (kind == 3 ? near_dr(k) : dir_dr(kind - 4));
-          const int nc_ = c + (kind == 3 ? near_dc(k) : dir_dc(kind - 4));
-          if (nr_ >= 0 && nr_ < H && nc_ >= 0 && nc_ < W && vw.rd(nr_ * W + nc_) == b) {
-            vw.wr(pos, (uint8_t)out);
-            vw.wr(nr_ * W + nc_, kFloorCode);
-            done = true;
-            break;
-          }
-        }
-      }
     }
   }
 }
 
-// ref:goals.py:347-394 / ref:vecenv.py:435-477
-__device__ bool check_goal(const View& vw, uint32_t goal, int ev, int H, int W, int ar, int ac, int pocket) {
-  const int kind = goal & 0xff, a1 = (goal >> 8) & 0xff, a2 = (goal >> 16) & 0xff, a3 = goal >> 24;
+// Agent-relative goals (ref:goals.py:361-378); the TILE_* kinds never pass the
+// gate of a MOVE / PICK_UP event.
+__device__ bool agent_goal(const View& vw, uint32_t goal, int ev, int H, int W, int ar, int ac, int pocket) {
+  const int kind = goal & 0xff, a1 = (goal >> 8) & 0xff, a2 = (goal >> 16) & 0xff;
   if (kind == 0 || kind > 14 || !((cGoalGate[kind] >> ev) & 1)) return false;
   switch (kind) {
     case 1: return pocket == a1;
     case 2: return vw.rd(ar * W + ac) == a1;
     case 5: return ar == a1 && ac == a2;
-    case 6: return a2 < H && a3 < W && vw.rd(a2 * W + a3) == a1;
     case 3:
       for (int k = 0; k < 4; ++k) {
         const int r = ar + near_dr(k), c = ac + near_dc(k);
@@ -264,20 +262,39 @@ __device__ bool check_goal(const View& vw, uint32_t goal, int ev, int H, int W, 
       const int r = ar + dir_dr(kind - 11), c = ac + dir_dc(kind - 11);
       return r >= 0 && r < H && c >= 0 && c < W && vw.rd(r * W + c) == a1;
     }
-    default: {  // TILE_NEAR (4) and TILE_NEAR_{UP,RIGHT,DOWN,LEFT} (7..10)
-      const int nofs = kind == 4 ? 4 : 1;
-      for (int pos = 0; pos < H * W; ++pos) {
-        if (vw.rd(pos) != a1) continue;
-        const int r = pos / W, c = pos - (pos / W) * W;
-        for (int k = 0; k < nofs; ++k) {
-          const int nr_ = r + (kind == 4 ? near_dr(k) : dir_dr(kind - 7));
-          const int nc_ = c + (kind == 4 ? near_dc(k) : dir_dc(kind - 7));
-          if (nr_ >= 0 && nr_ < H && nc_ >= 0 && nc_ < W && vw.rd(nr_ * W + nc_) == a2) return true;
+    default: return false;
+  }
+}
+
+// Warp-wide scan of grid G for the first cell (row-major) holding `a` that
+// has a neighbour `b` at one of the offsets (NEAR_OFFSETS order for `all4`,
+// else the single offset (odr, odc)).  Returns the cell (or -1) and its
+// neighbour on every lane.  ref:rules.py:192-213 / ref:goals.py:380-394.
+__device__ __forceinline__ int warp_tile_scan(const uint8_t* G, int H, int W, int lane, int a, int b, bool all4,
+                                              int odr, int odc, int& nb_out) {
+  const int HW = H * W;
+  for (int base = 0; base < HW; base += 32) {
+    const int pos = base + lane;
+    int nb = -1;
+    if (pos < HW && G[pos] == a) {
+      const int r = pos / W, c = pos - (pos / W) * W;
+      for (int k = 0; k < (all4 ? 4 : 1); ++k) {
+        const int nr_ = r + (all4 ? near_dr(k) : odr), nc_ = c + (all4 ? near_dc(k) : odc);
+        if (nr_ >= 0 && nr_ < H && nc_ >= 0 && nc_ < W && G[nr_ * W + nc_] == b) {
+          nb = nr_ * W + nc_;
+          break;
         }
       }
-      return false;
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, nb >= 0);
+    if (m) {
+      const int win = __ffs(m) - 1;
+      nb_out = __shfl_sync(0xffffffffu, nb, win);
+      return base + win;
     }
   }
+  nb_out = -1;
+  return -1;
 }
 
 // ------------------------------------------------------- observation
@@ -445,7 +462,7 @@ __device__ int count_filtered(const WarpScratch& ws, int lane, int F, int W, int
 // builders ref:scenarios.py:291-412 (batched: ref:vecenv.py:242-291).
 // Called by all 32 lanes with the same arguments; writes the new grid to
 // `gdst` and returns the new pose / goal on every lane.
-__device__ ResetOut warp_reset(const xmg_env_desc& d, const WarpScratch& ws, int lane, uint64_t ek_hi,
+__device__ __noinline__ ResetOut warp_reset(const xmg_env_desc& d, const WarpScratch& ws, int lane, uint64_t ek_hi,
                                uint64_t ek_lo, const uint32_t* row, uint32_t goal_in, uint8_t* gdst,
                                uint64_t& st_hi, uint64_t& st_lo) {
   const int H = d.height, W = d.width, HW = H * W;
@@ -562,7 +579,6 @@ __device__ ResetOut warp_reset(const xmg_env_desc& d, const WarpScratch& ws, int
   __syncwarp();
   return res;
 }
-
 // ------------------------------------------------------- the fused step
 __device__ __forceinline__ int load_action(const void* a, int dtype, int64_t e) {
   switch (dtype) {
@@ -577,28 +593,112 @@ __device__ __forceinline__ uint64_t pack_agent(int r, int c, int d, int pocket, 
          ((uint64_t)(uint32_t)pocket << 24) | ((uint64_t)sc << 32);
 }
 
+// One PUT_DOWN event resolved by the whole warp on a shared-memory copy G of
+// the env's grid: the rule pass (ref:rules.py:162-213, event PUT_DOWN) and
+// then the goal check (ref:goals.py:347-394).  The pocket is untouched
+// (AGENT_HOLD is gated on PICK_UP).  Writes the grid back when a rule fired;
+// returns the goal predicate on every lane.
+__device__ __noinline__ bool warp_put_event(const WarpScratch& ws, int lane, uint8_t* genv, int H, int W, int ar, int ac,
+                               const uint32_t* rules, int nr, uint32_t goal, bool& dirty) {
+  const int HW = H * W;
+  uint8_t* G = ws.grid;
+  for (int i = lane; i < HW; i += 32) G[i] = genv[i];
+  __syncwarp();
+  dirty = false;
+  for (int s = 0; s < nr; ++s) {
+    const uint32_t rw = rules[s];
+    const int kind = rw & 0xff, a = (rw >> 8) & 0xff, b = (rw >> 16) & 0xff, out = rw >> 24;
+    if (kind == 0 || kind > 11 || !((cRuleGate[kind] >> 2) & 1)) continue;
+    if (kind == 2 || kind >= 8) {  // agent-near family: every lane evaluates the same cells
+      int tgt = -1;
+      if (kind == 2) {
+        for (int k = 0; k < 4; ++k) {
+          const int r = ar + near_dr(k), c = ac + near_dc(k);
+          if (r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a) { tgt = r * W + c; break; }
+        }
+      } else {
+        const int r = ar + dir_dr(kind - 8), c = ac + dir_dc(kind - 8);
+        if (r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a) tgt = r * W + c;
+      }
+      __syncwarp();
+      if (tgt >= 0) {
+        if (lane == 0) G[tgt] = (uint8_t)out;
+        dirty = true;
+      }
+      __syncwarp();
+    } else {  // TILE_NEAR (3) / TILE_NEAR_{UP,RIGHT,DOWN,LEFT} (4..7)
+      int nb;
+      const int pos = warp_tile_scan(G, H, W, lane, a, b, kind == 3, dir_dr(kind - 4), dir_dc(kind - 4), nb);
+      if (pos >= 0) {
+        if (lane == 0) {
+          G[pos] = (uint8_t)out;
+          G[nb] = kFloorCode;
+        }
+        dirty = true;
+      }
+      __syncwarp();
+    }
+  }
+  bool hit = false;
+  const int kind = goal & 0xff, a1 = (goal >> 8) & 0xff, a2 = (goal >> 16) & 0xff, a3 = goal >> 24;
+  if (kind != 0 && kind <= 14 && ((cGoalGate[kind] >> 2) & 1)) {
+    switch (kind) {
+      case 2: hit = G[ar * W + ac] == a1; break;
+      case 5: hit = ar == a1 && ac == a2; break;
+      case 6: hit = a2 < H && a3 < W && G[a2 * W + a3] == a1; break;
+      case 3:
+        for (int k = 0; k < 4; ++k) {
+          const int r = ar + near_dr(k), c = ac + near_dc(k);
+          hit |= r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a1;
+        }
+        break;
+      case 11: case 12: case 13: case 14: {
+        const int r = ar + dir_dr(kind - 11), c = ac + dir_dc(kind - 11);
+        hit = r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a1;
+        break;
+      }
+      default: {  // TILE_NEAR (4), TILE_NEAR_{UP,RIGHT,DOWN,LEFT} (7..10)
+        int nb;
+        hit = warp_tile_scan(G, H, W, lane, a1, a2, kind == 4, dir_dr(kind - 7), dir_dc(kind - 7), nb) >= 0;
+      }
+    }
+  }
+  if (dirty)
+    for (int i = lane; i < HW; i += 32) genv[i] = G[i];
+  __syncwarp();
+  return hit;
+}
+
+// Copy the staged range of grid G into lane `src`'s window stage (warp-wide).
+__device__ __forceinline__ void restage_from(const uint8_t* G, uint8_t* ostage, int sbase, int slo, int shi,
+                                             int lane) {
+  for (int f = slo + lane; f < shi; f += 32) ostage[f - sbase] = G[f];
+}
+
 template <int MAXCH>
-__global__ void __launch_bounds__(kThreads) step_kernel(const xmg_env_desc d, const xmg_state s, const xmg_out o,
+__global__ void __launch_bounds__(kThreads, XMG_MINB) step_kernel(const xmg_env_desc d, const xmg_state s, const xmg_out o,
                                                         const void* actions, int act_dtype,
                                                         const uint64_t* reset_keys, const int32_t* abort_flag,
                                                         int64_t n) {
   extern __shared__ __align__(128) uint8_t smem[];
   if (abort_flag != nullptr && *reinterpret_cast<volatile const int32_t*>(abort_flag) != 0) return;
 
-  const int H = d.height, W = d.width, HW = H * W, V = d.view_size;
-  const Geo geo = make_geo(H, W, V, MAXCH);
+  const int H = d.height, W = d.width, HW = H * W, V = d.view_size, R = d.rule_width;
+  const Geo geo = make_geo(H, W, V, MAXCH, R);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t e0 = (int64_t)blockIdx.x * kThreads;
   const int64_t e = e0 + tid;
   const bool valid = e < n;
   const bool reset_mode = reset_keys != nullptr;
 
-  uint8_t* obs_stage = smem;
+  uint8_t* stage_base = smem;
+  uint8_t* rb_base = stage_base + kThreads * geo.stg;
   View vw;
   vw.g = s.grids + (valid ? e : 0) * (int64_t)HW;
-  vw.stage = MAXCH ? smem + kThreads * round16(geo.ob) + tid * geo.stg : nullptr;
+  vw.stage = MAXCH ? stage_base + tid * geo.stg : nullptr;
   vw.sbase = vw.slo = vw.shi = 0;
-  uint8_t* wbase = smem + kThreads * round16(geo.ob) + kThreads * geo.stg + warp * geo.ws;
+  uint32_t* rbuf = reinterpret_cast<uint32_t*>(rb_base + tid * geo.rb);
+  uint8_t* wbase = rb_base + kThreads * geo.rb + warp * geo.ws;
   WarpScratch ws;
   ws.wd = reinterpret_cast<uint64_t*>(wbase);
   ws.fc = reinterpret_cast<uint16_t*>(wbase + 8 * geo.hwp);
@@ -618,7 +718,10 @@ __global__ void __launch_bounds__(kThreads) step_kernel(const xmg_env_desc d, co
 
   float rew = 0.f, disc = 1.f;
   int8_t stype = 0;
-  bool last = reset_mode;
+  bool last = reset_mode, goal = false;
+  uint32_t done_len = 0;  // length of the trial that just ended (stats)
+  int ev = -1, nr = 0;
+  uint32_t goal_word = 0;
 
   if (valid && !reset_mode) {
     // ---- stage the post-action window (MOVE: both candidate poses)
@@ -632,7 +735,6 @@ __global__ void __launch_bounds__(kThreads) step_kernel(const xmg_env_desc d, co
     const bool inside = tr >= 0 && tr < H && tc >= 0 && tc < W;
     const int tflat = tr * W + tc;
     const int tcode = inside ? vw.rd(tflat) : 0, tt = tcode >> 4;
-    int ev = -1;
     switch (act) {
       case 0:
         if (inside && ((kWalkable >> tt) & 1)) { r = tr; c = tc; ev = 0; }
@@ -657,20 +759,52 @@ __global__ void __launch_bounds__(kThreads) step_kernel(const xmg_env_desc d, co
           }
         }
     }
-    // ---- rules and goal, only after an event (ref:vecenv.py:344-349).
-    // TOGGLE gates no rule and no goal, so it never reaches here.
-    bool goal = false;
-    if (ev >= 0 && ev != 3) {
-      if (d.rule_width > 0) {
-        const uint32_t* row = d.task_rows + (int64_t)s.task[e] * d.row_words;
-        const int nr = row[1] & 0xff;
-        if (nr) apply_rules(vw, row + 2, nr, ev, H, W, r, c, pocket);
+    // ---- rules and goal after MOVE / PICK_UP / PUT_DOWN (ref:vecenv.py:344-349);
+    // TOGGLE gates no rule and no goal.  The task row is fetched with 128-bit loads.
+    if (ev >= 0 && ev <= 2) {
+      if (R > 0) {
+        const uint4* src = reinterpret_cast<const uint4*>(d.task_rows + (int64_t)s.task[e] * d.row_words);
+        const int nq = (2 + R + 3) >> 2;
+        for (int q = 0; q < nq; ++q) reinterpret_cast<uint4*>(rbuf)[q] = src[q];
+        nr = rbuf[1] & 0xff;
       }
-      goal = check_goal(vw, s.goal[e], ev, H, W, r, c, pocket);
+      goal_word = s.goal[e];
+      if (ev <= 1) {
+        if (nr) agent_rules(vw, rbuf + 2, nr, ev, H, W, r, c, pocket);
+        goal = agent_goal(vw, goal_word, ev, H, W, r, c, pocket);
+      }
     }
+  }
+
+  // ---- PUT_DOWN events: grid-wide rules and goals, one env at a time per warp
+  uint32_t pmask = __ballot_sync(0xffffffffu, ev == 2);
+  if (pmask) {
+    __syncwarp();  // the owners' PUT writes (global) and rule rows (smem) are visible
+    while (pmask) {
+      const int src = __ffs(pmask) - 1;
+      pmask &= pmask - 1;
+      const int ar = __shfl_sync(0xffffffffu, r, src), ac = __shfl_sync(0xffffffffu, c, src);
+      const uint32_t gw = __shfl_sync(0xffffffffu, goal_word, src);
+      const int nrs = __shfl_sync(0xffffffffu, nr, src);
+      const uint32_t* rules_s = reinterpret_cast<const uint32_t*>(rb_base + (warp * 32 + src) * geo.rb) + 2;
+      uint8_t* genv = s.grids + (e0 + warp * 32 + src) * (int64_t)HW;
+      bool dirty;
+      const bool hit = warp_put_event(ws, lane, genv, H, W, ar, ac, rules_s, nrs, gw, dirty);
+      if (MAXCH && dirty) {
+        const int sb = __shfl_sync(0xffffffffu, vw.sbase, src);
+        const int slo = __shfl_sync(0xffffffffu, vw.slo, src), shi = __shfl_sync(0xffffffffu, vw.shi, src);
+        restage_from(ws.grid, stage_base + (warp * 32 + src) * geo.stg, sb, slo, shi, lane);
+        __syncwarp();
+      }
+      if (lane == src) goal = hit;
+    }
+  }
+
+  if (valid && !reset_mode) {
     // ---- counters and reward, ref:vecenv.py:351-357 (fp64, no contraction)
     sc += 1;
     last = goal || sc >= (uint32_t)d.budget;
+    done_len = last ? sc : 0;
     if (goal) {
       const double frac = __ddiv_rn((double)sc, (double)d.budget);
       rew = __double2float_rn(__dsub_rn(1.0, __dmul_rn(0.9, frac)));
@@ -695,27 +829,25 @@ __global__ void __launch_bounds__(kThreads) step_kernel(const xmg_env_desc d, co
       rmask &= rmask - 1;
       const uint64_t hi = shfl64(ek_hi, src), lo = shfl64(ek_lo, src);
       const int t = __shfl_sync(0xffffffffu, task, src);
-      const uint32_t g_in = (d.scenario == XMG_SCENARIO_XLAND) ? d.task_rows[(int64_t)t * d.row_words] : 0u;
+      const uint32_t* row = d.task_rows + (int64_t)t * d.row_words;
+      const uint32_t g_in = (d.scenario == XMG_SCENARIO_XLAND) ? row[0] : 0u;
       uint8_t* gdst = s.grids + (e0 + warp * 32 + src) * (int64_t)HW;
       uint64_t st_hi, st_lo;
-      const ResetOut ro = warp_reset(d, ws, lane, hi, lo, d.task_rows + (int64_t)t * d.row_words, g_in, gdst,
-                                     st_hi, st_lo);
+      const ResetOut ro = warp_reset(d, ws, lane, hi, lo, row, g_in, gdst, st_hi, st_lo);
       if (MAXCH) {
         // restage the owner's window straight from the scratch grid
         int lo2, hi2;
         window_span(ro.r, ro.c, ro.d, 0, H, W, V, lo2, hi2);
         const uintptr_t gsrc = reinterpret_cast<uintptr_t>(gdst);
-        const int sbase = (int)(((gsrc + lo2) & ~uintptr_t(15)) - gsrc);
-        const int nch = (int)(((gsrc + hi2) - ((gsrc + lo2) & ~uintptr_t(15)) + 15) >> 4);
-        uint8_t* ostage = smem + kThreads * round16(geo.ob) + (warp * 32 + src) * geo.stg;
-        for (int k = lane; k < 16 * nch; k += 32) {
-          const int f = sbase + k;
-          if (f >= 0 && f < HW) ostage[k] = ws.grid[f];
-        }
+        const uintptr_t a0 = (gsrc + lo2) & ~uintptr_t(15);
+        const int sbase = (int)(a0 - gsrc);
+        const int nch = (int)(((gsrc + hi2) - a0 + 15) >> 4);
+        const int slo = max(sbase, 0), shi = min(sbase + 16 * nch, HW);
+        restage_from(ws.grid, stage_base + (warp * 32 + src) * geo.stg, sbase, slo, shi, lane);
         if (lane == src) {
           vw.sbase = sbase;
-          vw.slo = max(sbase, 0);
-          vw.shi = min(sbase + 16 * nch, HW);
+          vw.slo = slo;
+          vw.shi = shi;
         }
       }
       __syncwarp();
@@ -736,23 +868,41 @@ __global__ void __launch_bounds__(kThreads) step_kernel(const xmg_env_desc d, co
     o.step_type[e] = stype;
   }
 
-  // ---- observation: assembled in smem, one TMA bulk store per CTA
+  // ---- episode statistics: warp sums, one slot per CTA (ref RolloutStats)
+  if (o.stats != nullptr && !reset_mode) {
+    double rs = valid ? (double)rew : 0.0, trl = (valid && last) ? 1.0 : 0.0, ln = (double)done_len;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      rs += __shfl_down_sync(0xffffffffu, rs, off);
+      trl += __shfl_down_sync(0xffffffffu, trl, off);
+      ln += __shfl_down_sync(0xffffffffu, ln, off);
+    }
+    if (lane == 0 && trl + rs > 0.0) {
+      atomicAdd(o.stats + 3 * blockIdx.x, rs);
+      atomicAdd(o.stats + 3 * blockIdx.x + 1, trl);
+      atomicAdd(o.stats + 3 * blockIdx.x + 2, ln);
+    }
+  }
+
+  // ---- observation: assembled in smem, one TMA bulk store per warp
   if (o.obs != nullptr) {
-    if (valid) write_obs(vw, obs_stage + tid * geo.ob, r, c, dir, H, W, V, d.see_through_walls != 0);
-    const int64_t nvalid = min((int64_t)kThreads, n - e0);
+    uint8_t* wsrc = wbase;  // this warp's scratch, free once resets / PUT events are done
+    if (valid) write_obs(vw, wsrc + lane * geo.ob, r, c, dir, H, W, V, d.see_through_walls != 0);
+    const int64_t w0 = e0 + warp * 32;
+    const int nvalid = (int)max((int64_t)0, min((int64_t)32, n - w0));
     const uint32_t bytes = (uint32_t)(nvalid * geo.ob);
     const uint32_t bulk = bytes & ~15u;
+    uint8_t* gdst = o.obs + w0 * geo.ob;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    uint8_t* gdst = o.obs + e0 * geo.ob;
-    if (tid == 0 && bulk) {
-      const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(obs_stage);
+    __syncwarp();
+    if (lane == 0 && bulk) {
+      const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(wsrc);
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                    ::"l"(gdst), "r"(saddr), "r"(bulk) : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
-    for (uint32_t k = bulk + tid; k < bytes; k += kThreads) gdst[k] = obs_stage[k];
-    if (tid == 0 && bulk) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    for (uint32_t k = bulk + lane; k < bytes; k += 32) gdst[k] = wsrc[k];
+    if (lane == 0 && bulk) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
 }
 
@@ -818,7 +968,9 @@ int check_launch(const char* what) {
 
 int pick_maxch(const xmg_env_desc* d) {
   const int need = needed_chunks(d->width, d->view_size);
+  if (need <= 6) return 6;
   if (need <= 8) return 8;
+  if (need <= 12) return 12;
   if (need <= 16) return 16;
   if (need <= 32) return 32;
   return 0;
@@ -827,7 +979,7 @@ int pick_maxch(const xmg_env_desc* d) {
 template <int MAXCH>
 int launch_step(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
                 const uint64_t* keys, const int32_t* abort_flag, int64_t n, cudaStream_t st) {
-  const Geo geo = make_geo(d->height, d->width, d->view_size, MAXCH);
+  const Geo geo = make_geo(d->height, d->width, d->view_size, MAXCH, d->rule_width);
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -848,7 +1000,7 @@ int validate_desc(const xmg_env_desc* d, int64_t n) {
   if (d->scenario < 0 || d->scenario > 6) return fail("unknown scenario");
   if (d->num_segments > 12) return fail("too many door segments");
   if (!d->base_cells || !d->task_rows) return fail("null base_cells / task_rows");
-  const Geo geo = make_geo(d->height, d->width, d->view_size, pick_maxch(d));
+  const Geo geo = make_geo(d->height, d->width, d->view_size, pick_maxch(d), d->rule_width);
   if (geo.total > 227 * 1024)
     return fail("grid too large for the shared-memory reset scratch of this build (H*W <= ~4000)");
   return 0;
@@ -857,7 +1009,9 @@ int validate_desc(const xmg_env_desc* d, int64_t n) {
 int dispatch_step(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
                   const uint64_t* keys, const int32_t* abort_flag, int64_t n, cudaStream_t st) {
   switch (pick_maxch(d)) {
+    case 6: return launch_step<6>(d, s, o, actions, dtype, keys, abort_flag, n, st);
     case 8: return launch_step<8>(d, s, o, actions, dtype, keys, abort_flag, n, st);
+    case 12: return launch_step<12>(d, s, o, actions, dtype, keys, abort_flag, n, st);
     case 16: return launch_step<16>(d, s, o, actions, dtype, keys, abort_flag, n, st);
     case 32: return launch_step<32>(d, s, o, actions, dtype, keys, abort_flag, n, st);
     default: return launch_step<0>(d, s, o, actions, dtype, keys, abort_flag, n, st);
@@ -943,7 +1097,7 @@ int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* a
 
 int64_t xmg_step_smem_bytes(const xmg_env_desc* desc) {
   if (!desc) return -1;
-  return make_geo(desc->height, desc->width, desc->view_size, pick_maxch(desc)).total;
+  return make_geo(desc->height, desc->width, desc->view_size, pick_maxch(desc), desc->rule_width).total;
 }
 
 }  // extern "C"

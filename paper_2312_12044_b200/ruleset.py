@@ -113,7 +113,8 @@ def pack_raw_rows(raw: np.ndarray, max_rules: int, max_objects: int) -> TaskTabl
     rules = _left_pack(ra, rules)[:, :R]
     objs = _left_pack(oa, objs)[:, :O]
     ow = (O + 3) // 4
-    words = np.zeros((m, 2 + R + ow), np.uint32)
+    # rows padded to 16 bytes so the kernel fetches them with 128-bit loads
+    words = np.zeros((m, (2 + R + ow + 3) // 4 * 4), np.uint32)
     words[:, 0] = np.ascontiguousarray(goal).view(np.uint32)[:, 0]
     words[:, 1] = rc.astype(np.uint32) | (oc.astype(np.uint32) << 8)
     if R:
@@ -121,7 +122,7 @@ def pack_raw_rows(raw: np.ndarray, max_rules: int, max_objects: int) -> TaskTabl
     if O:
         ob = np.zeros((m, 4 * ow), np.uint8)
         ob[:, :O] = objs
-        words[:, 2 + R:] = ob.view(np.uint32)
+        words[:, 2 + R:2 + R + ow] = ob.view(np.uint32)
     return TaskTable(words, R, O, O)
 
 

@@ -206,7 +206,7 @@ class VecEnv:
             base = bordered(h, w, goal=scen in (1, 2, 3))
             nseg = 0
         if scen != 0:
-            table = TaskTable(np.zeros((1, 2), np.uint32), 0, 0, 0)  # ports bring their own goal, no rules
+            table = TaskTable(np.zeros((1, 4), np.uint32), 0, 0, 0)  # ports bring their own goal, no rules
             ids = np.zeros(n, np.int32)
         self._ids_host = ids
 
@@ -233,6 +233,7 @@ class VecEnv:
         if _lib.lib().xmg_step_smem_bytes(C.byref(self._desc)) > 227 * 1024:
             raise _lib.NativeLibraryError(f"{h}x{w} grids exceed the shared-memory budget of this build")
         self._outs = None
+        self.stats: torch.Tensor | None = None
         self.launches = 0  # kernels of ours launched by this VecEnv
 
     # -- views
@@ -258,9 +259,20 @@ class VecEnv:
             self._outs = outs
         return outs
 
-    @staticmethod
-    def _out_struct(outs) -> _lib.Out:
-        return _lib.Out(_ptr(outs[0]), _ptr(outs[1]), _ptr(outs[2]), _ptr(outs[3]))
+    def _out_struct(self, outs) -> _lib.Out:
+        return _lib.Out(_ptr(outs[0]), _ptr(outs[1]), _ptr(outs[2]), _ptr(outs[3]), _ptr(self.stats))
+
+    def enable_stats(self) -> torch.Tensor:
+        """Accumulate episode statistics inside the step kernel: returns the
+        (num_ctas, 3) float64 tensor of per-CTA [sum reward, finished trials,
+        sum of their lengths] (ref RolloutStats, harness.py:314-354)."""
+        if self.stats is None:
+            self.stats = torch.zeros(((self.num_envs + 127) // 128, 3), dtype=torch.float64, device=self.device)
+        return self.stats
+
+    def episode_stats(self) -> torch.Tensor:
+        """(3,) float64 totals of the per-CTA accumulators."""
+        return self.enable_stats().sum(dim=0)
 
     # -- reset
     def reset(self, key: Key, compute_obs: bool = True) -> VecTimeStep:
@@ -283,7 +295,7 @@ class VecEnv:
 
     def _reset_keys(self, keys: torch.Tensor, compute_obs: bool) -> VecTimeStep:
         outs = self._alloc_out(compute_obs)
-        o = self._out_struct(outs)
+        o = _lib.Out(_ptr(outs[0]), _ptr(outs[1]), _ptr(outs[2]), _ptr(outs[3]), None)
         _lib.check(_lib.lib().xmg_reset(C.byref(self._desc), C.byref(self._state), keys.data_ptr(), self.num_envs,
                                         C.byref(o), _stream(self.device)), "xmg_reset")
         self.launches += 1
