@@ -21,10 +21,11 @@
  *   grids  u8  [n][H*W]   row-major entity codes tile*16+color
  *                          (allocation must extend >= 64 bytes past n*H*W:
  *                          the step kernel reads 16-byte aligned chunks)
- *   agent  u64 [n]        r | c<<8 | dir<<16 | pocket<<24 | step_count<<32
+ *   agent  u64 [n][2]     word 0: r | c<<8 | dir<<16 | pocket<<24 | step_count<<32
+ *                         word 1: goal | task<<32, where goal = encoding bytes
+ *                         (kind, a1, a2, a3) little-endian and task = the row
+ *                         of the task table this env runs (one 16-byte load)
  *   rng    u64 [n][2]     state key (hi, lo) = ref EnvState.rng
- *   goal   u32 [n]        goal encoding bytes (kind, a1, a2, a3) little-endian
- *   task   i32 [n]        row of the task table this env runs
  * Task table (read-only), u32 [num_tasks][row_words]:
  *   word 0 = goal, word 1 = rule_count | obj_count<<8,
  *   words 2..2+R-1 = active rules (kind, in_a, in_b, out) left-packed,
@@ -69,6 +70,9 @@ typedef struct xmg_env_desc {
     int32_t obj_width;           /* O (max active objects over the table) */
     int32_t row_words;           /* u32 words per task row: 2 + R + ceil(O/4), rounded up to 4 */
     int32_t num_tasks;           /* M rows in task_rows */
+    int32_t resample_tasks;      /* 0: a trial keeps its env's task (reference semantics,
+                                  * vecenv.py:224-233); 1 (extension): every reset draws
+                                  * task = rows[word0(split(ek, 2)) % M] (benchio.py:57-58) */
     const uint8_t* base_cells;   /* [H*W] grid before doors/objects for this scenario */
     const int16_t* seg_off;      /* [num_segments+1] offsets into seg_cells */
     const int16_t* seg_cells;    /* flat cell indices of each door segment */
@@ -77,10 +81,8 @@ typedef struct xmg_env_desc {
 
 typedef struct xmg_state {
     uint8_t* grids;
-    uint64_t* agent;
-    uint64_t* rng;
-    uint32_t* goal;
-    int32_t* task;
+    uint64_t* agent;   /* [n][2] */
+    uint64_t* rng;     /* [n][2] */
 } xmg_state;
 
 /* VecTimeStep (vecenv.py:95-105): observations may be NULL (compute_obs=False) */

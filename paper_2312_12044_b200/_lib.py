@@ -41,13 +41,13 @@ class EnvDesc(C.Structure):
     _fields_ = [("height", C.c_int32), ("width", C.c_int32), ("view_size", C.c_int32), ("budget", C.c_int32),
                 ("scenario", C.c_int32), ("see_through_walls", C.c_int32), ("num_segments", C.c_int32),
                 ("fixed_doors", C.c_int32), ("rule_width", C.c_int32), ("obj_width", C.c_int32),
-                ("row_words", C.c_int32), ("num_tasks", C.c_int32), ("base_cells", C.c_void_p),
+                ("row_words", C.c_int32), ("num_tasks", C.c_int32), ("resample_tasks", C.c_int32),
+                ("base_cells", C.c_void_p),
                 ("seg_off", C.c_void_p), ("seg_cells", C.c_void_p), ("task_rows", C.c_void_p)]
 
 
 class State(C.Structure):
-    _fields_ = [("grids", C.c_void_p), ("agent", C.c_void_p), ("rng", C.c_void_p), ("goal", C.c_void_p),
-                ("task", C.c_void_p)]
+    _fields_ = [("grids", C.c_void_p), ("agent", C.c_void_p), ("rng", C.c_void_p)]
 
 
 class Out(C.Structure):

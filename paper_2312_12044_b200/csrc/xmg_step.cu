@@ -8,19 +8,22 @@
 //   (:359-361 -> :224-291) -> egocentric observation (:481-500).
 //
 // Mapping:
-//  * one thread per env, 128 envs per CTA; the per-env SoA state is read with
-//    coalesced 8-byte loads (agent word) and written back the same way;
-//  * the grid bytes the step needs (the view window around the post-action
-//    pose, extended one cell ahead for MOVE so the target cell is inside) are
-//    fetched as 16-byte aligned chunks straight into a per-thread shared
-//    memory stage: the rest of a 13x13..25x25 grid is never read on the
-//    common no-event path;
-//  * rare work is warp-cooperative: every env whose trial ends is rebuilt by
-//    its whole warp (Philox draws spread over the lanes, the stable argsort of
-//    the reference replaced by an exact rank count in shared memory, the new
-//    grid written with contiguous stores);
+//  * one thread per env, 128 envs per CTA, no CTA-wide barrier after the
+//    kernel prologue;
+//  * per env one 16-byte state word (pose, pocket, step count, goal, task)
+//    read with a single coalesced 128-bit load;
+//  * the grid bytes the step needs (the view window of the post-action pose,
+//    extended one cell ahead for MOVE so the target cell is inside) are
+//    copied global->shared with cp.async (LDGSTS) in 16-byte aligned chunks,
+//    together with a speculative copy of the env's rule row (L2-resident task
+//    table); the rest of the grid is never read on the common path;
+//  * rare work is warp-cooperative: PUT_DOWN events (the only events that
+//    gate grid-wide predicates) are resolved by the whole warp with ballot
+//    scans, and every env whose trial ends is rebuilt by its whole warp
+//    (Philox draws spread over the lanes; the reference's stable argsort
+//    replaced by a bucket counting sort on the uniform draw words);
 //  * observations are assembled in shared memory in the reference layout
-//    (n, v, v, 2) and leave the CTA as one TMA bulk store (cp.async.bulk).
+//    (n, v, v, 2) and leave each warp as one TMA bulk store (cp.async.bulk).
 // Nothing here is a dense contraction, so no tensor cores are used; the
 // kernel is bounded by HBM bytes per env-step (roofline).
 
@@ -101,7 +104,7 @@ constexpr uint32_t kOpaque = (1u << kWall) | (1u << kClosed) | (1u << kLocked);
 __constant__ uint8_t cRuleGate[12] = {0, 0x2, 0x7, 0x4, 0x4, 0x4, 0x4, 0x4, 0x7, 0x7, 0x7, 0x7};
 __constant__ uint8_t cGoalGate[15] = {0, 0x2, 0x7, 0x7, 0x4, 0x7, 0x4, 0x4, 0x4, 0x4, 0x4, 0x7, 0x7, 0x7, 0x7};
 
-// direction deltas (ref:core.py:272) and the view's right-hand vector (ref:observation.py:24-25)
+// direction deltas (ref:core.py:272)
 __device__ __forceinline__ int dir_dr(int d) { return d == 0 ? -1 : (d == 2 ? 1 : 0); }
 __device__ __forceinline__ int dir_dc(int d) { return d == 1 ? 1 : (d == 3 ? -1 : 0); }
 // NEAR_OFFSETS = up, left, right, down (ref:rules.py:76)
@@ -109,22 +112,26 @@ __device__ __forceinline__ int near_dr(int k) { return k == 0 ? -1 : (k == 3 ? 1
 __device__ __forceinline__ int near_dc(int k) { return k == 1 ? -1 : (k == 2 ? 1 : 0); }
 
 constexpr int kThreads = 128;  // envs per CTA
+constexpr int kMaxDynSmem = 227 * 1024 - 1024;  // leave room for the static shared desc copy
+constexpr int kWarps = kThreads / 32;
 #ifndef XMG_MINB
 #define XMG_MINB 6  // min resident CTAs per SM the register allocation targets
 #endif
-constexpr int kWarps = kThreads / 32;
+#ifndef XMG_RARE
+#define XMG_RARE __forceinline__  // rare paths (reset, PUT_DOWN, occlusion) inlined: measured faster
+#endif
 
 // ------------------------------------------------------- smem geometry
-// Per CTA: obs stage [128][2v^2] (warp w owns rows 32w..32w+31, stored with
-// one bulk copy per warp), per-thread window stage, per-thread rule-row
-// buffer, per-warp reset / event scratch.  No CTA-wide barrier is used.
+// Per CTA: per-thread window stage, per-thread rule-row buffer, per-warp
+// scratch (reset / PUT_DOWN event work; reused as the warp's observation
+// stage at the end).  No CTA-wide barrier is used anywhere.
 struct Geo {
   int ob;      // observation bytes per env (2 v^2)
   int stg;     // per-thread window stage bytes (16*maxch + 16 bank pad)
   int rb;      // per-thread rule-row buffer bytes (header + R rules, 16-aligned)
-  int hwp;     // H*W rounded up to 16 (+16)
+  int hwp;     // H*W + 16 rounded up to 16
+  int lg;      // log2 of the reset bucket count (>= 5)
   int ws;      // per-warp scratch bytes
-  int maxch;   // window chunk capacity
   int64_t total;
 };
 
@@ -133,13 +140,13 @@ __host__ __device__ inline int round16(int x) { return (x + 15) & ~15; }
 __host__ __device__ inline Geo make_geo(int H, int W, int V, int maxch, int R) {
   Geo g;
   g.ob = 2 * V * V;
-  g.maxch = maxch;
   g.stg = maxch ? 16 * maxch + 16 : 0;
   g.rb = 16 * ((2 + R + 3) / 4);
   g.hwp = round16(H * W + 16);
-  // Wd: u64[hwp] | FC: u16[hwp] | G: u8[hwp] | misc: 64 u64
-  g.ws = 8 * g.hwp + 2 * g.hwp + g.hwp + 512;
-  // the warp's observation stage (32 x 2v^2) reuses its scratch at the end
+  g.lg = 5;
+  while ((1 << g.lg) < H * W) ++g.lg;
+  // wd: u64[hwp] | fc: u16[hwp] | slot: u16[hwp] | bk: u32[2^lg] | grid: u8[hwp] | misc: 64 u64
+  g.ws = 8 * g.hwp + 2 * g.hwp + 2 * g.hwp + 4 * (1 << g.lg) + g.hwp + 512;
   if (g.ws < 32 * g.ob) g.ws = round16(32 * g.ob);
   g.total = (int64_t)kThreads * (g.stg + g.rb) + (int64_t)kWarps * g.ws;
   return g;
@@ -147,6 +154,15 @@ __host__ __device__ inline Geo make_geo(int H, int W, int V, int maxch, int R) {
 
 // chunk capacity needed for the (MOVE-extended) window: span = v*W + v bytes
 inline int needed_chunks(int W, int V) { return (V * W + V + 30) / 16; }
+
+// ------------------------------------------------------- async copies
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
 
 // ------------------------------------------------------- per-thread view
 // The bytes of one env's grid staged in shared memory: stage[k] mirrors grid
@@ -182,31 +198,22 @@ __device__ __forceinline__ void window_span(int r, int c, int d, int ext, int H,
   hi = r1 * W + c1 + 1;
 }
 
+// Stage grid bytes [lo, hi) of this thread's env with 16-byte cp.async
+// chunks (aligned on the global address; the grid buffer is padded).
 template <int MAXCH>
-__device__ __forceinline__ void stage_from_global(View& vw, int lo, int hi, int HW) {
+__device__ __forceinline__ void stage_issue(View& vw, int lo, int hi, int HW) {
   if constexpr (MAXCH == 0) {
-    vw.slo = vw.shi = 0;
-    vw.sbase = 0;
+    vw.slo = vw.shi = vw.sbase = 0;
   } else {
-    const uintptr_t a0 = reinterpret_cast<uintptr_t>(vw.g + lo) & ~uintptr_t(15);
-    const uintptr_t a1 = reinterpret_cast<uintptr_t>(vw.g + hi);
-    const int nch = (int)((a1 - a0 + 15) >> 4);
-    vw.sbase = (int)(a0 - reinterpret_cast<uintptr_t>(vw.g));
+    const uintptr_t gb = reinterpret_cast<uintptr_t>(vw.g);
+    const uintptr_t a0 = (gb + lo) & ~uintptr_t(15);
+    const int nch = (int)((gb + hi - a0 + 15) >> 4);
+    vw.sbase = (int)(a0 - gb);
     vw.slo = max(vw.sbase, 0);
     vw.shi = min(vw.sbase + 16 * nch, HW);
-    const uint4* src = reinterpret_cast<const uint4*>(a0);
-    uint4* dst = reinterpret_cast<uint4*>(vw.stage);
-    constexpr int B = MAXCH < 8 ? MAXCH : 8;
 #pragma unroll
-    for (int k0 = 0; k0 < MAXCH; k0 += B) {
-      uint4 buf[B];
-#pragma unroll
-      for (int k = 0; k < B; ++k)
-        if (k0 + k < nch) buf[k] = src[k0 + k];
-#pragma unroll
-      for (int k = 0; k < B; ++k)
-        if (k0 + k < nch) dst[k0 + k] = buf[k];
-    }
+    for (int k = 0; k < MAXCH; ++k)
+      if (k < nch) cp_async16(vw.stage + 16 * k, reinterpret_cast<const void*>(a0 + 16 * k));
   }
 }
 
@@ -220,8 +227,8 @@ __device__ __forceinline__ void stage_from_global(View& vw, int lo, int hi, int 
 // predicate (TILE_NEAR* rules, TILE_* goals) is gated on PUT_DOWN only
 // (ref:rules.py:60-72, ref:goals.py:268-283): PUT_DOWN events are resolved
 // by the whole warp (warp_put_event), one env at a time.
-__device__ __noinline__ void agent_rules(const View& vw, const uint32_t* rules, int nr, int ev, int H, int W, int ar, int ac,
-                            int& pocket) {
+__device__ XMG_RARE int agent_rules(View vw, const uint32_t* rules, int nr, int ev, int H, int W, int ar, int ac,
+                                        int pocket) {
   for (int s = 0; s < nr; ++s) {
     const uint32_t rw = rules[s];
     const int kind = rw & 0xff, a = (rw >> 8) & 0xff, out = rw >> 24;
@@ -241,6 +248,7 @@ __device__ __noinline__ void agent_rules(const View& vw, const uint32_t* rules, 
       if (r >= 0 && r < H && c >= 0 && c < W && vw.rd(r * W + c) == a) vw.wr(r * W + c, (uint8_t)out);
     }
   }
+  return pocket;
 }
 
 // Agent-relative goals (ref:goals.py:361-378); the TILE_* kinds never pass the
@@ -298,6 +306,46 @@ __device__ __forceinline__ int warp_tile_scan(const uint8_t* G, int H, int W, in
 }
 
 // ------------------------------------------------------- observation
+// See-through view (ref:vecenv.py:481-500): view cell (i, j) is world
+// (r0 + i*dri + j*drj, c0 + i*dci + j*dcj), an affine map per facing;
+// off-grid cells read END_OF_MAP (0, 0).  Output pairs (tile, color).
+template <int VV>
+__device__ __forceinline__ void obs_see(const uint8_t* stage, int sbase, uint8_t* dst, int r, int c, int d, int H,
+                                        int W, int Vrt) {
+  const int V = VV ? VV : Vrt;
+  const int h = V / 2;
+  int r0, c0, dri, dci, drj, dcj;
+  switch (d) {
+    case 0: r0 = r - (V - 1); c0 = c - h; dri = 1; dci = 0; drj = 0; dcj = 1; break;
+    case 1: r0 = r - h; c0 = c + (V - 1); dri = 0; dci = -1; drj = 1; dcj = 0; break;
+    case 2: r0 = r + (V - 1); c0 = c + h; dri = -1; dci = 0; drj = 0; dcj = -1; break;
+    default: r0 = r + h; c0 = c - (V - 1); dri = 0; dci = 1; drj = -1; dcj = 0; break;
+  }
+  const uint8_t* sp = stage - sbase;
+  uint16_t* o = reinterpret_cast<uint16_t*>(dst);
+  if constexpr (VV != 0) {
+#pragma unroll
+    for (int i = 0; i < VV; ++i) {
+#pragma unroll
+      for (int j = 0; j < VV; ++j) {
+        const int wr = r0 + i * dri + j * drj, wc = c0 + i * dci + j * dcj;
+        uint32_t code = 0;
+        if ((unsigned)wr < (unsigned)H && (unsigned)wc < (unsigned)W) code = sp[wr * W + wc];
+        o[i * VV + j] = (uint16_t)((code >> 4) | ((code & 15u) << 8));
+      }
+    }
+  } else {
+    for (int i = 0; i < V; ++i) {
+      for (int j = 0; j < V; ++j) {
+        const int wr = r0 + i * dri + j * drj, wc = c0 + i * dci + j * dcj;
+        uint32_t code = 0;
+        if ((unsigned)wr < (unsigned)H && (unsigned)wc < (unsigned)W) code = sp[wr * W + wc];
+        o[i * V + j] = (uint16_t)((code >> 4) | ((code & 15u) << 8));
+      }
+    }
+  }
+}
+
 // exact-integer line of sight, ref:observation.py:46-87
 __device__ bool seg_crosses_cell(int p0r, int p0c, int dr, int dc, int cr, int cc) {
   int lo_n = 0, lo_d = 1, hi_n = 1, hi_d = 1;
@@ -329,8 +377,8 @@ __device__ bool cell_visible(const View& vw, int W, int r0, int c0, int r1, int 
   return true;
 }
 
-// (v, v, 2) window, row 0 farthest ahead, agent at (v-1, v/2): ref:vecenv.py:481-500
-__device__ void write_obs(const View& vw, uint8_t* dst, int r, int c, int d, int H, int W, int V, bool see) {
+// Occluded view (see_through_walls=False), ref:observation.py:90-110.
+__device__ XMG_RARE void obs_occluded(View vw, uint8_t* dst, int r, int c, int d, int H, int W, int V) {
   const int h = V / 2;
   const int fr = dir_dr(d), fc = dir_dc(d);
   const int rr = fc, rc = -fr;  // right-hand vector (ref:observation.py:25)
@@ -342,7 +390,7 @@ __device__ void write_obs(const View& vw, uint8_t* dst, int r, int c, int d, int
       const int wr = r + ahead * fr + lat * rr, wc = c + ahead * fc + lat * rc;
       uint16_t v = 0;
       if (wr >= 0 && wr < H && wc >= 0 && wc < W) {
-        if (!see && !cell_visible(vw, W, r, c, wr, wc)) {
+        if (!cell_visible(vw, W, r, c, wr, wc)) {
           v = 1 | (1 << 8);  // (UNSEEN, UNSEEN)
         } else {
           const int code = vw.rd(wr * W + wc);
@@ -356,16 +404,33 @@ __device__ void write_obs(const View& vw, uint8_t* dst, int r, int c, int d, int
 
 // ------------------------------------------------------- warp-cooperative reset
 struct ResetOut {
+  uint64_t st_hi, st_lo;  // next state key
   int r, c, d;
   uint32_t goal;
+  int task;
 };
 
 struct WarpScratch {
-  uint64_t* wd;   // draw words by free-cell index
-  uint16_t* fc;   // free cells (flat), row-major
-  uint8_t* grid;  // trial grid under construction
-  uint64_t* misc; // 64 words: door words [0,24), agent words [24,26), results [32..)
+  uint64_t* wd;    // draw words by free-cell index
+  uint16_t* fc;    // free cells (flat), row-major
+  uint16_t* slot;  // free-cell indices in bucket order
+  uint32_t* bk;    // bucket offsets
+  uint8_t* grid;   // trial grid under construction / PUT_DOWN working copy
+  uint64_t* misc;  // 64 words: door words [0,24), agent words [24,28), results [32..)
+  int lg;
 };
+
+__device__ __forceinline__ WarpScratch make_scratch(uint8_t* wbase, int hwp, int lg) {
+  WarpScratch ws;
+  ws.wd = reinterpret_cast<uint64_t*>(wbase);
+  ws.fc = reinterpret_cast<uint16_t*>(wbase + 8 * hwp);
+  ws.slot = reinterpret_cast<uint16_t*>(wbase + 10 * hwp);
+  ws.bk = reinterpret_cast<uint32_t*>(wbase + 12 * hwp);
+  ws.grid = wbase + 12 * hwp + 4 * (1 << lg);
+  ws.misc = reinterpret_cast<uint64_t*>(ws.grid + hwp);
+  ws.lg = lg;
+  return ws;
+}
 
 __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
   const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src);
@@ -421,26 +486,55 @@ __device__ __forceinline__ bool col_ok(int mode, int cell, int W, int x) {
 }
 
 // Rank of every (filtered) free cell in the stable argsort of its draw word
-// (ref:core.py:328-333, ref:vecenv.py:261-265: ties broken by index), then
-// place `nobj` objects at ranks 0..nobj-1 and report the cell of rank
-// `spawn_rank`.  Exact counting: rank(f) = #{g : (w_g, g) < (w_f, f)}.
+// (ref:core.py:328-333, ref:vecenv.py:261-265: ties broken by index).  The
+// words are uniform, so a counting sort on their top `lg` bits puts < 1
+// other cell in a bucket on average; the rank is the bucket's offset plus an
+// exact (word, index) comparison inside the bucket.  Places `nobj` objects at
+// ranks 0..nobj-1 and records in misc[32] the cell of rank
+// spawn_base + spawn_word % (count - spawn_base) (ref:scenarios.py:281-288).
 __device__ void rank_place(const WarpScratch& ws, int lane, int F, int W, int mode, int x, const uint8_t* objs,
-                           int nobj, int spawn_rank) {
+                           int nobj, int spawn_base, uint64_t spawn_word) {
+  const int lg = ws.lg, nb = 1 << lg, sh = 64 - lg;
+  for (int i = lane; i < nb; i += 32) ws.bk[i] = 0;
+  __syncwarp();
+  for (int f = lane; f < F; f += 32)
+    if (col_ok(mode, ws.fc[f], W, x)) atomicAdd(&ws.bk[ws.wd[f] >> sh], 1u);
+  __syncwarp();
+  // exclusive scan of the bucket counts: lane owns nb/32 consecutive buckets
+  const int per = nb >> 5;
+  uint32_t loc = 0;
+  for (int k = 0; k < per; ++k) loc += ws.bk[lane * per + k];
+  uint32_t inc = loc;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += t;
+  }
+  const int total = __shfl_sync(0xffffffffu, (int)inc, 31);
+  uint32_t run = inc - loc;
+  for (int k = 0; k < per; ++k) {
+    const uint32_t v = ws.bk[lane * per + k];
+    ws.bk[lane * per + k] = run;
+    run += v;
+  }
+  __syncwarp();
+  // scatter: afterwards bk[b] is the end of bucket b
+  for (int f = lane; f < F; f += 32)
+    if (col_ok(mode, ws.fc[f], W, x)) ws.slot[atomicAdd(&ws.bk[ws.wd[f] >> sh], 1u)] = (uint16_t)f;
+  __syncwarp();
+  const int tail = total - spawn_base;
+  const int spawn_rank = tail > 0 ? spawn_base + (int)(spawn_word % (uint64_t)tail) : -1;
   for (int f = lane; f < F; f += 32) {
     const int cell = ws.fc[f];
     if (!col_ok(mode, cell, W, x)) continue;
     const uint64_t wf = ws.wd[f];
-    int rank = 0;
-    if (mode == 0) {
-      for (int g = 0; g < F; ++g) {
-        const uint64_t wg = ws.wd[g];
-        rank += (wg < wf) | ((wg == wf) & (g < f));
-      }
-    } else {
-      for (int g = 0; g < F; ++g) {
-        const uint64_t wg = ws.wd[g];
-        rank += ((wg < wf) | ((wg == wf) & (g < f))) & col_ok(mode, ws.fc[g], W, x);
-      }
+    const int b = (int)(wf >> sh);
+    const int lo = b ? (int)ws.bk[b - 1] : 0, hi = (int)ws.bk[b];
+    int rank = lo;
+    for (int p = lo; p < hi; ++p) {
+      const int g = ws.slot[p];
+      const uint64_t wg = ws.wd[g];
+      rank += (wg < wf) | ((wg == wf) & (g < f));
     }
     if (rank < nobj) ws.grid[cell] = objs[rank];
     if (rank == spawn_rank) reinterpret_cast<int*>(ws.misc + 32)[0] = cell;
@@ -448,35 +542,38 @@ __device__ void rank_place(const WarpScratch& ws, int lane, int F, int W, int mo
   __syncwarp();
 }
 
-__device__ int count_filtered(const WarpScratch& ws, int lane, int F, int W, int mode, int x) {
-  int n = 0;
-  for (int base = 0; base < F; base += 32) {
-    const int f = base + lane;
-    n += __popc(__ballot_sync(0xffffffffu, f < F && col_ok(mode, ws.fc[f], W, x)));
-  }
-  return n;
-}
-
 // Rebuild one env's trial from the episode key ek: ref:vecenv.py:224-233
 // (ks = split(ek, 0), next state key = split(ek, 1)) and the scenario
 // builders ref:scenarios.py:291-412 (batched: ref:vecenv.py:242-291).
 // Called by all 32 lanes with the same arguments; writes the new grid to
-// `gdst` and returns the new pose / goal on every lane.
-__device__ __noinline__ ResetOut warp_reset(const xmg_env_desc& d, const WarpScratch& ws, int lane, uint64_t ek_hi,
-                               uint64_t ek_lo, const uint32_t* row, uint32_t goal_in, uint8_t* gdst,
-                               uint64_t& st_hi, uint64_t& st_lo) {
+// `gdst` and returns the new pose / goal / task on every lane.
+__device__ XMG_RARE ResetOut warp_reset(const xmg_env_desc* dp, uint8_t* wbase, int hwp, int lg, int lane,
+                                            uint64_t ek_hi, uint64_t ek_lo, int task_in, uint32_t goal_in,
+                                            uint8_t* gdst) {
+  const xmg_env_desc& d = *dp;  // CTA copy in shared memory
+  const WarpScratch ws = make_scratch(wbase, hwp, lg);
   const int H = d.height, W = d.width, HW = H * W;
   const int sc = d.scenario;
-  // ks (lane 0) and the next state key (lane 1)
+  // ks (lane 0), the next state key (lane 1), the task-resampling key (lane 2)
   Words4 kw = {0, 0, 0, 0};
-  if (lane < 2) kw = philox((uint64_t)lane, 0, kDomSplit, 0, ek_hi, ek_lo);
+  if (lane < 3) kw = philox((uint64_t)lane, 0, kDomSplit, 0, ek_hi, ek_lo);
   const uint64_t ks_hi = shfl64(kw.w0, 0), ks_lo = shfl64(kw.w1, 0);
-  st_hi = shfl64(kw.w0, 1);
-  st_lo = shfl64(kw.w1, 1);
+  ResetOut res;
+  res.st_hi = shfl64(kw.w0, 1);
+  res.st_lo = shfl64(kw.w1, 1);
+  res.goal = goal_in;
+  res.task = task_in;
+  if (d.resample_tasks && sc == XMG_SCENARIO_XLAND) {
+    // extension (not in the reference): draw a fresh task per trial as
+    // Benchmark.sample_ruleset(split(ek, 2)) = rows[word0 % M] (ref:benchio.py:57-58)
+    Words4 tw = {0, 0, 0, 0};
+    if (lane == 2) tw = philox(0, 0, kDomDraw, 0, kw.w0, kw.w1);
+    res.task = (int)(shfl64(tw.w0, 2) % (uint64_t)d.num_tasks);
+    res.goal = d.task_rows[(int64_t)res.task * d.row_words];
+  }
+  const uint32_t* row = d.task_rows + (int64_t)res.task * d.row_words;
   // base cells of this scenario
   for (int i = lane; i < HW; i += 32) ws.grid[i] = d.base_cells[i];
-  ResetOut res;
-  res.goal = goal_in;
   if (sc == XMG_SCENARIO_EMPTY) {  // ref:scenarios.py:320-327
     __syncwarp();
     for (int i = lane; i < HW; i += 32) gdst[i] = ws.grid[i];
@@ -494,16 +591,18 @@ __device__ __noinline__ ResetOut warp_reset(const xmg_env_desc& d, const WarpScr
   int wall_col = -1, color = 0;
   const bool two_rooms = sc == XMG_SCENARIO_DOOR_KEY || sc == XMG_SCENARIO_UNLOCK || sc == XMG_SCENARIO_UNLOCK_PICKUP;
   if (two_rooms) {  // ref:scenarios.py:341-353, 373-385
-    const Words4 w = philox(0, 0, kDomDraw, 0, k0h, k0l);  // redundant on every lane
+    Words4 w = {0, 0, 0, 0};
+    if (lane == 0) w = philox(0, 0, kDomDraw, 0, k0h, k0l);
+    const uint64_t w0 = shfl64(w.w0, 0), w1 = shfl64(w.w1, 0);
     int door_row;
     if (sc == XMG_SCENARIO_DOOR_KEY) {
-      wall_col = 2 + (int)(w.w0 % (uint64_t)(W - 4));
-      door_row = 1 + (int)(w.w1 % (uint64_t)(H - 2));
+      wall_col = 2 + (int)(w0 % (uint64_t)(W - 4));
+      door_row = 1 + (int)(w1 % (uint64_t)(H - 2));
       color = 7;  // yellow
     } else {
       wall_col = (W - 1) / 2;
-      door_row = 1 + (int)(w.w0 % (uint64_t)(H - 2));
-      color = cGenColors[w.w1 % 10];
+      door_row = 1 + (int)(w0 % (uint64_t)(H - 2));
+      color = cGenColors[w1 % 10];
     }
     __syncwarp();
     for (int r = lane; r < H; r += 32) ws.grid[r * W + wall_col] = kWallCode;
@@ -539,14 +638,10 @@ __device__ __noinline__ ResetOut warp_reset(const xmg_env_desc& d, const WarpScr
       nobj = 0;
       res.goal = 2u | ((uint32_t)kGreenGoal << 8);
     }
-    const int tail = F - nobj;
-    const int spawn = tail > 0 ? nobj + (int)(a0 % (uint64_t)tail) : -1;
-    rank_place(ws, lane, F, W, 0, 0, objs, nobj, spawn);
+    rank_place(ws, lane, F, W, 0, 0, objs, nobj, nobj, a0);
   } else {  // two-room ports: shuffle all free cells, keep the left room
-    const int L = count_filtered(ws, lane, F, W, 1, wall_col);
     objs_local[0] = (uint8_t)(kKey * 16 + color);
-    const int spawn = L > 1 ? 1 + (int)(a0 % (uint64_t)(L - 1)) : -1;
-    rank_place(ws, lane, F, W, 1, wall_col, objs_local, 1, spawn);
+    rank_place(ws, lane, F, W, 1, wall_col, objs_local, 1, 1, a0);
     if (sc == XMG_SCENARIO_DOOR_KEY) {
       res.goal = 2u | ((uint32_t)kGreenGoal << 8);
     } else if (sc == XMG_SCENARIO_UNLOCK) {  // ref:scenarios.py:393-397
@@ -579,6 +674,7 @@ __device__ __noinline__ ResetOut warp_reset(const xmg_env_desc& d, const WarpScr
   __syncwarp();
   return res;
 }
+
 // ------------------------------------------------------- the fused step
 __device__ __forceinline__ int load_action(const void* a, int dtype, int64_t e) {
   switch (dtype) {
@@ -598,10 +694,10 @@ __device__ __forceinline__ uint64_t pack_agent(int r, int c, int d, int pocket, 
 // then the goal check (ref:goals.py:347-394).  The pocket is untouched
 // (AGENT_HOLD is gated on PICK_UP).  Writes the grid back when a rule fired;
 // returns the goal predicate on every lane.
-__device__ __noinline__ bool warp_put_event(const WarpScratch& ws, int lane, uint8_t* genv, int H, int W, int ar, int ac,
-                               const uint32_t* rules, int nr, uint32_t goal, bool& dirty) {
+__device__ XMG_RARE int warp_put_event(uint8_t* G, int lane, uint8_t* genv, int H, int W, int ar, int ac,
+                                           const uint32_t* rules, int nr, uint32_t goal) {
   const int HW = H * W;
-  uint8_t* G = ws.grid;
+  bool dirty;
   for (int i = lane; i < HW; i += 32) G[i] = genv[i];
   __syncwarp();
   dirty = false;
@@ -666,7 +762,7 @@ __device__ __noinline__ bool warp_put_event(const WarpScratch& ws, int lane, uin
   if (dirty)
     for (int i = lane; i < HW; i += 32) genv[i] = G[i];
   __syncwarp();
-  return hit;
+  return (int)hit | ((int)dirty << 1);
 }
 
 // Copy the staged range of grid G into lane `src`'s window stage (warp-wide).
@@ -676,12 +772,15 @@ __device__ __forceinline__ void restage_from(const uint8_t* G, uint8_t* ostage, 
 }
 
 template <int MAXCH>
-__global__ void __launch_bounds__(kThreads, XMG_MINB) step_kernel(const xmg_env_desc d, const xmg_state s, const xmg_out o,
-                                                        const void* actions, int act_dtype,
-                                                        const uint64_t* reset_keys, const int32_t* abort_flag,
-                                                        int64_t n) {
+__global__ void __launch_bounds__(kThreads, XMG_MINB) step_kernel(const xmg_env_desc d, const xmg_state s,
+                                                                  const xmg_out o, const void* actions, int act_dtype,
+                                                                  const uint64_t* reset_keys,
+                                                                  const int32_t* abort_flag, int64_t n) {
   extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ xmg_env_desc sdesc;  // for the out-of-line rare paths (no local copies)
   if (abort_flag != nullptr && *reinterpret_cast<volatile const int32_t*>(abort_flag) != 0) return;
+  if (threadIdx.x == 0) sdesc = d;
+  __syncthreads();
 
   const int H = d.height, W = d.width, HW = H * W, V = d.view_size, R = d.rule_width;
   const Geo geo = make_geo(H, W, V, MAXCH, R);
@@ -693,42 +792,47 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_kernel(const xmg_env_
 
   uint8_t* stage_base = smem;
   uint8_t* rb_base = stage_base + kThreads * geo.stg;
+  uint8_t* wbase = rb_base + kThreads * geo.rb + warp * geo.ws;
   View vw;
   vw.g = s.grids + (valid ? e : 0) * (int64_t)HW;
   vw.stage = MAXCH ? stage_base + tid * geo.stg : nullptr;
   vw.sbase = vw.slo = vw.shi = 0;
   uint32_t* rbuf = reinterpret_cast<uint32_t*>(rb_base + tid * geo.rb);
-  uint8_t* wbase = rb_base + kThreads * geo.rb + warp * geo.ws;
-  WarpScratch ws;
-  ws.wd = reinterpret_cast<uint64_t*>(wbase);
-  ws.fc = reinterpret_cast<uint16_t*>(wbase + 8 * geo.hwp);
-  ws.grid = wbase + 10 * geo.hwp;
-  ws.misc = reinterpret_cast<uint64_t*>(wbase + 11 * geo.hwp);
+  const WarpScratch ws = make_scratch(wbase, geo.hwp, geo.lg);
 
-  // ---- load: agent word (coalesced 8 B) and action
-  uint64_t ag = 0;
+  // ---- load: the 16-byte state word and the action
+  ulonglong2 ag = make_ulonglong2(0, 0);
   int act = 1;
   if (valid) {
-    ag = s.agent[e];
+    ag = reinterpret_cast<const ulonglong2*>(s.agent)[e];
     if (!reset_mode) act = load_action(actions, act_dtype, e);
   }
-  int r = (int)(ag & 0xff), c = (int)((ag >> 8) & 0xff), dir = (int)((ag >> 16) & 3);
-  int pocket = (int)((ag >> 24) & 0xff);
-  uint32_t sc = (uint32_t)(ag >> 32);
+  int r = (int)(ag.x & 0xff), c = (int)((ag.x >> 8) & 0xff), dir = (int)((ag.x >> 16) & 3);
+  int pocket = (int)((ag.x >> 24) & 0xff);
+  uint32_t sc = (uint32_t)(ag.x >> 32);
+  uint32_t goal_word = (uint32_t)ag.y;
+  int task = (int)(ag.y >> 32);
 
   float rew = 0.f, disc = 1.f;
   int8_t stype = 0;
-  bool last = reset_mode, goal = false;
+  bool last = reset_mode, goal = false, word1_dirty = false;
   uint32_t done_len = 0;  // length of the trial that just ended (stats)
   int ev = -1, nr = 0;
-  uint32_t goal_word = 0;
 
   if (valid && !reset_mode) {
-    // ---- stage the post-action window (MOVE: both candidate poses)
+    // ---- stage the post-action window (MOVE: both candidate poses) and,
+    // for actions that can raise an event, the env's rule row
     const int nd = act == 1 ? ((dir + 3) & 3) : (act == 2 ? ((dir + 1) & 3) : dir);
     int lo, hi;
     window_span(r, c, nd, act == 0 ? 1 : 0, H, W, V, lo, hi);
-    stage_from_global<MAXCH>(vw, lo, hi, HW);
+    stage_issue<MAXCH>(vw, lo, hi, HW);
+    const bool may_event = act == 0 || act == 3 || act == 4;
+    if (R > 0 && may_event) {
+      const uint32_t* src = d.task_rows + (int64_t)task * d.row_words;
+      const int nq = (2 + R + 3) >> 2;
+      for (int q = 0; q < nq; ++q) cp_async16(rbuf + 4 * q, src + 4 * q);
+    }
+    if (MAXCH || (R > 0 && may_event)) cp_async_wait_all();
 
     // ---- action, ref:vecenv.py:306-342 / ref:env.py:148-191
     const int tr = r + dir_dr(dir), tc = c + dir_dc(dir);
@@ -759,20 +863,12 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_kernel(const xmg_env_
           }
         }
     }
-    // ---- rules and goal after MOVE / PICK_UP / PUT_DOWN (ref:vecenv.py:344-349);
-    // TOGGLE gates no rule and no goal.  The task row is fetched with 128-bit loads.
-    if (ev >= 0 && ev <= 2) {
-      if (R > 0) {
-        const uint4* src = reinterpret_cast<const uint4*>(d.task_rows + (int64_t)s.task[e] * d.row_words);
-        const int nq = (2 + R + 3) >> 2;
-        for (int q = 0; q < nq; ++q) reinterpret_cast<uint4*>(rbuf)[q] = src[q];
-        nr = rbuf[1] & 0xff;
-      }
-      goal_word = s.goal[e];
-      if (ev <= 1) {
-        if (nr) agent_rules(vw, rbuf + 2, nr, ev, H, W, r, c, pocket);
-        goal = agent_goal(vw, goal_word, ev, H, W, r, c, pocket);
-      }
+    // ---- rules and goal after MOVE / PICK_UP (ref:vecenv.py:344-349);
+    // TOGGLE gates no rule and no goal; PUT_DOWN is resolved warp-wide below.
+    if (R > 0 && ev >= 0 && ev <= 2) nr = rbuf[1] & 0xff;
+    if (ev == 0 || ev == 1) {
+      if (nr) pocket = agent_rules(vw, rbuf + 2, nr, ev, H, W, r, c, pocket);
+      goal = agent_goal(vw, goal_word, ev, H, W, r, c, pocket);
     }
   }
 
@@ -788,9 +884,9 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_kernel(const xmg_env_
       const int nrs = __shfl_sync(0xffffffffu, nr, src);
       const uint32_t* rules_s = reinterpret_cast<const uint32_t*>(rb_base + (warp * 32 + src) * geo.rb) + 2;
       uint8_t* genv = s.grids + (e0 + warp * 32 + src) * (int64_t)HW;
-      bool dirty;
-      const bool hit = warp_put_event(ws, lane, genv, H, W, ar, ac, rules_s, nrs, gw, dirty);
-      if (MAXCH && dirty) {
+      const int res = warp_put_event(ws.grid, lane, genv, H, W, ar, ac, rules_s, nrs, gw);
+      const bool hit = res & 1;
+      if (MAXCH && (res & 2)) {
         const int sb = __shfl_sync(0xffffffffu, vw.sbase, src);
         const int slo = __shfl_sync(0xffffffffu, vw.slo, src), shi = __shfl_sync(0xffffffffu, vw.shi, src);
         restage_from(ws.grid, stage_base + (warp * 32 + src) * geo.stg, sb, slo, shi, lane);
@@ -817,23 +913,19 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_kernel(const xmg_env_
   uint32_t rmask = __ballot_sync(0xffffffffu, valid && last);
   if (rmask) {
     uint64_t ek_hi = 0, ek_lo = 0;
-    int task = 0;
     if (valid && last) {
-      const uint64_t* kp = reset_mode ? reset_keys + 2 * e : s.rng + 2 * e;
-      ek_hi = kp[0];
-      ek_lo = kp[1];
-      task = s.task[e];
+      const ulonglong2 k = reinterpret_cast<const ulonglong2*>(reset_mode ? reset_keys : s.rng)[e];
+      ek_hi = k.x;
+      ek_lo = k.y;
     }
     while (rmask) {
       const int src = __ffs(rmask) - 1;
       rmask &= rmask - 1;
       const uint64_t hi = shfl64(ek_hi, src), lo = shfl64(ek_lo, src);
       const int t = __shfl_sync(0xffffffffu, task, src);
-      const uint32_t* row = d.task_rows + (int64_t)t * d.row_words;
-      const uint32_t g_in = (d.scenario == XMG_SCENARIO_XLAND) ? row[0] : 0u;
+      const uint32_t g_in = __shfl_sync(0xffffffffu, goal_word, src);
       uint8_t* gdst = s.grids + (e0 + warp * 32 + src) * (int64_t)HW;
-      uint64_t st_hi, st_lo;
-      const ResetOut ro = warp_reset(d, ws, lane, hi, lo, row, g_in, gdst, st_hi, st_lo);
+      const ResetOut ro = warp_reset(&sdesc, wbase, geo.hwp, geo.lg, lane, hi, lo, t, g_in, gdst);
       if (MAXCH) {
         // restage the owner's window straight from the scratch grid
         int lo2, hi2;
@@ -853,16 +945,22 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_kernel(const xmg_env_
       __syncwarp();
       if (lane == src) {
         r = ro.r; c = ro.c; dir = ro.d; pocket = 0; sc = 0;
-        s.rng[2 * e] = st_hi;
-        s.rng[2 * e + 1] = st_lo;
-        s.goal[e] = ro.goal;
+        goal_word = ro.goal;
+        task = ro.task;
+        word1_dirty = true;
+        reinterpret_cast<ulonglong2*>(s.rng)[e] = make_ulonglong2(ro.st_hi, ro.st_lo);
       }
     }
   }
 
   // ---- per-env outputs (coalesced)
   if (valid) {
-    s.agent[e] = pack_agent(r, c, dir, pocket, sc);
+    const uint64_t w0 = pack_agent(r, c, dir, pocket, sc);
+    if (word1_dirty)
+      reinterpret_cast<ulonglong2*>(s.agent)[e] =
+          make_ulonglong2(w0, (uint64_t)goal_word | ((uint64_t)(uint32_t)task << 32));
+    else
+      s.agent[2 * e] = w0;
     o.reward[e] = rew;
     o.discount[e] = disc;
     o.step_type[e] = stype;
@@ -887,7 +985,15 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_kernel(const xmg_env_
   // ---- observation: assembled in smem, one TMA bulk store per warp
   if (o.obs != nullptr) {
     uint8_t* wsrc = wbase;  // this warp's scratch, free once resets / PUT events are done
-    if (valid) write_obs(vw, wsrc + lane * geo.ob, r, c, dir, H, W, V, d.see_through_walls != 0);
+    if (valid) {
+      uint8_t* dst = wsrc + lane * geo.ob;
+      if (MAXCH && d.see_through_walls) {
+        if (V == 5) obs_see<5>(vw.stage, vw.sbase, dst, r, c, dir, H, W, V);
+        else obs_see<0>(vw.stage, vw.sbase, dst, r, c, dir, H, W, V);
+      } else {
+        obs_occluded(vw, dst, r, c, dir, H, W, V);
+      }
+    }
     const int64_t w0 = e0 + warp * 32;
     const int nvalid = (int)max((int64_t)0, min((int64_t)32, n - w0));
     const uint32_t bytes = (uint32_t)(nvalid * geo.ob);
@@ -930,11 +1036,11 @@ __global__ void random_actions_kernel(const uint64_t* keys, int64_t n, int64_t t
   if (idx >= n * nblocks) return;
   const int64_t i = idx % n, b = b0 + idx / n;
   const Words4 w = philox((uint64_t)b, 0, kDomDraw, 0, keys[2 * i], keys[2 * i + 1]);
-  const uint64_t ws[4] = {w.w0, w.w1, w.w2, w.w3};
+  const uint64_t wv[4] = {w.w0, w.w1, w.w2, w.w3};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int64_t t = 4 * b + k - t0;
-    if (t >= 0 && t < steps) actions[t * n + i] = (uint8_t)(ws[k] % 6);
+    if (t >= 0 && t < steps) actions[t * n + i] = (uint8_t)(wv[k] % 6);
   }
 }
 
@@ -983,7 +1089,11 @@ int launch_step(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, con
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(step_kernel<MAXCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncAttributes fa;
+    attr_err = cudaFuncGetAttributes(&fa, step_kernel<MAXCH>);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(step_kernel<MAXCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kMaxDynSmem - (int)fa.sharedSizeBytes);
   });
   if (attr_err != cudaSuccess) return fail(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
   const int64_t blocks = (n + kThreads - 1) / kThreads;
@@ -995,14 +1105,18 @@ int launch_step(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, con
 int validate_desc(const xmg_env_desc* d, int64_t n) {
   if (!d) return fail("null env description");
   if (n < 1) return fail("n must be >= 1");
+  if (n > ((int64_t)1 << 40)) return fail("n too large");
   if (d->height < 1 || d->height > 255 || d->width < 1 || d->width > 255) return fail("grid size outside [1, 255]");
   if (d->view_size < 3 || !(d->view_size & 1)) return fail("view_size must be odd and >= 3");
   if (d->scenario < 0 || d->scenario > 6) return fail("unknown scenario");
   if (d->num_segments > 12) return fail("too many door segments");
+  if (d->rule_width < 0 || d->rule_width > 255 || d->obj_width < 0 || d->obj_width > 255) return fail("bad widths");
+  if (d->row_words < 4 || (d->row_words & 3)) return fail("row_words must be a positive multiple of 4");
+  if (d->num_tasks < 1) return fail("empty task table");
   if (!d->base_cells || !d->task_rows) return fail("null base_cells / task_rows");
   const Geo geo = make_geo(d->height, d->width, d->view_size, pick_maxch(d), d->rule_width);
-  if (geo.total > 227 * 1024)
-    return fail("grid too large for the shared-memory reset scratch of this build (H*W <= ~4000)");
+  if (geo.total > kMaxDynSmem)
+    return fail("grid too large for the shared-memory scratch of this build (H*W <= ~3000)");
   return 0;
 }
 

@@ -141,7 +141,8 @@ class EnvState:
 # ------------------------------------------------------------ VecEnv
 class VecEnv:
     def __init__(self, params: EnvParams, num_envs: int, rulesets=None, *, device=None, task_ids=None,
-                 strict: bool = False, global_offset: int = 0, reuse_outputs: bool = False):
+                 strict: bool = False, global_offset: int = 0, reuse_outputs: bool = False,
+                 resample_tasks: bool = False):
         if num_envs < 1:
             raise ValueError(f"num_envs must be >= 1, got {num_envs}")
         self.params = params
@@ -199,7 +200,8 @@ class VecEnv:
             fixed = int(plan.fixed_doors)
             nseg = len(plan.door_segments)
             free = int(((base >> 4) == 3).sum())
-            used_obj = int(((table.rows[ids, 1] >> 8) & 0xFF).max()) if scen == 0 else 1
+            rows = table.rows if resample_tasks else table.rows[ids]
+            used_obj = int(((rows[:, 1] >> 8) & 0xFF).max()) if scen == 0 else 1
             if used_obj >= free:  # ref vecenv.py:171-175
                 raise GridFull(f"{used_obj} objects on {free} free cells")
         else:
@@ -216,21 +218,22 @@ class VecEnv:
         self._seg_cells = torch.from_numpy(seg_cells.astype(np.int16)).to(dev)
         self._table = torch.from_numpy(table.rows.view(np.int32).copy()).to(dev)
         self.grids_flat = torch.zeros(n * self._hw + GRID_PAD, dtype=torch.uint8, device=dev)
-        self.agent = torch.zeros(n, dtype=torch.int64, device=dev)
+        # 16-byte state word per env: [pose | pocket | step count, goal | task << 32]
+        goals = table.rows[ids, 0].astype(np.uint64) if scen == 0 else np.zeros(n, np.uint64)
+        word1 = goals | (ids.astype(np.uint64) << np.uint64(32))
+        agent = np.zeros((n, 2), np.uint64)
+        agent[:, 1] = word1
+        self.agent = torch.from_numpy(agent.view(np.int64)).to(dev)
         self.rng = torch.zeros((n, 2), dtype=torch.int64, device=dev)
-        self.task = torch.from_numpy(ids).to(dev)
-        goals = table.rows[ids, 0] if scen == 0 else np.zeros(n, np.uint32)
-        self.goal = torch.from_numpy(goals.view(np.int32).copy()).to(dev)
         self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self._flag_checked = True
 
         self._desc = _lib.EnvDesc(h, w, v, params.step_budget, scen, int(params.see_through_walls), nseg, fixed,
                                   table.rule_width if scen == 0 else 0, table.obj_width, table.row_words,
-                                  table.num_tasks, self._base.data_ptr(), self._seg_off.data_ptr(),
-                                  self._seg_cells.data_ptr(), self._table.data_ptr())
-        self._state = _lib.State(self.grids_flat.data_ptr(), self.agent.data_ptr(), self.rng.data_ptr(),
-                                 self.goal.data_ptr(), self.task.data_ptr())
-        if _lib.lib().xmg_step_smem_bytes(C.byref(self._desc)) > 227 * 1024:
+                                  table.num_tasks, int(resample_tasks and scen == 0), self._base.data_ptr(),
+                                  self._seg_off.data_ptr(), self._seg_cells.data_ptr(), self._table.data_ptr())
+        self._state = _lib.State(self.grids_flat.data_ptr(), self.agent.data_ptr(), self.rng.data_ptr())
+        if _lib.lib().xmg_step_smem_bytes(C.byref(self._desc)) > 226 * 1024:
             raise _lib.NativeLibraryError(f"{h}x{w} grids exceed the shared-memory budget of this build")
         self._outs = None
         self.stats: torch.Tensor | None = None
@@ -243,9 +246,19 @@ class VecEnv:
 
     def agent_fields(self) -> torch.Tensor:
         """(N, 5) int64: row, col, dir, pocket, step_count."""
-        a = self.agent
+        a = self.agent[:, 0]
         return torch.stack([a & 0xFF, (a >> 8) & 0xFF, (a >> 16) & 0xFF, (a >> 24) & 0xFF,
                             (a >> 32) & 0xFFFFFFFF], dim=1)
+
+    @property
+    def goal(self) -> torch.Tensor:
+        """(N,) goal encodings (kind | a1 << 8 | a2 << 16 | a3 << 24)."""
+        return self.agent[:, 1] & 0xFFFFFFFF
+
+    @property
+    def task(self) -> torch.Tensor:
+        """(N,) task-table row of each env."""
+        return (self.agent[:, 1] >> 32) & 0xFFFFFFFF
 
     # -- outputs
     def _alloc_out(self, compute_obs: bool):
@@ -353,13 +366,13 @@ class VecEnv:
         if self._tasks is not None:
             return self._tasks[i]
         if self._benchmark is not None:
-            return self._benchmark.get_ruleset(int(self._ids_host[i]))
+            return self._benchmark.get_ruleset(int(self.task[i].item()))
         return Ruleset()
 
     def env_state(self, i: int) -> EnvState:
         """The i-th env as a scalar EnvState (ref vecenv.py:511-521)."""
         g = self.grids[i].cpu().numpy().tobytes()
-        a = int(self.agent[i].item()) & ((1 << 64) - 1)
+        a = int(self.agent[i, 0].item()) & ((1 << 64) - 1)
         k = self.rng[i].cpu().numpy().view(np.uint64)
         agent = AgentState(Position(a & 0xFF, (a >> 8) & 0xFF), Direction((a >> 16) & 3), (a >> 24) & 0xFF)
         return EnvState(Grid(self.params.height, self.params.width, g), agent, self.ruleset_of(i),
