@@ -28,7 +28,9 @@
  *   rng    u64 [n][2]     state key (hi, lo) = ref EnvState.rng
  * Task table (read-only), u32 [num_tasks][row_words]:
  *   word 0 = goal, word 1 = rule_count | obj_count<<8,
- *   words 2..2+R-1 = active rules (kind, in_a, in_b, out) left-packed,
+ *   word 2 = bitmask of rule slots gated on MOVE, word 3 = on PICK_UP
+ *   (AGENT_NEAR family / + AGENT_HOLD, ref rules.py:60-72; all ones if R > 32),
+ *   words 4..4+R-1 = active rules (kind, in_a, in_b, out) left-packed,
  *   then ceil(O/4) words of active object codes, left-packed; rows are
  *   padded to a multiple of 4 words (16-byte aligned 128-bit loads).
  */
@@ -68,7 +70,7 @@ typedef struct xmg_env_desc {
     int32_t fixed_doors;         /* R6: doors at segment midpoints */
     int32_t rule_width;          /* R (max active rules over the table) */
     int32_t obj_width;           /* O (max active objects over the table) */
-    int32_t row_words;           /* u32 words per task row: 2 + R + ceil(O/4), rounded up to 4 */
+    int32_t row_words;           /* u32 words per task row: 4 + R + ceil(O/4), rounded up to 4 */
     int32_t num_tasks;           /* M rows in task_rows */
     int32_t resample_tasks;      /* 0: a trial keeps its env's task (reference semantics,
                                   * vecenv.py:224-233); 1 (extension): every reset draws
@@ -83,6 +85,9 @@ typedef struct xmg_state {
     uint8_t* grids;
     uint64_t* agent;   /* [n][2] */
     uint64_t* rng;     /* [n][2] */
+    uint32_t* work;    /* [xmg_work_words(n)], zero-initialised once: the queues of
+                        * rare work (PUT_DOWN events, trial resets) handed from
+                        * the streaming kernel to the warp-per-env kernel */
 } xmg_state;
 
 /* VecTimeStep (vecenv.py:95-105): observations may be NULL (compute_obs=False) */
@@ -130,16 +135,25 @@ void xmg_philox_host(const uint64_t ctr[4], uint64_t k0, uint64_t k1, uint64_t o
 int32_t xmg_reset(const xmg_env_desc* desc, const xmg_state* state, const uint64_t* keys /*[n][2]*/, int64_t n,
                   const xmg_out* out, void* stream);
 
-/* Sets *flag (device int32, caller zeroes it) to 1 when any action lies
- * outside [0, 6): the device half of ref vecenv.py:297-301 (InvalidAction). */
-int32_t xmg_validate_actions(const void* actions, int32_t action_dtype, int64_t n, int32_t* flag, void* stream);
+/* Raises *flag (device u32, zero-initialised once) to `epoch` when any action
+ * lies outside [0, 6): the device half of ref vecenv.py:297-301
+ * (InvalidAction).  The step with the same epoch then touches nothing. */
+int32_t xmg_validate_actions(const void* actions, int32_t action_dtype, int64_t n, uint32_t epoch, uint32_t* flag,
+                             void* stream);
 
 /* ref VecEnv.step (vecenv.py:295-364): action, rules, goal, reward, auto-reset
- * from each env's own rng, observation of the next playable state.
- * abort_flag (device, nullable): when *abort_flag != 0 no env is touched
- * (pairs with xmg_validate_actions so an invalid batch mutates nothing). */
+ * from each env's own rng, observation of the next playable state.  Two
+ * kernels on `stream`: a streaming one-thread-per-env pass and a
+ * one-warp-per-env pass over the envs it queued (PUT_DOWN events, resets).
+ * `epoch` numbers the caller's steps (consecutive calls on one state must use
+ * consecutive epochs: its parity selects the queue buffers).  abort_flag
+ * (device, nullable): when *abort_flag == epoch no env is touched (pairs with
+ * xmg_validate_actions so an invalid batch mutates nothing). */
 int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* actions, int32_t action_dtype,
-                 int64_t n, const xmg_out* out, const int32_t* abort_flag, void* stream);
+                 int64_t n, const xmg_out* out, const uint32_t* abort_flag, uint32_t epoch, void* stream);
+
+/* Size in u32 words of xmg_state.work for n envs. */
+int64_t xmg_work_words(int64_t n);
 
 /* Bytes of dynamic shared memory per 128-env CTA the step/reset kernels use
  * for this description (host query, for capacity checks). <0 if unsupported. */

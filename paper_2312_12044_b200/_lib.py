@@ -30,7 +30,7 @@ ACT_U8, ACT_I32, ACT_I64 = 0, 1, 2
 
 EXPORTS = ("xmg_abi_version", "xmg_last_error", "xmg_philox", "xmg_split_batch", "xmg_random_actions",
            "xmg_key_from_seed", "xmg_fold_in", "xmg_philox_host", "xmg_reset", "xmg_validate_actions",
-           "xmg_step", "xmg_step_smem_bytes")
+           "xmg_step", "xmg_step_smem_bytes", "xmg_work_words")
 
 
 class NativeLibraryError(RuntimeError):
@@ -47,7 +47,7 @@ class EnvDesc(C.Structure):
 
 
 class State(C.Structure):
-    _fields_ = [("grids", C.c_void_p), ("agent", C.c_void_p), ("rng", C.c_void_p)]
+    _fields_ = [("grids", C.c_void_p), ("agent", C.c_void_p), ("rng", C.c_void_p), ("work", C.c_void_p)]
 
 
 class Out(C.Structure):
@@ -83,9 +83,10 @@ def _bind(L):
         "xmg_fold_in": ([u64, u64, u64, i32, vp], None),
         "xmg_philox_host": ([vp, u64, u64, vp], None),
         "xmg_reset": ([C.POINTER(EnvDesc), C.POINTER(State), vp, i64, C.POINTER(Out), vp], i32),
-        "xmg_validate_actions": ([vp, i32, i64, vp, vp], i32),
-        "xmg_step": ([C.POINTER(EnvDesc), C.POINTER(State), vp, i32, i64, C.POINTER(Out), vp, vp], i32),
+        "xmg_validate_actions": ([vp, i32, i64, C.c_uint32, vp, vp], i32),
+        "xmg_step": ([C.POINTER(EnvDesc), C.POINTER(State), vp, i32, i64, C.POINTER(Out), vp, C.c_uint32, vp], i32),
         "xmg_step_smem_bytes": ([C.POINTER(EnvDesc)], i64),
+        "xmg_work_words": ([i64], i64),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

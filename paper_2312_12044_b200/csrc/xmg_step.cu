@@ -112,45 +112,20 @@ __device__ __forceinline__ int near_dr(int k) { return k == 0 ? -1 : (k == 3 ? 1
 __device__ __forceinline__ int near_dc(int k) { return k == 1 ? -1 : (k == 2 ? 1 : 0); }
 
 constexpr int kThreads = 128;  // envs per CTA
+constexpr int kRowHeader = 4;  // task row: goal, counts, MOVE slot mask, PICK_UP slot mask
 constexpr int kMaxDynSmem = 227 * 1024 - 1024;  // leave room for the static shared desc copy
 constexpr int kWarps = kThreads / 32;
 #ifndef XMG_MINB
 #define XMG_MINB 6  // min resident CTAs per SM the register allocation targets
 #endif
+#ifndef XMG_MINB_RARE
+#define XMG_MINB_RARE 4  // step_rare: <= 128 registers
+#endif
 #ifndef XMG_RARE
 #define XMG_RARE __forceinline__  // rare paths (reset, PUT_DOWN, occlusion) inlined: measured faster
 #endif
 
-// ------------------------------------------------------- smem geometry
-// Per CTA: per-thread window stage, per-thread rule-row buffer, per-warp
-// scratch (reset / PUT_DOWN event work; reused as the warp's observation
-// stage at the end).  No CTA-wide barrier is used anywhere.
-struct Geo {
-  int ob;      // observation bytes per env (2 v^2)
-  int stg;     // per-thread window stage bytes (16*maxch + 16 bank pad)
-  int rb;      // per-thread rule-row buffer bytes (header + R rules, 16-aligned)
-  int hwp;     // H*W + 16 rounded up to 16
-  int lg;      // log2 of the reset bucket count (>= 5)
-  int ws;      // per-warp scratch bytes
-  int64_t total;
-};
-
 __host__ __device__ inline int round16(int x) { return (x + 15) & ~15; }
-
-__host__ __device__ inline Geo make_geo(int H, int W, int V, int maxch, int R) {
-  Geo g;
-  g.ob = 2 * V * V;
-  g.stg = maxch ? 16 * maxch + 16 : 0;
-  g.rb = 16 * ((2 + R + 3) / 4);
-  g.hwp = round16(H * W + 16);
-  g.lg = 5;
-  while ((1 << g.lg) < H * W) ++g.lg;
-  // wd: u64[hwp] | fc: u16[hwp] | slot: u16[hwp] | bk: u32[2^lg] | grid: u8[hwp] | misc: 64 u64
-  g.ws = 8 * g.hwp + 2 * g.hwp + 2 * g.hwp + 4 * (1 << g.lg) + g.hwp + 512;
-  if (g.ws < 32 * g.ob) g.ws = round16(32 * g.ob);
-  g.total = (int64_t)kThreads * (g.stg + g.rb) + (int64_t)kWarps * g.ws;
-  return g;
-}
 
 // chunk capacity needed for the (MOVE-extended) window: span = v*W + v bytes
 inline int needed_chunks(int W, int V) { return (V * W + V + 30) / 16; }
@@ -225,12 +200,12 @@ __device__ __forceinline__ void stage_issue(View& vw, int lo, int hi, int HW) {
 // AGENT_NEAR, AGENT_NEAR_{UP,RIGHT,DOWN,LEFT}) and agent-relative goals, so
 // they are resolved per lane from the staged window.  Every grid-wide
 // predicate (TILE_NEAR* rules, TILE_* goals) is gated on PUT_DOWN only
-// (ref:rules.py:60-72, ref:goals.py:268-283): PUT_DOWN events are resolved
-// by the whole warp (warp_put_event), one env at a time.
-__device__ XMG_RARE int agent_rules(View vw, const uint32_t* rules, int nr, int ev, int H, int W, int ar, int ac,
-                                        int pocket) {
-  for (int s = 0; s < nr; ++s) {
-    const uint32_t rw = rules[s];
+// (ref:rules.py:60-72, ref:goals.py:268-283): PUT_DOWN events are queued and
+// resolved by step_rare (warp_put_event).
+__device__ XMG_RARE int agent_rules(View vw, const uint32_t* rules, uint32_t slots, int ev, int H, int W, int ar,
+                                    int ac, int pocket) {
+  for (; slots; slots &= slots - 1) {  // only the slots gated on this event, in stored order
+    const uint32_t rw = rules[__ffs(slots) - 1];
     const int kind = rw & 0xff, a = (rw >> 8) & 0xff, out = rw >> 24;
     if (kind == 0 || kind > 11 || !((cRuleGate[kind] >> ev) & 1)) continue;
     if (kind == 1) {  // AGENT_HOLD
@@ -272,37 +247,6 @@ __device__ bool agent_goal(const View& vw, uint32_t goal, int ev, int H, int W, 
     }
     default: return false;
   }
-}
-
-// Warp-wide scan of grid G for the first cell (row-major) holding `a` that
-// has a neighbour `b` at one of the offsets (NEAR_OFFSETS order for `all4`,
-// else the single offset (odr, odc)).  Returns the cell (or -1) and its
-// neighbour on every lane.  ref:rules.py:192-213 / ref:goals.py:380-394.
-__device__ __forceinline__ int warp_tile_scan(const uint8_t* G, int H, int W, int lane, int a, int b, bool all4,
-                                              int odr, int odc, int& nb_out) {
-  const int HW = H * W;
-  for (int base = 0; base < HW; base += 32) {
-    const int pos = base + lane;
-    int nb = -1;
-    if (pos < HW && G[pos] == a) {
-      const int r = pos / W, c = pos - (pos / W) * W;
-      for (int k = 0; k < (all4 ? 4 : 1); ++k) {
-        const int nr_ = r + (all4 ? near_dr(k) : odr), nc_ = c + (all4 ? near_dc(k) : odc);
-        if (nr_ >= 0 && nr_ < H && nc_ >= 0 && nc_ < W && G[nr_ * W + nc_] == b) {
-          nb = nr_ * W + nc_;
-          break;
-        }
-      }
-    }
-    const uint32_t m = __ballot_sync(0xffffffffu, nb >= 0);
-    if (m) {
-      const int win = __ffs(m) - 1;
-      nb_out = __shfl_sync(0xffffffffu, nb, win);
-      return base + win;
-    }
-  }
-  nb_out = -1;
-  return -1;
 }
 
 // ------------------------------------------------------- observation
@@ -542,33 +486,31 @@ __device__ void rank_place(const WarpScratch& ws, int lane, int F, int W, int mo
   __syncwarp();
 }
 
-// Rebuild one env's trial from the episode key ek: ref:vecenv.py:224-233
-// (ks = split(ek, 0), next state key = split(ek, 1)) and the scenario
-// builders ref:scenarios.py:291-412 (batched: ref:vecenv.py:242-291).
-// Called by all 32 lanes with the same arguments; writes the new grid to
-// `gdst` and returns the new pose / goal / task on every lane.
-__device__ XMG_RARE ResetOut warp_reset(const xmg_env_desc* dp, uint8_t* wbase, int hwp, int lg, int lane,
-                                            uint64_t ek_hi, uint64_t ek_lo, int task_in, uint32_t goal_in,
-                                            uint8_t* gdst) {
+// Every key a trial reset consumes, derived from the episode key ek:
+// ref:vecenv.py:224-227 (ks = split(ek, 0), next state key st = split(ek, 1))
+// and ref:scenarios.py:293,344,363,376 (k0, k1, k2 = split(ks, 3)); see
+// warp_trial_keys.
+struct TrialKeys {
+  uint64_t st_hi, st_lo, k0h, k0l, k1h, k1l, k2h, k2l, task_word;
+};
+
+// Rebuild one env's trial with the scenario builders ref:scenarios.py:291-412
+// (batched: ref:vecenv.py:242-291).  Called by all 32 lanes with the same
+// arguments; writes the new grid to `gdst` (and leaves it in ws.grid) and
+// returns the new pose / goal / task on every lane.
+__device__ XMG_RARE ResetOut warp_build(const xmg_env_desc* dp, uint8_t* wbase, int hwp, int lg, int lane,
+                                        const TrialKeys& key, int task_in, uint32_t goal_in, uint8_t* gdst) {
   const xmg_env_desc& d = *dp;  // CTA copy in shared memory
   const WarpScratch ws = make_scratch(wbase, hwp, lg);
   const int H = d.height, W = d.width, HW = H * W;
   const int sc = d.scenario;
-  // ks (lane 0), the next state key (lane 1), the task-resampling key (lane 2)
-  Words4 kw = {0, 0, 0, 0};
-  if (lane < 3) kw = philox((uint64_t)lane, 0, kDomSplit, 0, ek_hi, ek_lo);
-  const uint64_t ks_hi = shfl64(kw.w0, 0), ks_lo = shfl64(kw.w1, 0);
   ResetOut res;
-  res.st_hi = shfl64(kw.w0, 1);
-  res.st_lo = shfl64(kw.w1, 1);
+  res.st_hi = key.st_hi;
+  res.st_lo = key.st_lo;
   res.goal = goal_in;
   res.task = task_in;
   if (d.resample_tasks && sc == XMG_SCENARIO_XLAND) {
-    // extension (not in the reference): draw a fresh task per trial as
-    // Benchmark.sample_ruleset(split(ek, 2)) = rows[word0 % M] (ref:benchio.py:57-58)
-    Words4 tw = {0, 0, 0, 0};
-    if (lane == 2) tw = philox(0, 0, kDomDraw, 0, kw.w0, kw.w1);
-    res.task = (int)(shfl64(tw.w0, 2) % (uint64_t)d.num_tasks);
+    res.task = (int)(key.task_word % (uint64_t)d.num_tasks);
     res.goal = d.task_rows[(int64_t)res.task * d.row_words];
   }
   const uint32_t* row = d.task_rows + (int64_t)res.task * d.row_words;
@@ -579,14 +521,10 @@ __device__ XMG_RARE ResetOut warp_reset(const xmg_env_desc* dp, uint8_t* wbase, 
     for (int i = lane; i < HW; i += 32) gdst[i] = ws.grid[i];
     res.r = 1; res.c = 1; res.d = 1;
     res.goal = 2u | ((uint32_t)kGreenGoal << 8);
+    __syncwarp();
     return res;
   }
-  // k0, k1, k2 = split(ks, 3): doors/wall, cells/objects, agent
-  Words4 sk = {0, 0, 0, 0};
-  if (lane < 3) sk = philox((uint64_t)lane, 0, kDomSplit, 0, ks_hi, ks_lo);
-  const uint64_t k0h = shfl64(sk.w0, 0), k0l = shfl64(sk.w1, 0);
-  const uint64_t k1h = shfl64(sk.w0, 1), k1l = shfl64(sk.w1, 1);
-  const uint64_t k2h = shfl64(sk.w0, 2), k2l = shfl64(sk.w1, 2);
+  const uint64_t k0h = key.k0h, k0l = key.k0l, k1h = key.k1h, k1l = key.k1l, k2h = key.k2h, k2l = key.k2l;
 
   int wall_col = -1, color = 0;
   const bool two_rooms = sc == XMG_SCENARIO_DOOR_KEY || sc == XMG_SCENARIO_UNLOCK || sc == XMG_SCENARIO_UNLOCK_PICKUP;
@@ -627,7 +565,7 @@ __device__ XMG_RARE ResetOut warp_reset(const xmg_env_desc* dp, uint8_t* wbase, 
     const uint8_t* objs;
     if (sc == XMG_SCENARIO_XLAND) {  // ref:vecenv.py:261-279
       nobj = (row[1] >> 8) & 0xff;
-      objs = reinterpret_cast<const uint8_t*>(row + 2 + d.rule_width);
+      objs = reinterpret_cast<const uint8_t*>(row + kRowHeader + d.rule_width);
     } else if (sc == XMG_SCENARIO_FOUR_ROOMS) {  // ref:scenarios.py:361-370
       objs_local[0] = kGreenGoal;
       objs = objs_local;
@@ -675,7 +613,35 @@ __device__ XMG_RARE ResetOut warp_reset(const xmg_env_desc* dp, uint8_t* wbase, 
   return res;
 }
 
-// ------------------------------------------------------- the fused step
+// ------------------------------------------------------- the step: two kernels
+// step_main (one thread per env, streaming) applies the action, the
+// agent-relative rules / goals of MOVE and PICK_UP, the counters, reward and
+// observation of every env, and defers the two rare cases into a work queue:
+//   * PUT_DOWN events (grid-wide TILE_NEAR rules / goals, ref:rules.py:60-72),
+//   * finished trials (auto-reset, ref:vecenv.py:359-361).
+// step_rare (one warp per queued env) drains the queue: the PUT_DOWN rule
+// pass + goal + reward, the trial rebuild, and the observation of every env
+// it touched.  Both run back to back on the caller's stream.
+//
+// Work queues (state.work, xmg_work_words(n) u32): a PUT_DOWN queue and a
+// reset queue, each split in kQueues sub-queues fed by the CTAs with
+// blockIdx % kQueues == k (spreads the atomics).  Counts are double-buffered
+// by step parity: step t appends to counts[t & 1] while its CTA 0 clears
+// counts[(t + 1) & 1] (consumed by the previous step), so no kernel ever
+// waits for another.  Layout: counts [2 parities][2 kinds][kQueues], then the
+// PUT entries (kQueues x queue_cap) and the reset entries (kQueues x queue_cap).
+constexpr int kQueues = 128;
+constexpr int kWorkHeader = 4 * kQueues;
+__host__ __device__ inline int count_index(uint32_t parity, int kind, int q) {
+  return (int)((parity & 1) * 2 * kQueues + kind * kQueues + q);
+}
+constexpr uint32_t kQPut = 1u << 31, kQReset = 1u << 30, kQEnv = (1u << 30) - 1;
+
+__host__ __device__ inline int64_t queue_cap(int64_t n) {
+  const int64_t blocks = (n + kThreads - 1) / kThreads;
+  return (blocks + kQueues - 1) / kQueues * kThreads;
+}
+
 __device__ __forceinline__ int load_action(const void* a, int dtype, int64_t e) {
   switch (dtype) {
     case XMG_ACT_U8: return reinterpret_cast<const uint8_t*>(a)[e];
@@ -689,156 +655,111 @@ __device__ __forceinline__ uint64_t pack_agent(int r, int c, int d, int pocket, 
          ((uint64_t)(uint32_t)pocket << 24) | ((uint64_t)sc << 32);
 }
 
-// One PUT_DOWN event resolved by the whole warp on a shared-memory copy G of
-// the env's grid: the rule pass (ref:rules.py:162-213, event PUT_DOWN) and
-// then the goal check (ref:goals.py:347-394).  The pocket is untouched
-// (AGENT_HOLD is gated on PICK_UP).  Writes the grid back when a rule fired;
-// returns the goal predicate on every lane.
-__device__ XMG_RARE int warp_put_event(uint8_t* G, int lane, uint8_t* genv, int H, int W, int ar, int ac,
-                                           const uint32_t* rules, int nr, uint32_t goal) {
-  const int HW = H * W;
-  bool dirty;
-  for (int i = lane; i < HW; i += 32) G[i] = genv[i];
-  __syncwarp();
-  dirty = false;
-  for (int s = 0; s < nr; ++s) {
-    const uint32_t rw = rules[s];
-    const int kind = rw & 0xff, a = (rw >> 8) & 0xff, b = (rw >> 16) & 0xff, out = rw >> 24;
-    if (kind == 0 || kind > 11 || !((cRuleGate[kind] >> 2) & 1)) continue;
-    if (kind == 2 || kind >= 8) {  // agent-near family: every lane evaluates the same cells
-      int tgt = -1;
-      if (kind == 2) {
-        for (int k = 0; k < 4; ++k) {
-          const int r = ar + near_dr(k), c = ac + near_dc(k);
-          if (r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a) { tgt = r * W + c; break; }
-        }
-      } else {
-        const int r = ar + dir_dr(kind - 8), c = ac + dir_dc(kind - 8);
-        if (r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a) tgt = r * W + c;
-      }
-      __syncwarp();
-      if (tgt >= 0) {
-        if (lane == 0) G[tgt] = (uint8_t)out;
-        dirty = true;
-      }
-      __syncwarp();
-    } else {  // TILE_NEAR (3) / TILE_NEAR_{UP,RIGHT,DOWN,LEFT} (4..7)
-      int nb;
-      const int pos = warp_tile_scan(G, H, W, lane, a, b, kind == 3, dir_dr(kind - 4), dir_dc(kind - 4), nb);
-      if (pos >= 0) {
-        if (lane == 0) {
-          G[pos] = (uint8_t)out;
-          G[nb] = kFloorCode;
-        }
-        dirty = true;
-      }
-      __syncwarp();
-    }
-  }
-  bool hit = false;
-  const int kind = goal & 0xff, a1 = (goal >> 8) & 0xff, a2 = (goal >> 16) & 0xff, a3 = goal >> 24;
-  if (kind != 0 && kind <= 14 && ((cGoalGate[kind] >> 2) & 1)) {
-    switch (kind) {
-      case 2: hit = G[ar * W + ac] == a1; break;
-      case 5: hit = ar == a1 && ac == a2; break;
-      case 6: hit = a2 < H && a3 < W && G[a2 * W + a3] == a1; break;
-      case 3:
-        for (int k = 0; k < 4; ++k) {
-          const int r = ar + near_dr(k), c = ac + near_dc(k);
-          hit |= r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a1;
-        }
-        break;
-      case 11: case 12: case 13: case 14: {
-        const int r = ar + dir_dr(kind - 11), c = ac + dir_dc(kind - 11);
-        hit = r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a1;
-        break;
-      }
-      default: {  // TILE_NEAR (4), TILE_NEAR_{UP,RIGHT,DOWN,LEFT} (7..10)
-        int nb;
-        hit = warp_tile_scan(G, H, W, lane, a1, a2, kind == 4, dir_dr(kind - 7), dir_dc(kind - 7), nb) >= 0;
-      }
-    }
-  }
-  if (dirty)
-    for (int i = lane; i < HW; i += 32) genv[i] = G[i];
-  __syncwarp();
-  return (int)hit | ((int)dirty << 1);
+// float32(1.0 - 0.9 * (sc / budget)) in IEEE double without contraction
+// (ref:env.py:204, ref:vecenv.py:355)
+__device__ __forceinline__ float goal_reward(uint32_t sc, int budget) {
+  const double frac = __ddiv_rn((double)sc, (double)budget);
+  return __double2float_rn(__dsub_rn(1.0, __dmul_rn(0.9, frac)));
 }
 
-// Copy the staged range of grid G into lane `src`'s window stage (warp-wide).
-__device__ __forceinline__ void restage_from(const uint8_t* G, uint8_t* ostage, int sbase, int slo, int shi,
-                                             int lane) {
-  for (int f = slo + lane; f < shi; f += 32) ostage[f - sbase] = G[f];
+// Per-CTA episode statistics slot (ref RolloutStats, harness.py:314-354).
+__device__ __forceinline__ void warp_stats(double* stats, int slot, double rs, double trl, double ln) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    rs += __shfl_down_sync(0xffffffffu, rs, off);
+    trl += __shfl_down_sync(0xffffffffu, trl, off);
+    ln += __shfl_down_sync(0xffffffffu, ln, off);
+  }
+  if ((threadIdx.x & 31) == 0 && trl + rs > 0.0) {
+    atomicAdd(stats + 3 * slot, rs);
+    atomicAdd(stats + 3 * slot + 1, trl);
+    atomicAdd(stats + 3 * slot + 2, ln);
+  }
+}
+
+struct MainGeo {
+  int ob, stg, rb;
+  int64_t total;
+};
+
+__host__ __device__ inline MainGeo make_main_geo(int V, int maxch, int R) {
+  MainGeo g;
+  g.ob = 2 * V * V;
+  g.stg = 16 * maxch + 16;
+  g.rb = 16 * ((kRowHeader + R + 3) / 4);
+  g.total = (int64_t)kThreads * (g.stg + g.rb) + (int64_t)kWarps * round16(32 * g.ob);
+  return g;
+}
+
+// abort iff *flag == epoch: xmg_validate_actions tags a rejected batch with
+// the epoch of its step (atomicMax), so the flag never needs clearing.
+__device__ __forceinline__ bool batch_rejected(const uint32_t* flag, uint32_t epoch) {
+  return flag != nullptr && *reinterpret_cast<volatile const uint32_t*>(flag) == epoch;
 }
 
 template <int MAXCH>
-__global__ void __launch_bounds__(kThreads, XMG_MINB) step_kernel(const xmg_env_desc d, const xmg_state s,
-                                                                  const xmg_out o, const void* actions, int act_dtype,
-                                                                  const uint64_t* reset_keys,
-                                                                  const int32_t* abort_flag, int64_t n) {
+__global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_desc d, const xmg_state s,
+                                                                const xmg_out o, const void* actions, int act_dtype,
+                                                                const uint32_t* abort_flag, uint32_t epoch,
+                                                                int64_t n) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ xmg_env_desc sdesc;  // for the out-of-line rare paths (no local copies)
-  if (abort_flag != nullptr && *reinterpret_cast<volatile const int32_t*>(abort_flag) != 0) return;
-  if (threadIdx.x == 0) sdesc = d;
-  __syncthreads();
+  // clear the counts the previous step consumed; this step appends to the others
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < 2 * kQueues; i += blockDim.x) s.work[count_index(epoch + 1, 0, 0) + i] = 0;
+  if (batch_rejected(abort_flag, epoch)) return;
 
   const int H = d.height, W = d.width, HW = H * W, V = d.view_size, R = d.rule_width;
-  const Geo geo = make_geo(H, W, V, MAXCH, R);
+  const MainGeo geo = make_main_geo(V, MAXCH, R);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t e0 = (int64_t)blockIdx.x * kThreads;
   const int64_t e = e0 + tid;
   const bool valid = e < n;
-  const bool reset_mode = reset_keys != nullptr;
 
-  uint8_t* stage_base = smem;
-  uint8_t* rb_base = stage_base + kThreads * geo.stg;
-  uint8_t* wbase = rb_base + kThreads * geo.rb + warp * geo.ws;
+  uint8_t* rb_base = smem + kThreads * geo.stg;
+  uint8_t* obs_stage = rb_base + kThreads * geo.rb + warp * round16(32 * geo.ob);
   View vw;
   vw.g = s.grids + (valid ? e : 0) * (int64_t)HW;
-  vw.stage = MAXCH ? stage_base + tid * geo.stg : nullptr;
+  vw.stage = smem + tid * geo.stg;
   vw.sbase = vw.slo = vw.shi = 0;
   uint32_t* rbuf = reinterpret_cast<uint32_t*>(rb_base + tid * geo.rb);
-  const WarpScratch ws = make_scratch(wbase, geo.hwp, geo.lg);
 
   // ---- load: the 16-byte state word and the action
   ulonglong2 ag = make_ulonglong2(0, 0);
   int act = 1;
   if (valid) {
     ag = reinterpret_cast<const ulonglong2*>(s.agent)[e];
-    if (!reset_mode) act = load_action(actions, act_dtype, e);
+    act = load_action(actions, act_dtype, e);
   }
   int r = (int)(ag.x & 0xff), c = (int)((ag.x >> 8) & 0xff), dir = (int)((ag.x >> 16) & 3);
   int pocket = (int)((ag.x >> 24) & 0xff);
   uint32_t sc = (uint32_t)(ag.x >> 32);
-  uint32_t goal_word = (uint32_t)ag.y;
-  int task = (int)(ag.y >> 32);
+  const uint32_t goal_word = (uint32_t)ag.y;
+  const int task = (int)(ag.y >> 32);
 
-  float rew = 0.f, disc = 1.f;
-  int8_t stype = 0;
-  bool last = reset_mode, goal = false, word1_dirty = false;
-  uint32_t done_len = 0;  // length of the trial that just ended (stats)
-  int ev = -1, nr = 0;
-
-  if (valid && !reset_mode) {
+  uint32_t qflags = 0;
+  float rew = 0.f;
+  bool last = false;
+  if (valid) {
     // ---- stage the post-action window (MOVE: both candidate poses) and,
     // for actions that can raise an event, the env's rule row
     const int nd = act == 1 ? ((dir + 3) & 3) : (act == 2 ? ((dir + 1) & 3) : dir);
     int lo, hi;
     window_span(r, c, nd, act == 0 ? 1 : 0, H, W, V, lo, hi);
     stage_issue<MAXCH>(vw, lo, hi, HW);
-    const bool may_event = act == 0 || act == 3 || act == 4;
-    if (R > 0 && may_event) {
+    const bool rules_needed = R > 0 && (act == 0 || act == 3);
+    if (rules_needed) {
       const uint32_t* src = d.task_rows + (int64_t)task * d.row_words;
-      const int nq = (2 + R + 3) >> 2;
+      const int nq = (kRowHeader + R + 3) >> 2;
       for (int q = 0; q < nq; ++q) cp_async16(rbuf + 4 * q, src + 4 * q);
     }
-    if (MAXCH || (R > 0 && may_event)) cp_async_wait_all();
+    cp_async_wait_all();
 
     // ---- action, ref:vecenv.py:306-342 / ref:env.py:148-191
     const int tr = r + dir_dr(dir), tc = c + dir_dc(dir);
     const bool inside = tr >= 0 && tr < H && tc >= 0 && tc < W;
     const int tflat = tr * W + tc;
     const int tcode = inside ? vw.rd(tflat) : 0, tt = tcode >> 4;
+    int ev = -1;
     switch (act) {
       case 0:
         if (inside && ((kWalkable >> tt) & 1)) { r = tr; c = tc; ev = 0; }
@@ -863,131 +784,66 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_kernel(const xmg_env_
           }
         }
     }
-    // ---- rules and goal after MOVE / PICK_UP (ref:vecenv.py:344-349);
-    // TOGGLE gates no rule and no goal; PUT_DOWN is resolved warp-wide below.
-    if (R > 0 && ev >= 0 && ev <= 2) nr = rbuf[1] & 0xff;
+    // ---- MOVE / PICK_UP: agent-relative rules (only the slots their event
+    // gates, in stored order) and goal; TOGGLE gates no rule and no goal.
+    bool goal = false;
     if (ev == 0 || ev == 1) {
-      if (nr) pocket = agent_rules(vw, rbuf + 2, nr, ev, H, W, r, c, pocket);
+      const int nr = R > 0 ? (int)(rbuf[1] & 0xff) : 0;
+      if (nr && R > 32) {
+        for (int s0 = 0; s0 < nr; s0 += 32)
+          pocket = agent_rules(vw, rbuf + kRowHeader + s0, nr - s0 >= 32 ? 0xffffffffu : (1u << (nr - s0)) - 1u, ev,
+                               H, W, r, c, pocket);
+      } else if (nr) {
+        const uint32_t slots = rbuf[2 + ev];
+        if (slots) pocket = agent_rules(vw, rbuf + kRowHeader, slots, ev, H, W, r, c, pocket);
+      }
       goal = agent_goal(vw, goal_word, ev, H, W, r, c, pocket);
     }
-  }
-
-  // ---- PUT_DOWN events: grid-wide rules and goals, one env at a time per warp
-  uint32_t pmask = __ballot_sync(0xffffffffu, ev == 2);
-  if (pmask) {
-    __syncwarp();  // the owners' PUT writes (global) and rule rows (smem) are visible
-    while (pmask) {
-      const int src = __ffs(pmask) - 1;
-      pmask &= pmask - 1;
-      const int ar = __shfl_sync(0xffffffffu, r, src), ac = __shfl_sync(0xffffffffu, c, src);
-      const uint32_t gw = __shfl_sync(0xffffffffu, goal_word, src);
-      const int nrs = __shfl_sync(0xffffffffu, nr, src);
-      const uint32_t* rules_s = reinterpret_cast<const uint32_t*>(rb_base + (warp * 32 + src) * geo.rb) + 2;
-      uint8_t* genv = s.grids + (e0 + warp * 32 + src) * (int64_t)HW;
-      const int res = warp_put_event(ws.grid, lane, genv, H, W, ar, ac, rules_s, nrs, gw);
-      const bool hit = res & 1;
-      if (MAXCH && (res & 2)) {
-        const int sb = __shfl_sync(0xffffffffu, vw.sbase, src);
-        const int slo = __shfl_sync(0xffffffffu, vw.slo, src), shi = __shfl_sync(0xffffffffu, vw.shi, src);
-        restage_from(ws.grid, stage_base + (warp * 32 + src) * geo.stg, sb, slo, shi, lane);
-        __syncwarp();
-      }
-      if (lane == src) goal = hit;
-    }
-  }
-
-  if (valid && !reset_mode) {
-    // ---- counters and reward, ref:vecenv.py:351-357 (fp64, no contraction)
+    // ---- counters and reward, ref:vecenv.py:351-357
     sc += 1;
-    last = goal || sc >= (uint32_t)d.budget;
-    done_len = last ? sc : 0;
-    if (goal) {
-      const double frac = __ddiv_rn((double)sc, (double)d.budget);
-      rew = __double2float_rn(__dsub_rn(1.0, __dmul_rn(0.9, frac)));
+    if (ev == 2) {
+      qflags = kQPut;  // rules, goal and reward resolved by step_rare
+    } else {
+      last = goal || sc >= (uint32_t)d.budget;
+      if (goal) rew = goal_reward(sc, d.budget);
+      o.reward[e] = rew;
+      o.discount[e] = last ? 0.f : 1.f;
+      o.step_type[e] = last ? 2 : 1;
+      if (last) qflags = kQReset;
     }
-    disc = last ? 0.f : 1.f;
-    stype = last ? 2 : 1;
+    s.agent[2 * e] = pack_agent(r, c, dir, pocket, sc);
   }
 
-  // ---- auto-reset: every finished env is rebuilt by its whole warp
-  uint32_t rmask = __ballot_sync(0xffffffffu, valid && last);
-  if (rmask) {
-    uint64_t ek_hi = 0, ek_lo = 0;
-    if (valid && last) {
-      const ulonglong2 k = reinterpret_cast<const ulonglong2*>(reset_mode ? reset_keys : s.rng)[e];
-      ek_hi = k.x;
-      ek_lo = k.y;
-    }
-    while (rmask) {
-      const int src = __ffs(rmask) - 1;
-      rmask &= rmask - 1;
-      const uint64_t hi = shfl64(ek_hi, src), lo = shfl64(ek_lo, src);
-      const int t = __shfl_sync(0xffffffffu, task, src);
-      const uint32_t g_in = __shfl_sync(0xffffffffu, goal_word, src);
-      uint8_t* gdst = s.grids + (e0 + warp * 32 + src) * (int64_t)HW;
-      const ResetOut ro = warp_reset(&sdesc, wbase, geo.hwp, geo.lg, lane, hi, lo, t, g_in, gdst);
-      if (MAXCH) {
-        // restage the owner's window straight from the scratch grid
-        int lo2, hi2;
-        window_span(ro.r, ro.c, ro.d, 0, H, W, V, lo2, hi2);
-        const uintptr_t gsrc = reinterpret_cast<uintptr_t>(gdst);
-        const uintptr_t a0 = (gsrc + lo2) & ~uintptr_t(15);
-        const int sbase = (int)(a0 - gsrc);
-        const int nch = (int)(((gsrc + hi2) - a0 + 15) >> 4);
-        const int slo = max(sbase, 0), shi = min(sbase + 16 * nch, HW);
-        restage_from(ws.grid, stage_base + (warp * 32 + src) * geo.stg, sbase, slo, shi, lane);
-        if (lane == src) {
-          vw.sbase = sbase;
-          vw.slo = slo;
-          vw.shi = shi;
-        }
-      }
-      __syncwarp();
-      if (lane == src) {
-        r = ro.r; c = ro.c; dir = ro.d; pocket = 0; sc = 0;
-        goal_word = ro.goal;
-        task = ro.task;
-        word1_dirty = true;
-        reinterpret_cast<ulonglong2*>(s.rng)[e] = make_ulonglong2(ro.st_hi, ro.st_lo);
-      }
-    }
-  }
-
-  // ---- per-env outputs (coalesced)
-  if (valid) {
-    const uint64_t w0 = pack_agent(r, c, dir, pocket, sc);
-    if (word1_dirty)
-      reinterpret_cast<ulonglong2*>(s.agent)[e] =
-          make_ulonglong2(w0, (uint64_t)goal_word | ((uint64_t)(uint32_t)task << 32));
-    else
-      s.agent[2 * e] = w0;
-    o.reward[e] = rew;
-    o.discount[e] = disc;
-    o.step_type[e] = stype;
-  }
-
-  // ---- episode statistics: warp sums, one slot per CTA (ref RolloutStats)
-  if (o.stats != nullptr && !reset_mode) {
-    double rs = valid ? (double)rew : 0.0, trl = (valid && last) ? 1.0 : 0.0, ln = (double)done_len;
+  // ---- defer the rare work: warp-aggregated append to this CTA's sub-queue
+  const uint32_t qm = __ballot_sync(0xffffffffu, qflags != 0);
+  if (qm) {
+    const int k = blockIdx.x % kQueues;
+    // PUT_DOWN and reset entries go to their own queues
 #pragma unroll
-    for (int off = 16; off; off >>= 1) {
-      rs += __shfl_down_sync(0xffffffffu, rs, off);
-      trl += __shfl_down_sync(0xffffffffu, trl, off);
-      ln += __shfl_down_sync(0xffffffffu, ln, off);
-    }
-    if (lane == 0 && trl + rs > 0.0) {
-      atomicAdd(o.stats + 3 * blockIdx.x, rs);
-      atomicAdd(o.stats + 3 * blockIdx.x + 1, trl);
-      atomicAdd(o.stats + 3 * blockIdx.x + 2, ln);
+    for (int kind = 0; kind < 2; ++kind) {
+      const uint32_t want = kind ? kQReset : kQPut;
+      const uint32_t km = __ballot_sync(0xffffffffu, qflags == want);
+      if (!km) continue;
+      const int leader = __ffs(km) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(s.work + count_index(epoch, kind, k), (uint32_t)__popc(km));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (qflags == want) {
+        const int64_t slot = (int64_t)(kind * kQueues + k) * queue_cap(n) + base + __popc(km & ((1u << lane) - 1));
+        s.work[kWorkHeader + slot] = (uint32_t)e;
+      }
     }
   }
+
+  // ---- episode statistics of the trials decided here
+  if (o.stats != nullptr) warp_stats(o.stats, blockIdx.x, rew, last ? 1.0 : 0.0, last ? (double)sc : 0.0);
 
   // ---- observation: assembled in smem, one TMA bulk store per warp
+  // (envs queued for step_rare get theirs rewritten there)
   if (o.obs != nullptr) {
-    uint8_t* wsrc = wbase;  // this warp's scratch, free once resets / PUT events are done
     if (valid) {
-      uint8_t* dst = wsrc + lane * geo.ob;
-      if (MAXCH && d.see_through_walls) {
+      uint8_t* dst = obs_stage + lane * geo.ob;
+      if (d.see_through_walls) {
         if (V == 5) obs_see<5>(vw.stage, vw.sbase, dst, r, c, dir, H, W, V);
         else obs_see<0>(vw.stage, vw.sbase, dst, r, c, dir, H, W, V);
       } else {
@@ -1002,13 +858,367 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_kernel(const xmg_env_
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0 && bulk) {
-      const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(wsrc);
+      const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(obs_stage);
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                    ::"l"(gdst), "r"(saddr), "r"(bulk) : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
-    for (uint32_t k = bulk + lane; k < bytes; k += 32) gdst[k] = wsrc[k];
+    for (uint32_t k = bulk + lane; k < bytes; k += 32) gdst[k] = obs_stage[k];
     if (lane == 0 && bulk) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
+// ------------------------------------------------------- step_rare
+// Observation of pose (r, c, d) on a shared-memory grid copy G, by one lane
+// (lane_obs) or one view cell per lane (warp_obs), written straight to the
+// env's (v, v, 2) record.
+__device__ __forceinline__ uint16_t obs_cell(const uint8_t* G, int r, int c, int d, int H, int W, int V, int cell,
+                                             bool see) {
+  const int h = V / 2;
+  const int fr = dir_dr(d), fc = dir_dc(d), rr = fc, rc = -fr;
+  const int i = cell / V, j = cell - (cell / V) * V;
+  const int ahead = V - 1 - i, lat = j - h;
+  const int wr = r + ahead * fr + lat * rr, wc = c + ahead * fc + lat * rc;
+  if (wr < 0 || wr >= H || wc < 0 || wc >= W) return 0;
+  if (!see) {
+    View vw;  // grid fully staged: stage == G, range [0, HW)
+    vw.g = nullptr;
+    vw.stage = const_cast<uint8_t*>(G);
+    vw.sbase = 0;
+    vw.slo = 0;
+    vw.shi = H * W;
+    if (!cell_visible(vw, W, r, c, wr, wc)) return 1 | (1 << 8);  // (UNSEEN, UNSEEN)
+  }
+  const int code = G[wr * W + wc];
+  return (uint16_t)((code >> 4) | ((code & 15) << 8));
+}
+
+__device__ __forceinline__ void warp_obs(const uint8_t* G, uint8_t* gobs, int lane, int r, int c, int d, int H, int W,
+                                         int V, bool see) {
+  for (int cell = lane; cell < V * V; cell += 32)
+    reinterpret_cast<uint16_t*>(gobs)[cell] = obs_cell(G, r, c, d, H, W, V, cell, see);
+}
+
+// ------------------------------------------------------- bit-parallel grids
+// Cell p of an env's grid is bit (p & 31) of word (p >> 5); lane k of a warp
+// holds word k of a bitmap (lanes >= K hold 0).  One ballot builds a word,
+// neighbour relations are multiword shifts done with shuffles.
+__device__ __forceinline__ uint32_t shl_cells(uint32_t x, int s, int lane) {  // bit p <- bit p - s
+  const int q = s >> 5, r = s & 31;
+  uint32_t hi = __shfl_up_sync(0xffffffffu, x, q);
+  uint32_t lo = __shfl_up_sync(0xffffffffu, x, q + 1);
+  if (lane < q) hi = 0;
+  if (lane < q + 1) lo = 0;
+  return r ? ((hi << r) | (lo >> (32 - r))) : hi;
+}
+
+__device__ __forceinline__ uint32_t shr_cells(uint32_t x, int s, int lane) {  // bit p <- bit p + s
+  const int q = s >> 5, r = s & 31;
+  uint32_t lo = __shfl_down_sync(0xffffffffu, x, q);
+  uint32_t hi = __shfl_down_sync(0xffffffffu, x, q + 1);
+  if (lane + q > 31) lo = 0;
+  if (lane + q + 1 > 31) hi = 0;
+  return r ? ((lo >> r) | (hi << (32 - r))) : lo;
+}
+
+template <int KMAX>
+struct Cells {
+  int code[KMAX];  // code[k] = G[32k + lane], 0x100 beyond the grid
+};
+
+template <int KMAX>
+__device__ __forceinline__ void cells_load(Cells<KMAX>& cl, const uint8_t* G, int HW, int lane) {
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    const int p = 32 * k + lane;
+    cl.code[k] = p < HW ? (int)G[p] : 0x100;
+  }
+}
+
+template <int KMAX>
+__device__ __forceinline__ void cells_set(Cells<KMAX>& cl, int p, int v, int lane) {
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k)
+    if (k == (p >> 5) && lane == (p & 31)) cl.code[k] = v;
+}
+
+// First cell p (row-major) holding `a` with `b` at the neighbour given by
+// `dir` (0 up, 1 right, 2 down, 3 left, -1: the first of NEAR_OFFSETS up,
+// left, right, down) -- ref:rules.py:192-213, ref:goals.py:380-394.  Returns
+// p (or -1) and the neighbour cell on every lane.
+template <int KMAX>
+__device__ __forceinline__ int bit_tile_scan(const Cells<KMAX>& cl, int lane, int a, int b, int dir, int W,
+                                             uint32_t col0, uint32_t colL, int& nb) {
+  uint32_t am = 0, bm = 0;
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    const uint32_t x = __ballot_sync(0xffffffffu, cl.code[k] == a);
+    const uint32_t y = __ballot_sync(0xffffffffu, cl.code[k] == b);
+    if (lane == k) {
+      am = x;
+      bm = y;
+    }
+  }
+  nb = -1;
+  if (!__any_sync(0xffffffffu, am != 0)) return -1;
+  const uint32_t up = am & shl_cells(bm, W, lane);             // b at p - W
+  const uint32_t left = am & shl_cells(bm, 1, lane) & ~col0;   // b at p - 1, same row
+  const uint32_t right = am & shr_cells(bm, 1, lane) & ~colL;  // b at p + 1, same row
+  const uint32_t down = am & shr_cells(bm, W, lane);           // b at p + W
+  const uint32_t any = dir < 0 ? (up | left | right | down) : dir == 0 ? up : dir == 1 ? right : dir == 2 ? down : left;
+  const uint32_t wm = __ballot_sync(0xffffffffu, any != 0);
+  if (!wm) return -1;
+  const int k = __ffs(wm) - 1;
+  const int bit = __ffs(__shfl_sync(0xffffffffu, any, k)) - 1;
+  const int p = 32 * k + bit;
+  if (dir < 0) {
+    const bool u = (__shfl_sync(0xffffffffu, up, k) >> bit) & 1;
+    const bool l = (__shfl_sync(0xffffffffu, left, k) >> bit) & 1;
+    const bool rt = (__shfl_sync(0xffffffffu, right, k) >> bit) & 1;
+    nb = u ? p - W : l ? p - 1 : rt ? p + 1 : p + W;
+  } else {
+    nb = dir == 0 ? p - W : dir == 1 ? p + 1 : dir == 2 ? p + W : p - 1;
+  }
+  return p;
+}
+
+// One PUT_DOWN event of one env, resolved by the whole warp: the rule pass
+// (ref:rules.py:162-213, event PUT_DOWN) then the goal (ref:goals.py:347-394)
+// on the shared-memory grid copy G (+ its bitmap form in registers).
+// Rewritten cells go to G and through to the grid in global memory.
+// Returns goal | dirty << 1 on every lane.
+template <int KMAX>
+__device__ __forceinline__ int warp_put_event(uint8_t* G, Cells<KMAX>& cl, uint8_t* genv, int lane, int H, int W, int ar, int ac,
+                              const uint32_t* rules, int nr, uint32_t goal, uint32_t col0, uint32_t colL) {
+  bool dirty = false;
+  for (int s = 0; s < nr; ++s) {
+    const uint32_t rw = rules[s];
+    const int kind = rw & 0xff, a = (rw >> 8) & 0xff, b = (rw >> 16) & 0xff, out = rw >> 24;
+    if (kind == 0 || kind > 11 || !((cRuleGate[kind] >> 2) & 1)) continue;
+    int p = -1, q = -1;
+    if (kind == 2 || kind >= 8) {  // agent-near family: every lane evaluates the same cells
+      for (int k = 0; k < (kind == 2 ? 4 : 1); ++k) {
+        const int r = ar + (kind == 2 ? near_dr(k) : dir_dr(kind - 8));
+        const int c = ac + (kind == 2 ? near_dc(k) : dir_dc(kind - 8));
+        if (r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a) { p = r * W + c; break; }
+      }
+    } else {  // TILE_NEAR (3) / TILE_NEAR_{UP,RIGHT,DOWN,LEFT} (4..7)
+      p = bit_tile_scan<KMAX>(cl, lane, a, b, kind == 3 ? -1 : kind - 4, W, col0, colL, q);
+    }
+    if (p >= 0) {
+      __syncwarp();
+      if (lane == 0) {
+        G[p] = (uint8_t)out;
+        genv[p] = (uint8_t)out;
+        if (q >= 0) {
+          G[q] = kFloorCode;
+          genv[q] = kFloorCode;
+        }
+      }
+      cells_set<KMAX>(cl, p, out, lane);
+      if (q >= 0) cells_set<KMAX>(cl, q, kFloorCode, lane);
+      dirty = true;
+      __syncwarp();
+    }
+  }
+  bool hit = false;
+  const int kind = goal & 0xff, a1 = (goal >> 8) & 0xff, a2 = (goal >> 16) & 0xff, a3 = goal >> 24;
+  if (kind != 0 && kind <= 14 && ((cGoalGate[kind] >> 2) & 1)) {
+    switch (kind) {
+      case 2: hit = G[ar * W + ac] == a1; break;
+      case 5: hit = ar == a1 && ac == a2; break;
+      case 6: hit = a2 < H && a3 < W && G[a2 * W + a3] == a1; break;
+      case 3:
+        for (int k = 0; k < 4; ++k) {
+          const int r = ar + near_dr(k), c = ac + near_dc(k);
+          hit |= r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a1;
+        }
+        break;
+      case 11: case 12: case 13: case 14: {
+        const int r = ar + dir_dr(kind - 11), c = ac + dir_dc(kind - 11);
+        hit = r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a1;
+        break;
+      }
+      default: {  // TILE_NEAR (4), TILE_NEAR_{UP,RIGHT,DOWN,LEFT} (7..10)
+        int q;
+        hit = bit_tile_scan<KMAX>(cl, lane, a1, a2, kind == 4 ? -1 : kind - 7, W, col0, colL, q) >= 0;
+      }
+    }
+  }
+  return (int)hit | ((int)dirty << 1);
+}
+
+// The trial keys of one env derived by the warp in two levels (lanes 0-2,
+// then lanes 0-3): ref:vecenv.py:225-226, ref:scenarios.py:293.
+__device__ __forceinline__ TrialKeys warp_trial_keys(int lane, uint64_t ek_hi, uint64_t ek_lo, bool resample) {
+  Words4 w = {0, 0, 0, 0};
+  if (lane < 3) w = philox((uint64_t)lane, 0, kDomSplit, 0, ek_hi, ek_lo);  // ks, st, task key
+  const uint64_t ks_hi = shfl64(w.w0, 0), ks_lo = shfl64(w.w1, 0);
+  TrialKeys k;
+  k.st_hi = shfl64(w.w0, 1);
+  k.st_lo = shfl64(w.w1, 1);
+  const uint64_t tk_hi = shfl64(w.w0, 2), tk_lo = shfl64(w.w1, 2);
+  Words4 v = {0, 0, 0, 0};
+  if (lane < 3) v = philox((uint64_t)lane, 0, kDomSplit, 0, ks_hi, ks_lo);  // k0, k1, k2
+  else if (lane == 3 && resample) v = philox(0, 0, kDomDraw, 0, tk_hi, tk_lo);
+  k.k0h = shfl64(v.w0, 0); k.k0l = shfl64(v.w1, 0);
+  k.k1h = shfl64(v.w0, 1); k.k1l = shfl64(v.w1, 1);
+  k.k2h = shfl64(v.w0, 2); k.k2l = shfl64(v.w1, 2);
+  k.task_word = shfl64(v.w0, 3);
+  return k;
+}
+
+struct RareGeo {
+  int hwp, lg, ws, rbw;
+  int64_t total;
+};
+
+__host__ __device__ inline RareGeo make_rare_geo(int H, int W, int R) {
+  RareGeo g;
+  g.hwp = round16(H * W + 16);
+  g.lg = 5;
+  while ((1 << g.lg) < H * W) ++g.lg;
+  g.rbw = round16(4 * (kRowHeader + R));
+  // per warp: wd: u64[hwp] | fc: u16[hwp] | slot: u16[hwp] | bk: u32[2^lg] | grid: u8[hwp] | misc: 64 u64 | rules
+  g.ws = 8 * g.hwp + 2 * g.hwp + 2 * g.hwp + 4 * (1 << g.lg) + g.hwp + 512 + g.rbw;
+  g.total = (int64_t)kWarps * g.ws;
+  return g;
+}
+
+// Rebuild env e's trial (ref:vecenv.py:359-361 -> :224-291), whole warp.
+__device__ __forceinline__ void warp_reset_env(const xmg_env_desc& d, const xmg_env_desc* sd, const xmg_state& s,
+                                               const xmg_out& o, uint8_t* wbase, const RareGeo& geo, int lane,
+                                               int64_t e, uint64_t ek_hi, uint64_t ek_lo, int task, bool reset_mode) {
+  const int H = d.height, W = d.width, HW = H * W, V = d.view_size, ob = 2 * V * V;
+  const WarpScratch ws = make_scratch(wbase, geo.hwp, geo.lg);
+  const bool resample = d.resample_tasks && d.scenario == XMG_SCENARIO_XLAND;
+  const TrialKeys key = warp_trial_keys(lane, ek_hi, ek_lo, resample);
+  const uint32_t g_in = d.scenario == XMG_SCENARIO_XLAND ? d.task_rows[(int64_t)task * d.row_words] : 0u;
+  const ResetOut ro = warp_build(sd, wbase, geo.hwp, geo.lg, lane, key, task, g_in, s.grids + e * (int64_t)HW);
+  if (lane == 0) {
+    reinterpret_cast<ulonglong2*>(s.rng)[e] = make_ulonglong2(ro.st_hi, ro.st_lo);
+    reinterpret_cast<ulonglong2*>(s.agent)[e] = make_ulonglong2(
+        pack_agent(ro.r, ro.c, ro.d, 0, 0), (uint64_t)ro.goal | ((uint64_t)(uint32_t)ro.task << 32));
+    if (reset_mode) {
+      o.reward[e] = 0.f;
+      o.discount[e] = 1.f;
+      o.step_type[e] = 0;
+    }
+  }
+  if (o.obs != nullptr) warp_obs(ws.grid, o.obs + e * ob, lane, ro.r, ro.c, ro.d, H, W, V, d.see_through_walls != 0);
+  __syncwarp();
+}
+
+// step_rare drains the two queues step_main filled, one env per warp:
+//  * PUT_DOWN queue: the grid-wide rule pass, goal, reward (warp_put_event);
+//  * reset queue: the trial rebuild (warp_build).
+// Sub-queue q of each kind is served by the warps gw with gw % kQueues == q,
+// striding over its entries.  reset_keys != nullptr: reset mode (ref
+// VecEnv.reset_with_keys, vecenv.py:205-222), every env [0, n) rebuilt from
+// keys[e] with a FIRST record.
+template <int KMAX>
+__global__ void __launch_bounds__(kThreads, XMG_MINB_RARE) step_rare(const xmg_env_desc d, const xmg_state s,
+                                                                     const xmg_out o, const uint64_t* reset_keys,
+                                                                     const uint32_t* abort_flag, uint32_t epoch,
+                                                                     int64_t n) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ xmg_env_desc sdesc;  // read by the out-of-line paths without local copies
+  if (threadIdx.x == 0) sdesc = d;
+  __syncthreads();
+  if (batch_rejected(abort_flag, epoch)) return;
+  const int H = d.height, W = d.width, HW = H * W, V = d.view_size, ob = 2 * V * V, R = d.rule_width;
+  const RareGeo geo = make_rare_geo(H, W, R);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint8_t* wbase = smem + warp * geo.ws;
+  const WarpScratch ws = make_scratch(wbase, geo.hwp, geo.lg);
+  uint32_t* rules_s = reinterpret_cast<uint32_t*>(wbase + geo.ws - geo.rbw);
+  const bool reset_mode = reset_keys != nullptr;
+  const bool see = d.see_through_walls != 0;
+  const int64_t qcap = queue_cap(n);
+  const int gw = blockIdx.x * kWarps + warp, tw = gridDim.x * kWarps;
+
+  if (reset_mode) {
+    for (int64_t e = gw; e < n; e += tw) {
+      const ulonglong2 ek = reinterpret_cast<const ulonglong2*>(reset_keys)[e];
+      const int task = (int)(reinterpret_cast<const ulonglong2*>(s.agent)[e].y >> 32);
+      warp_reset_env(d, &sdesc, s, o, wbase, geo, lane, e, ek.x, ek.y, task, true);
+    }
+    return;
+  }
+
+  // column masks of this lane's bitmap word (first / last column)
+  uint32_t col0 = 0, colL = 0;
+  {
+    int c = (32 * lane) % W;
+    for (int j = 0; j < 32; ++j) {
+      const int p = 32 * lane + j;
+      if (p < HW) {
+        if (c == 0) col0 |= 1u << j;
+        if (c == W - 1) colL |= 1u << j;
+      }
+      c = c + 1 == W ? 0 : c + 1;
+    }
+  }
+  const int q = gw % kQueues, j = gw / kQueues, per_q = tw / kQueues;
+
+  // ---- PUT_DOWN events
+  {
+    const int64_t cnt = s.work[count_index(epoch, 0, q)];
+    const uint32_t* qp = s.work + kWorkHeader + (int64_t)q * qcap;
+    for (int64_t i = j; i < cnt; i += per_q) {
+      const int64_t e = qp[i];
+      uint8_t* genv = s.grids + e * (int64_t)HW;
+      const ulonglong2 ag = reinterpret_cast<const ulonglong2*>(s.agent)[e];
+      for (int k = lane; k < HW; k += 32) ws.grid[k] = genv[k];
+      const int task = (int)(ag.y >> 32);
+      if (R > 0) {
+        const uint32_t* row = d.task_rows + (int64_t)task * d.row_words;
+        for (int k = lane; k < kRowHeader + R; k += 32) rules_s[k] = row[k];
+      }
+      __syncwarp();
+      const int r = (int)(ag.x & 0xff), c = (int)((ag.x >> 8) & 0xff), dir = (int)((ag.x >> 16) & 3);
+      const uint32_t sc = (uint32_t)(ag.x >> 32);
+      const int nr = R > 0 ? (int)(rules_s[1] & 0xff) : 0;
+      Cells<KMAX> cl;
+      cells_load<KMAX>(cl, ws.grid, HW, lane);
+      const int res = warp_put_event<KMAX>(ws.grid, cl, genv, lane, H, W, r, c, rules_s + kRowHeader, nr,
+                                           (uint32_t)ag.y, col0, colL);
+      const bool last = (res & 1) || sc >= (uint32_t)d.budget;
+      const float rew = (res & 1) ? goal_reward(sc, d.budget) : 0.f;
+      if (lane == 0) {
+        o.reward[e] = rew;
+        o.discount[e] = last ? 0.f : 1.f;
+        o.step_type[e] = last ? 2 : 1;
+        if (o.stats != nullptr && (rew != 0.f || last)) {
+          const int slot = (int)(e / kThreads);
+          atomicAdd(o.stats + 3 * slot, (double)rew);
+          if (last) {
+            atomicAdd(o.stats + 3 * slot + 1, 1.0);
+            atomicAdd(o.stats + 3 * slot + 2, (double)sc);
+          }
+        }
+      }
+      if (last) {
+        const ulonglong2 ek = reinterpret_cast<const ulonglong2*>(s.rng)[e];
+        __syncwarp();
+        warp_reset_env(d, &sdesc, s, o, wbase, geo, lane, e, ek.x, ek.y, task, false);
+      } else if ((res & 2) && o.obs != nullptr) {
+        // a rule changed the grid: the observation step_main wrote is stale
+        warp_obs(ws.grid, o.obs + e * ob, lane, r, c, dir, H, W, V, see);
+      }
+      __syncwarp();
+    }
+  }
+  // ---- trial resets
+  {
+    const int64_t cnt = s.work[count_index(epoch, 1, q)];
+    const uint32_t* qp = s.work + kWorkHeader + (int64_t)(kQueues + q) * qcap;
+    for (int64_t i = j; i < cnt; i += per_q) {
+      const int64_t e = qp[i];
+      const ulonglong2 ek = reinterpret_cast<const ulonglong2*>(s.rng)[e];
+      const int task = (int)(reinterpret_cast<const ulonglong2*>(s.agent)[e].y >> 32);
+      warp_reset_env(d, &sdesc, s, o, wbase, geo, lane, e, ek.x, ek.y, task, false);
+    }
   }
 }
 
@@ -1044,7 +1254,7 @@ __global__ void random_actions_kernel(const uint64_t* keys, int64_t n, int64_t t
   }
 }
 
-__global__ void validate_kernel(const void* a, int dtype, int64_t n, int32_t* flag) {
+__global__ void validate_kernel(const void* a, int dtype, int64_t n, uint32_t epoch, uint32_t* flag) {
   bool bad = false;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t v;
@@ -1055,7 +1265,7 @@ __global__ void validate_kernel(const void* a, int dtype, int64_t n, int32_t* fl
     }
     bad |= v < 0 || v >= 6;
   }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(flag, 1);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicMax(flag, epoch);
 }
 
 // ------------------------------------------------------- host side
@@ -1082,30 +1292,65 @@ int pick_maxch(const xmg_env_desc* d) {
   return 0;
 }
 
-template <int MAXCH>
-int launch_step(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
-                const uint64_t* keys, const int32_t* abort_flag, int64_t n, cudaStream_t st) {
-  const Geo geo = make_geo(d->height, d->width, d->view_size, MAXCH, d->rule_width);
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    cudaFuncAttributes fa;
-    attr_err = cudaFuncGetAttributes(&fa, step_kernel<MAXCH>);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(step_kernel<MAXCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kMaxDynSmem - (int)fa.sharedSizeBytes);
-  });
-  if (attr_err != cudaSuccess) return fail(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
-  const int64_t blocks = (n + kThreads - 1) / kThreads;
-  step_kernel<MAXCH><<<(unsigned)blocks, kThreads, (size_t)geo.total, st>>>(*d, *s, *o, actions, dtype, keys,
-                                                                           abort_flag, n);
-  return check_launch("step_kernel");
+template <typename K>
+cudaError_t allow_smem(K kernel, int64_t dyn) {
+  cudaFuncAttributes fa;
+  cudaError_t err = cudaFuncGetAttributes(&fa, kernel);
+  if (err != cudaSuccess) return err;
+  if (dyn + (int64_t)fa.sharedSizeBytes > kMaxDynSmem + 1024) return cudaErrorInvalidValue;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem - (int)fa.sharedSizeBytes);
 }
 
-int validate_desc(const xmg_env_desc* d, int64_t n) {
+template <int MAXCH>
+int launch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
+                const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st) {
+  const MainGeo geo = make_main_geo(d->view_size, MAXCH, d->rule_width);
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] { attr_err = allow_smem(step_main<MAXCH>, kMaxDynSmem - 1024); });
+  if (attr_err != cudaSuccess) return fail(std::string("step_main attributes: ") + cudaGetErrorString(attr_err));
+  const int64_t blocks = (n + kThreads - 1) / kThreads;
+  step_main<MAXCH><<<(unsigned)blocks, kThreads, (size_t)geo.total, st>>>(*d, *s, *o, actions, dtype, flag, epoch,
+                                                                         n);
+  return check_launch("step_main");
+}
+
+int kmax_of(const xmg_env_desc* d) {
+  const int K = (d->height * d->width + 31) / 32;
+  return K <= 4 ? 4 : K <= 8 ? 8 : K <= 20 ? 20 : K <= 32 ? 32 : 0;
+}
+
+template <int KMAX>
+int launch_rare_k(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const uint64_t* keys,
+                  const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st) {
+  const RareGeo geo = make_rare_geo(d->height, d->width, d->rule_width);
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] { attr_err = allow_smem(step_rare<KMAX>, kMaxDynSmem - 1024); });
+  if (attr_err != cudaSuccess) return fail(std::string("step_rare attributes: ") + cudaGetErrorString(attr_err));
+  // one warp per 64 envs (the queues hold ~1.5% of the envs per step in
+  // steady state); a multiple of 32 CTAs so every sub-queue gets equal warps
+  int64_t blocks = (n + 4 * 64 - 1) / (4 * 64);
+  blocks = (blocks + 31) / 32 * 32;
+  step_rare<KMAX><<<(unsigned)blocks, kThreads, (size_t)geo.total, st>>>(*d, *s, *o, keys, flag, epoch, n);
+  return check_launch("step_rare");
+}
+
+int launch_rare(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const uint64_t* keys,
+                const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st) {
+  switch (kmax_of(d)) {
+    case 4: return launch_rare_k<4>(d, s, o, keys, flag, epoch, n, st);
+    case 8: return launch_rare_k<8>(d, s, o, keys, flag, epoch, n, st);
+    case 20: return launch_rare_k<20>(d, s, o, keys, flag, epoch, n, st);
+    default: return launch_rare_k<32>(d, s, o, keys, flag, epoch, n, st);
+  }
+}
+
+int validate_desc(const xmg_env_desc* d, const xmg_state* s, int64_t n) {
   if (!d) return fail("null env description");
+  if (!s || !s->grids || !s->agent || !s->rng || !s->work) return fail("null state buffer");
   if (n < 1) return fail("n must be >= 1");
-  if (n > ((int64_t)1 << 40)) return fail("n too large");
+  if (n > (int64_t)kQEnv) return fail("n too large for one launch (< 2^30)");
   if (d->height < 1 || d->height > 255 || d->width < 1 || d->width > 255) return fail("grid size outside [1, 255]");
   if (d->view_size < 3 || !(d->view_size & 1)) return fail("view_size must be odd and >= 3");
   if (d->scenario < 0 || d->scenario > 6) return fail("unknown scenario");
@@ -1114,21 +1359,22 @@ int validate_desc(const xmg_env_desc* d, int64_t n) {
   if (d->row_words < 4 || (d->row_words & 3)) return fail("row_words must be a positive multiple of 4");
   if (d->num_tasks < 1) return fail("empty task table");
   if (!d->base_cells || !d->task_rows) return fail("null base_cells / task_rows");
-  const Geo geo = make_geo(d->height, d->width, d->view_size, pick_maxch(d), d->rule_width);
-  if (geo.total > kMaxDynSmem)
+  if (pick_maxch(d) == 0) return fail("view window too wide for this build (v*W + v > 482)");
+  if (kmax_of(d) == 0) return fail("grid too large for this build (H*W <= 1024)");
+  if (make_main_geo(d->view_size, pick_maxch(d), d->rule_width).total > kMaxDynSmem - 1024 ||
+      make_rare_geo(d->height, d->width, d->rule_width).total > kMaxDynSmem - 1024)
     return fail("grid too large for the shared-memory scratch of this build (H*W <= ~3000)");
   return 0;
 }
 
-int dispatch_step(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
-                  const uint64_t* keys, const int32_t* abort_flag, int64_t n, cudaStream_t st) {
+int dispatch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
+                  const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st) {
   switch (pick_maxch(d)) {
-    case 6: return launch_step<6>(d, s, o, actions, dtype, keys, abort_flag, n, st);
-    case 8: return launch_step<8>(d, s, o, actions, dtype, keys, abort_flag, n, st);
-    case 12: return launch_step<12>(d, s, o, actions, dtype, keys, abort_flag, n, st);
-    case 16: return launch_step<16>(d, s, o, actions, dtype, keys, abort_flag, n, st);
-    case 32: return launch_step<32>(d, s, o, actions, dtype, keys, abort_flag, n, st);
-    default: return launch_step<0>(d, s, o, actions, dtype, keys, abort_flag, n, st);
+    case 6: return launch_main<6>(d, s, o, actions, dtype, flag, epoch, n, st);
+    case 8: return launch_main<8>(d, s, o, actions, dtype, flag, epoch, n, st);
+    case 12: return launch_main<12>(d, s, o, actions, dtype, flag, epoch, n, st);
+    case 16: return launch_main<16>(d, s, o, actions, dtype, flag, epoch, n, st);
+    default: return launch_main<32>(d, s, o, actions, dtype, flag, epoch, n, st);
   }
 }
 
@@ -1186,32 +1432,39 @@ int32_t xmg_random_actions(const uint64_t* keys, int64_t n, int64_t t0, int64_t 
   return check_launch("random_actions_kernel");
 }
 
-int32_t xmg_validate_actions(const void* actions, int32_t dtype, int64_t n, int32_t* flag, void* stream) {
+int32_t xmg_validate_actions(const void* actions, int32_t dtype, int64_t n, uint32_t epoch, uint32_t* flag,
+                             void* stream) {
   if (n <= 0) return 0;
   if (dtype < 0 || dtype > 2) return fail("unknown action dtype");
+  if (!flag) return fail("null flag");
   const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 8);
-  validate_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(actions, dtype, n, flag);
+  validate_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(actions, dtype, n, epoch, flag);
   return check_launch("validate_kernel");
 }
 
 int32_t xmg_reset(const xmg_env_desc* desc, const xmg_state* state, const uint64_t* keys, int64_t n,
                   const xmg_out* out, void* stream) {
-  if (validate_desc(desc, n)) return -1;
-  if (!state || !out || !keys) return fail("null state/out/keys");
-  return dispatch_step(desc, state, out, nullptr, 0, keys, nullptr, n, (cudaStream_t)stream);
+  if (validate_desc(desc, state, n)) return -1;
+  if (!out || !keys) return fail("null out/keys");
+  return launch_rare(desc, state, out, keys, nullptr, 0, n, (cudaStream_t)stream);
 }
 
 int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* actions, int32_t action_dtype,
-                 int64_t n, const xmg_out* out, const int32_t* abort_flag, void* stream) {
-  if (validate_desc(desc, n)) return -1;
-  if (!state || !out || !actions) return fail("null state/out/actions");
+                 int64_t n, const xmg_out* out, const uint32_t* abort_flag, uint32_t epoch, void* stream) {
+  if (validate_desc(desc, state, n)) return -1;
+  if (!out || !actions) return fail("null out/actions");
   if (action_dtype < 0 || action_dtype > 2) return fail("unknown action dtype");
-  return dispatch_step(desc, state, out, actions, action_dtype, nullptr, abort_flag, n, (cudaStream_t)stream);
+  if (dispatch_main(desc, state, out, actions, action_dtype, abort_flag, epoch, n, (cudaStream_t)stream)) return -1;
+  return launch_rare(desc, state, out, nullptr, abort_flag, epoch, n, (cudaStream_t)stream);
 }
 
 int64_t xmg_step_smem_bytes(const xmg_env_desc* desc) {
   if (!desc) return -1;
-  return make_geo(desc->height, desc->width, desc->view_size, pick_maxch(desc), desc->rule_width).total;
+  const int64_t a = make_main_geo(desc->view_size, pick_maxch(desc), desc->rule_width).total;
+  const int64_t b = make_rare_geo(desc->height, desc->width, desc->rule_width).total;
+  return a > b ? a : b;
 }
+
+int64_t xmg_work_words(int64_t n) { return kWorkHeader + 2 * kQueues * queue_cap(n); }
 
 }  // extern "C"

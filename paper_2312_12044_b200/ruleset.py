@@ -8,8 +8,9 @@
   is kept as one (M, row) uint8 matrix: a 2^20-task file is never turned into
   Python objects on the hot path.
 * ``TaskTable`` is the device form the step kernel reads (include/xmg.h):
-  u32 rows [goal, rule_count | obj_count << 8, R left-packed rules,
-  ceil(O/4) words of left-packed objects], built with vectorised NumPy.
+  u32 rows [goal, rule_count | obj_count << 8, MOVE-gated slot mask,
+  PICK_UP-gated slot mask, R left-packed rules, ceil(O/4) words of
+  left-packed objects], built with vectorised NumPy.
 * ``Benchmark.sample_ruleset`` = ``rulesets[randint(key, M)]``
   (ref benchio.py:57-58) and ``sample_indices`` is its batched twin for
   ``fold_in(root, i)`` keys, evaluated on the GPU.
@@ -31,6 +32,7 @@ import numpy as np
 
 from .core import FormatError, InvalidEncoding, InvalidProportion, Key, UnknownBenchmark, random_words, randint
 
+HEADER_WORDS = 4  # task-table row header: goal, counts, MOVE mask, PICK_UP mask
 MAX_RULES = 18
 MAX_INIT_OBJECTS = 18
 EMPTY_RULE = (0, 0, 0, 0)
@@ -114,15 +116,25 @@ def pack_raw_rows(raw: np.ndarray, max_rules: int, max_objects: int) -> TaskTabl
     objs = _left_pack(oa, objs)[:, :O]
     ow = (O + 3) // 4
     # rows padded to 16 bytes so the kernel fetches them with 128-bit loads
-    words = np.zeros((m, (2 + R + ow + 3) // 4 * 4), np.uint32)
+    words = np.zeros((m, (HEADER_WORDS + R + ow + 3) // 4 * 4), np.uint32)
     words[:, 0] = np.ascontiguousarray(goal).view(np.uint32)[:, 0]
     words[:, 1] = rc.astype(np.uint32) | (oc.astype(np.uint32) << 8)
     if R:
-        words[:, 2:2 + R] = np.ascontiguousarray(rules).view(np.uint32)[..., 0]
+        kinds = rules[..., 0].astype(np.int64)
+        slot_bits = (np.uint64(1) << np.arange(min(R, 32), dtype=np.uint64))
+        agent_near = (kinds == 2) | ((kinds >= 8) & (kinds <= 11))
+        # slots gated on MOVE / PICK_UP (ref rules.py:60-72); 0xFFFFFFFF when R > 32
+        if R <= 32:
+            words[:, 2] = (agent_near[:, :R].astype(np.uint64) * slot_bits).sum(axis=1).astype(np.uint32)
+            words[:, 3] = ((agent_near | (kinds == 1))[:, :R].astype(np.uint64) * slot_bits).sum(axis=1) \
+                .astype(np.uint32)
+        else:
+            words[:, 2] = words[:, 3] = 0xFFFFFFFF
+        words[:, HEADER_WORDS:HEADER_WORDS + R] = np.ascontiguousarray(rules).view(np.uint32)[..., 0]
     if O:
         ob = np.zeros((m, 4 * ow), np.uint8)
         ob[:, :O] = objs
-        words[:, 2 + R:2 + R + ow] = ob.view(np.uint32)
+        words[:, HEADER_WORDS + R:HEADER_WORDS + R + ow] = ob.view(np.uint32)
     return TaskTable(words, R, O, O)
 
 

@@ -225,14 +225,17 @@ class VecEnv:
         agent[:, 1] = word1
         self.agent = torch.from_numpy(agent.view(np.int64)).to(dev)
         self.rng = torch.zeros((n, 2), dtype=torch.int64, device=dev)
-        self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        self._flag_checked = True
+        self.work = torch.zeros(int(_lib.lib().xmg_work_words(n)), dtype=torch.int32, device=dev)
+        self._flag = torch.zeros(1, dtype=torch.int32, device=dev)  # epoch of the last rejected batch
+        self.epoch = 0          # steps issued on this state (queue parity, rejection tags)
+        self._checked_epoch = 0
 
         self._desc = _lib.EnvDesc(h, w, v, params.step_budget, scen, int(params.see_through_walls), nseg, fixed,
                                   table.rule_width if scen == 0 else 0, table.obj_width, table.row_words,
                                   table.num_tasks, int(resample_tasks and scen == 0), self._base.data_ptr(),
                                   self._seg_off.data_ptr(), self._seg_cells.data_ptr(), self._table.data_ptr())
-        self._state = _lib.State(self.grids_flat.data_ptr(), self.agent.data_ptr(), self.rng.data_ptr())
+        self._state = _lib.State(self.grids_flat.data_ptr(), self.agent.data_ptr(), self.rng.data_ptr(),
+                                 self.work.data_ptr())
         if _lib.lib().xmg_step_smem_bytes(C.byref(self._desc)) > 226 * 1024:
             raise _lib.NativeLibraryError(f"{h}x{w} grids exceed the shared-memory budget of this build")
         self._outs = None
@@ -330,12 +333,11 @@ class VecEnv:
                 dt = _lib.ACT_I64
             actions = actions.contiguous()
             if validate:
-                self._flag.zero_()
-                _lib.check(_lib.lib().xmg_validate_actions(actions.data_ptr(), dt, n, self._flag.data_ptr(),
-                                                           _stream(self.device)), "xmg_validate_actions")
+                _lib.check(_lib.lib().xmg_validate_actions(actions.data_ptr(), dt, n, (self.epoch + 1) & 0xFFFFFFFF,
+                                                           self._flag.data_ptr(), _stream(self.device)),
+                           "xmg_validate_actions")
                 self.launches += 1
                 flag_ptr = self._flag.data_ptr()
-                self._flag_checked = False
         else:
             a = np.asarray(actions)
             if a.shape != (n,):
@@ -346,20 +348,21 @@ class VecEnv:
             dt = _lib.ACT_U8
         outs = self._alloc_out(compute_obs)
         o = self._out_struct(outs)
+        self.epoch += 1
         _lib.check(_lib.lib().xmg_step(C.byref(self._desc), C.byref(self._state), actions.data_ptr(), dt, n,
-                                       C.byref(o), flag_ptr, _stream(self.device)), "xmg_step")
-        self.launches += 1
+                                       C.byref(o), flag_ptr, self.epoch & 0xFFFFFFFF, _stream(self.device)),
+                   "xmg_step")
+        self.launches += 2  # streaming pass + rare-work pass
         if self.strict and flag_ptr is not None:
             self.check()
         return VecTimeStep(*outs)
 
     def check(self) -> None:
         """Raise InvalidAction if a device-validated batch was rejected (syncs)."""
-        if not self._flag_checked:
-            bad = int(self._flag.item())
-            self._flag_checked = True
-            if bad:
-                raise InvalidAction("action outside [0, 5]; the batch was not applied")
+        flagged = int(self._flag.item()) & 0xFFFFFFFF  # syncs the stream
+        if flagged > self._checked_epoch:
+            self._checked_epoch = flagged
+            raise InvalidAction(f"action outside [0, 5] at step {flagged}; that batch was not applied")
 
     # -- inspection
     def ruleset_of(self, i: int) -> Ruleset:

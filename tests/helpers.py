@@ -55,8 +55,9 @@ def oracle_from_table(params, table, ids, threads=0):
     goals = rows[:, 0].copy().view(np.uint8).reshape(n, 4)
     rc = (rows[:, 1] & 0xFF).astype(np.int32)
     oc = ((rows[:, 1] >> 8) & 0xFF).astype(np.int32)
-    rules = rows[:, 2:2 + R].copy().view(np.uint8).reshape(n, max(R, 0), 4) if R else np.zeros((n, 1, 4), np.uint8)
-    objs = rows[:, 2 + R:].copy().view(np.uint8)[:, :O] if O else np.zeros((n, 1), np.uint8)
+    from paper_2312_12044_b200.ruleset import HEADER_WORDS as HW_
+    rules = rows[:, HW_:HW_ + R].copy().view(np.uint8).reshape(n, max(R, 0), 4) if R else np.zeros((n, 1, 4), np.uint8)
+    objs = rows[:, HW_ + R:].copy().view(np.uint8)[:, :O] if O else np.zeros((n, 1), np.uint8)
     return OracleVecEnv(params.height, params.width, params.view_size, params.step_budget, params.scenario,
                         int(params.layout), int(params.see_through_walls), goals, rules if R else np.zeros((n, 1, 4), np.uint8),
                         rc, objs if O else np.zeros((n, 1), np.uint8), oc, threads)

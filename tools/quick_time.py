@@ -43,6 +43,32 @@ def run(name):
           f"{ms / steps * 1e3:8.1f} us/step {n * steps / ms * 1e3 / 1e9:7.3f} G env-steps/s", flush=True)
 
 
+
+
+def burst(name="c3", around=506, k=4):
+    """Per-step device times around the synchronized budget reset."""
+    env_name, config, n, _ = RUNS[name]
+    _, params = make(env_name)
+    vec = VecEnv(params, n, load_benchmark(benchmark_file(config)) if config else None, reuse_outputs=True)
+    vec.reset(key_from_seed(0))
+    acts = random_actions(policy_keys(key_from_seed(1), n, device="cuda"), 0, around + k)
+    for t in range(around - 1):
+        vec.step(acts[t], True, False)
+    times = []
+    for t in range(around - 1, around - 1 + k):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        vec.step(acts[t], True, False)
+        e.record()
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e) * 1e3)
+    print(f"{os.environ.get('XMG_LIB', 'default')[-20:]:20s} burst {name}: steps {around - 1}..{around + k - 2} us: "
+          + " ".join(f"{x:.0f}" for x in times), flush=True)
+
+
 if __name__ == "__main__":
     for nm in (sys.argv[1:] or RUNS):
-        run(nm)
+        if nm.startswith("burst:"):
+            burst(nm.split(":")[1])
+        else:
+            run(nm)
