@@ -52,28 +52,45 @@ def algorithmic_bytes(h: int, w: int, rules: int, v: int) -> int:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region (NVML,
+    every ~2 ms; nvidia-smi as fallback)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.002):
         self.index = index
-        self.samples: list[list[str]] = []
+        self.period = period_s
+        self.sm: list[float] = []
+        self.max_sm: float | None = None
+        self.reasons: set[str] = set()
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.1)
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            names = {N.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
+                     N.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                     N.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                     N.nvmlClocksEventReasonSwPowerCap: "sw_power_cap",
+                     N.nvmlClocksEventReasonHwPowerBrakeSlowdown: "hw_power_brake_slowdown"}
+            while not self._stop.is_set():
+                self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+                bits = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.reasons.update(v for k, v in names.items() if bits & k)
+                self._stop.wait(self.period)
+        except Exception:  # no NVML: one nvidia-smi sample per 100 ms
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                    a, b = (float(x) for x in out.stdout.strip().split(","))
+                    self.sm.append(a)
+                    self.max_sm = b
+                except Exception:
+                    pass
+                self._stop.wait(0.1)
 
     def __enter__(self):
         self._t.start()
@@ -84,15 +101,10 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self) -> dict:
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4) if "Active" in s[3 + k]
-                          and not s[3 + k].startswith("Not")})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_sm, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_sm, "reasons": sorted(self.reasons),
+                "samples": len(self.sm)}
 
 
 def dist_env():
@@ -234,8 +246,9 @@ def run_ours(args):
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
     tot = tot.cpu().numpy()
 
-    # ---- dominant kernel alone: per-launch CUDA events on the launching stream
-    # (a fresh env at the same phase, validate off so only step_kernel runs)
+    # ---- the step kernels alone: CUDA events around each xmg_step (step_main +
+    # step_rare) on the launching stream (a fresh env at the same phase,
+    # validate off so only the two step kernels run between the events)
     params2, _, vec2 = make_workload(args.workload, dev, n, offset)
     vec2.reset(key_from_seed(0))
     for t in range(W + pre):
@@ -260,12 +273,15 @@ def run_ours(args):
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = bpe * n / (kern_ms / 1e3) / 1e9
-    traffic = load_traffic(f"{args.workload}:step_kernel")
+    traffic = load_traffic(f"{args.workload}:step")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": (traffic * n if traffic is not None else None),
-                "kernel": "step_kernel", "kernel_ms": kern_ms, "bytes_per_env_step": bpe,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
-                "traffic_note": "ncu dram__bytes_read.sum+write.sum per launch (profiles/ncu_summary.json)"}
+                "kernel": "xmg_step = step_main + step_rare (one env step, timed as a pair)",
+                "kernel_ms": kern_ms, "bytes_per_env_step": bpe,
+                "bytes_model": "SURVEY.md 8(d): H*W + 12 + 4 + 4R + 1 + 2v^2 + 9 (read-once-grid model)",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if peaks else "fallback 6650 GB/s",
+                "traffic_note": "ncu dram__bytes_read.sum+write.sum of both kernels per step "
+                                "(profiles/ncu_summary.json)"}
 
     # ---- e2e through the public API with HOST buffers (pinned), per step:
     # H2D of the step's actions, the step, D2H of the whole VecTimeStep.

@@ -494,6 +494,28 @@ struct TrialKeys {
   uint64_t st_hi, st_lo, k0h, k0l, k1h, k1l, k2h, k2l, task_word;
 };
 
+__device__ __forceinline__ TrialKeys derive_trial_keys(uint64_t ek_hi, uint64_t ek_lo, bool resample) {
+  TrialKeys k;
+  const Words4 ks = philox(0, 0, kDomSplit, 0, ek_hi, ek_lo);
+  const Words4 st = philox(1, 0, kDomSplit, 0, ek_hi, ek_lo);
+  k.st_hi = st.w0;
+  k.st_lo = st.w1;
+  const Words4 a = philox(0, 0, kDomSplit, 0, ks.w0, ks.w1);
+  const Words4 b = philox(1, 0, kDomSplit, 0, ks.w0, ks.w1);
+  const Words4 c = philox(2, 0, kDomSplit, 0, ks.w0, ks.w1);
+  k.k0h = a.w0; k.k0l = a.w1;
+  k.k1h = b.w0; k.k1l = b.w1;
+  k.k2h = c.w0; k.k2l = c.w1;
+  k.task_word = 0;
+  if (resample) {
+    // extension (not in the reference): a fresh task per trial, drawn as
+    // Benchmark.sample_ruleset(split(ek, 2)) = rows[word0 % M] (ref:benchio.py:57-58)
+    const Words4 tk = philox(2, 0, kDomSplit, 0, ek_hi, ek_lo);
+    k.task_word = philox(0, 0, kDomDraw, 0, tk.w0, tk.w1).w0;
+  }
+  return k;
+}
+
 // Rebuild one env's trial with the scenario builders ref:scenarios.py:291-412
 // (batched: ref:vecenv.py:242-291).  Called by all 32 lanes with the same
 // arguments; writes the new grid to `gdst` (and leaves it in ws.grid) and
@@ -1069,18 +1091,26 @@ __device__ __forceinline__ TrialKeys warp_trial_keys(int lane, uint64_t ek_hi, u
 }
 
 struct RareGeo {
-  int hwp, lg, ws, rbw;
+  int hwp, lg, ws, rbw, keys;
   int64_t total;
 };
+
+__host__ __device__ inline int log2_buckets(int hw) {  // >= 5, 2^lg >= hw
+  int lg = 5;
+  while ((1 << lg) < hw) ++lg;
+  return lg;
+}
 
 __host__ __device__ inline RareGeo make_rare_geo(int H, int W, int R) {
   RareGeo g;
   g.hwp = round16(H * W + 16);
-  g.lg = 5;
-  while ((1 << g.lg) < H * W) ++g.lg;
+  g.lg = log2_buckets(H * W);
   g.rbw = round16(4 * (kRowHeader + R));
-  // per warp: wd: u64[hwp] | fc: u16[hwp] | slot: u16[hwp] | bk: u32[2^lg] | grid: u8[hwp] | misc: 64 u64 | rules
-  g.ws = 8 * g.hwp + 2 * g.hwp + 2 * g.hwp + 4 * (1 << g.lg) + g.hwp + 512 + g.rbw;
+  g.keys = 32 * (int)sizeof(TrialKeys);
+  // per warp: wd: u64[hwp] | fc: u16[hwp] | slot: u16[hwp] | bk: u32[2^lg] | grid: u8[hwp] | misc: 64 u64
+  //           | rules | 32 trial keys | env description
+  g.ws = 8 * g.hwp + 2 * g.hwp + 2 * g.hwp + 4 * (1 << g.lg) + g.hwp + 512 + g.rbw + g.keys +
+         round16((int)sizeof(xmg_env_desc));
   g.total = (int64_t)kWarps * g.ws;
   return g;
 }
@@ -1088,11 +1118,9 @@ __host__ __device__ inline RareGeo make_rare_geo(int H, int W, int R) {
 // Rebuild env e's trial (ref:vecenv.py:359-361 -> :224-291), whole warp.
 __device__ __forceinline__ void warp_reset_env(const xmg_env_desc& d, const xmg_env_desc* sd, const xmg_state& s,
                                                const xmg_out& o, uint8_t* wbase, const RareGeo& geo, int lane,
-                                               int64_t e, uint64_t ek_hi, uint64_t ek_lo, int task, bool reset_mode) {
+                                               int64_t e, const TrialKeys& key, int task, bool reset_mode) {
   const int H = d.height, W = d.width, HW = H * W, V = d.view_size, ob = 2 * V * V;
   const WarpScratch ws = make_scratch(wbase, geo.hwp, geo.lg);
-  const bool resample = d.resample_tasks && d.scenario == XMG_SCENARIO_XLAND;
-  const TrialKeys key = warp_trial_keys(lane, ek_hi, ek_lo, resample);
   const uint32_t g_in = d.scenario == XMG_SCENARIO_XLAND ? d.task_rows[(int64_t)task * d.row_words] : 0u;
   const ResetOut ro = warp_build(sd, wbase, geo.hwp, geo.lg, lane, key, task, g_in, s.grids + e * (int64_t)HW);
   if (lane == 0) {
@@ -1109,63 +1137,89 @@ __device__ __forceinline__ void warp_reset_env(const xmg_env_desc& d, const xmg_
   __syncwarp();
 }
 
+// Resets of a group of up to 32 envs (one per lane, `mine`): each lane
+// derives its env's trial keys, then the warp rebuilds the envs one by one.
+__device__ __forceinline__ void warp_reset_group(const xmg_env_desc& d, const xmg_env_desc* sd, const xmg_state& s,
+                                                 const xmg_out& o, uint8_t* wbase, const RareGeo& geo,
+                                                 TrialKeys* keys, int lane, bool mine, int64_t e,
+                                                 const uint64_t* reset_keys) {
+  const bool resample = d.resample_tasks && d.scenario == XMG_SCENARIO_XLAND;
+  int task = 0;
+  if (mine) {
+    const ulonglong2 ek = reinterpret_cast<const ulonglong2*>(reset_keys ? reset_keys : s.rng)[e];
+    task = (int)(reinterpret_cast<const ulonglong2*>(s.agent)[e].y >> 32);
+    keys[lane] = derive_trial_keys(ek.x, ek.y, resample);
+  }
+  uint32_t m = __ballot_sync(0xffffffffu, mine);
+  __syncwarp();
+  while (m) {
+    const int src = __ffs(m) - 1;
+    m &= m - 1;
+    const int64_t es = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)e, src);
+    const int ts = __shfl_sync(0xffffffffu, task, src);
+    warp_reset_env(d, sd, s, o, wbase, geo, lane, es, keys[src], ts, reset_keys != nullptr);
+  }
+}
+
 // step_rare drains the two queues step_main filled, one env per warp:
 //  * PUT_DOWN queue: the grid-wide rule pass, goal, reward (warp_put_event);
-//  * reset queue: the trial rebuild (warp_build).
+//  * reset queue: the trial rebuild (warp_build), 32 envs' keys at a time.
 // Sub-queue q of each kind is served by the warps gw with gw % kQueues == q,
-// striding over its entries.  reset_keys != nullptr: reset mode (ref
-// VecEnv.reset_with_keys, vecenv.py:205-222), every env [0, n) rebuilt from
-// keys[e] with a FIRST record.
+// striding over its entries; warps without entries exit at once.
+// reset_keys != nullptr: reset mode (ref VecEnv.reset_with_keys,
+// vecenv.py:205-222), every env [0, n) rebuilt from keys[e] with a FIRST
+// record.
 template <int KMAX>
 __global__ void __launch_bounds__(kThreads, XMG_MINB_RARE) step_rare(const xmg_env_desc d, const xmg_state s,
                                                                      const xmg_out o, const uint64_t* reset_keys,
                                                                      const uint32_t* abort_flag, uint32_t epoch,
                                                                      int64_t n) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ xmg_env_desc sdesc;  // read by the out-of-line paths without local copies
-  if (threadIdx.x == 0) sdesc = d;
-  __syncthreads();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gw = blockIdx.x * kWarps + warp, tw = gridDim.x * kWarps;
+  const bool reset_mode = reset_keys != nullptr;
+  const int q = gw % kQueues, j = gw / kQueues, per_q = tw / kQueues;
+  int64_t cnt_put = 0, cnt_reset = 0;
+  if (!reset_mode) {
+    cnt_put = s.work[count_index(epoch, 0, q)];
+    cnt_reset = s.work[count_index(epoch, 1, q)];
+    if (j >= cnt_put && j >= cnt_reset) return;  // nothing queued for this warp
+  } else if (gw >= n) {
+    return;
+  }
   if (batch_rejected(abort_flag, epoch)) return;
+
   const int H = d.height, W = d.width, HW = H * W, V = d.view_size, ob = 2 * V * V, R = d.rule_width;
   const RareGeo geo = make_rare_geo(H, W, R);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint8_t* wbase = smem + warp * geo.ws;
   const WarpScratch ws = make_scratch(wbase, geo.hwp, geo.lg);
-  uint32_t* rules_s = reinterpret_cast<uint32_t*>(wbase + geo.ws - geo.rbw);
-  const bool reset_mode = reset_keys != nullptr;
+  uint32_t* rules_s = reinterpret_cast<uint32_t*>(wbase + geo.ws - geo.rbw - geo.keys -
+                                                  round16((int)sizeof(xmg_env_desc)));
+  TrialKeys* keys = reinterpret_cast<TrialKeys*>(wbase + geo.ws - geo.keys - round16((int)sizeof(xmg_env_desc)));
+  // this warp's copy of the description, for the out-of-line paths
+  xmg_env_desc* sdesc = reinterpret_cast<xmg_env_desc*>(wbase + geo.ws - round16((int)sizeof(xmg_env_desc)));
+  if (lane == 0) *sdesc = d;
+  __syncwarp();
   const bool see = d.see_through_walls != 0;
   const int64_t qcap = queue_cap(n);
-  const int gw = blockIdx.x * kWarps + warp, tw = gridDim.x * kWarps;
 
   if (reset_mode) {
-    for (int64_t e = gw; e < n; e += tw) {
-      const ulonglong2 ek = reinterpret_cast<const ulonglong2*>(reset_keys)[e];
-      const int task = (int)(reinterpret_cast<const ulonglong2*>(s.agent)[e].y >> 32);
-      warp_reset_env(d, &sdesc, s, o, wbase, geo, lane, e, ek.x, ek.y, task, true);
+    for (int64_t g0 = gw; g0 < n; g0 += 32 * (int64_t)tw) {
+      const int64_t e = g0 + (int64_t)lane * tw;
+      warp_reset_group(d, sdesc, s, o, wbase, geo, keys, lane, e < n, e, reset_keys);
     }
     return;
   }
 
-  // column masks of this lane's bitmap word (first / last column)
-  uint32_t col0 = 0, colL = 0;
-  {
-    int c = (32 * lane) % W;
-    for (int j = 0; j < 32; ++j) {
-      const int p = 32 * lane + j;
-      if (p < HW) {
-        if (c == 0) col0 |= 1u << j;
-        if (c == W - 1) colL |= 1u << j;
-      }
-      c = c + 1 == W ? 0 : c + 1;
-    }
-  }
-  const int q = gw % kQueues, j = gw / kQueues, per_q = tw / kQueues;
-
   // ---- PUT_DOWN events
-  {
-    const int64_t cnt = s.work[count_index(epoch, 0, q)];
+  if (j < cnt_put) {
+    // this lane's word of the first / last column bitmaps
+    uint32_t col0 = 0, colL = 0;
+    for (int p = (32 * lane + W - 1) / W * W; p < 32 * lane + 32 && p < HW; p += W) col0 |= 1u << (p - 32 * lane);
+    for (int p = (32 * lane) / W * W + W - 1; p < 32 * lane + 32 && p < HW; p += W)
+      if (p >= 32 * lane) colL |= 1u << (p - 32 * lane);
     const uint32_t* qp = s.work + kWorkHeader + (int64_t)q * qcap;
-    for (int64_t i = j; i < cnt; i += per_q) {
+    for (int64_t i = j; i < cnt_put; i += per_q) {
       const int64_t e = qp[i];
       uint8_t* genv = s.grids + e * (int64_t)HW;
       const ulonglong2 ag = reinterpret_cast<const ulonglong2*>(s.agent)[e];
@@ -1200,8 +1254,9 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB_RARE) step_rare(const xmg_e
       }
       if (last) {
         const ulonglong2 ek = reinterpret_cast<const ulonglong2*>(s.rng)[e];
+        const TrialKeys key = warp_trial_keys(lane, ek.x, ek.y, d.resample_tasks && d.scenario == XMG_SCENARIO_XLAND);
         __syncwarp();
-        warp_reset_env(d, &sdesc, s, o, wbase, geo, lane, e, ek.x, ek.y, task, false);
+        warp_reset_env(d, sdesc, s, o, wbase, geo, lane, e, key, task, false);
       } else if ((res & 2) && o.obs != nullptr) {
         // a rule changed the grid: the observation step_main wrote is stale
         warp_obs(ws.grid, o.obs + e * ob, lane, r, c, dir, H, W, V, see);
@@ -1209,15 +1264,13 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB_RARE) step_rare(const xmg_e
       __syncwarp();
     }
   }
-  // ---- trial resets
-  {
-    const int64_t cnt = s.work[count_index(epoch, 1, q)];
+  // ---- trial resets, 32 at a time (entries i0 + lane * per_q)
+  if (j < cnt_reset) {
     const uint32_t* qp = s.work + kWorkHeader + (int64_t)(kQueues + q) * qcap;
-    for (int64_t i = j; i < cnt; i += per_q) {
-      const int64_t e = qp[i];
-      const ulonglong2 ek = reinterpret_cast<const ulonglong2*>(s.rng)[e];
-      const int task = (int)(reinterpret_cast<const ulonglong2*>(s.agent)[e].y >> 32);
-      warp_reset_env(d, &sdesc, s, o, wbase, geo, lane, e, ek.x, ek.y, task, false);
+    for (int64_t i0 = j; i0 < cnt_reset; i0 += 32 * (int64_t)per_q) {
+      const int64_t i = i0 + (int64_t)lane * per_q;
+      const bool mine = i < cnt_reset;
+      warp_reset_group(d, sdesc, s, o, wbase, geo, keys, lane, mine, mine ? (int64_t)qp[i] : 0, nullptr);
     }
   }
 }
