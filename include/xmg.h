@@ -135,9 +135,16 @@ void xmg_philox_host(const uint64_t ctr[4], uint64_t k0, uint64_t k1, uint64_t o
 int32_t xmg_reset(const xmg_env_desc* desc, const xmg_state* state, const uint64_t* keys /*[n][2]*/, int64_t n,
                   const xmg_out* out, void* stream);
 
-/* Raises *flag (device u32, zero-initialised once) to `epoch` when any action
- * lies outside [0, 6): the device half of ref vecenv.py:297-301
- * (InvalidAction).  The step with the same epoch then touches nothing. */
+/* Validation flag block: XMG_FLAG_WORDS device u32, zero-initialised once.
+ * [0] epoch of the last rejected batch, [1] epoch of the last finished
+ * validation, [2] internal CTA counter. */
+#define XMG_FLAG_WORDS 4
+
+/* Raises flag[0] to `epoch` when any action lies outside [0, 6): the device
+ * half of ref vecenv.py:297-301 (InvalidAction), then publishes flag[1] =
+ * epoch.  The step with the same epoch then touches nothing.  May run
+ * concurrently with the previous step's second kernel (it only reads
+ * `actions`). */
 int32_t xmg_validate_actions(const void* actions, int32_t action_dtype, int64_t n, uint32_t epoch, uint32_t* flag,
                              void* stream);
 
@@ -147,8 +154,12 @@ int32_t xmg_validate_actions(const void* actions, int32_t action_dtype, int64_t 
  * one-warp-per-env pass over the envs it queued (PUT_DOWN events, resets).
  * `epoch` numbers the caller's steps (consecutive calls on one state must use
  * consecutive epochs: its parity selects the queue buffers).  abort_flag
- * (device, nullable): when *abort_flag == epoch no env is touched (pairs with
- * xmg_validate_actions so an invalid batch mutates nothing). */
+ * (device flag block, nullable): the step waits for flag[1] == epoch (the
+ * validation of this epoch), and when flag[0] == epoch no env is touched
+ * (pairs with xmg_validate_actions so an invalid batch mutates nothing).
+ * The first kernel of a step may start while the previous step's second
+ * kernel still runs: envs that kernel has not released yet are waited for
+ * individually (state.work bookkeeping). */
 int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* actions, int32_t action_dtype,
                  int64_t n, const xmg_out* out, const uint32_t* abort_flag, uint32_t epoch, void* stream);
 

@@ -31,6 +31,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -53,9 +54,10 @@ struct Words4 {
 
 // Philox4x64-10, ref:rng.py:42-57.  __umul64hi gives the high half of the
 // 64x64 product the reference builds from 32-bit limbs (rng.py:60-71).
+template <int UNROLL = 10>
 __device__ __forceinline__ Words4 philox(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3, uint64_t k0,
                                          uint64_t k1) {
-#pragma unroll
+#pragma unroll UNROLL
   for (int r = 0; r < 10; ++r) {
     const uint64_t hi0 = __umul64hi(kM0, c0), lo0 = kM0 * c0;
     const uint64_t hi1 = __umul64hi(kM1, c2), lo1 = kM1 * c2;
@@ -119,7 +121,7 @@ constexpr int kWarps = kThreads / 32;
 #define XMG_MINB 6  // min resident CTAs per SM the register allocation targets
 #endif
 #ifndef XMG_MINB_RARE
-#define XMG_MINB_RARE 4  // step_rare: <= 128 registers
+#define XMG_MINB_RARE 6  // step_rare: <= 80 registers, so the next step's kernels fit beside it
 #endif
 #ifndef XMG_RARE
 #define XMG_RARE __forceinline__  // rare paths (reset, PUT_DOWN, occlusion) inlined: measured faster
@@ -202,25 +204,57 @@ __device__ __forceinline__ void stage_issue(View& vw, int lo, int hi, int HW) {
 // predicate (TILE_NEAR* rules, TILE_* goals) is gated on PUT_DOWN only
 // (ref:rules.py:60-72, ref:goals.py:268-283): PUT_DOWN events are queued and
 // resolved by step_rare (warp_put_event).
-__device__ XMG_RARE int agent_rules(View vw, const uint32_t* rules, uint32_t slots, int ev, int H, int W, int ar,
-                                    int ac, int pocket) {
-  for (; slots; slots &= slots - 1) {  // only the slots gated on this event, in stored order
+// The agent's four neighbour cells in NEAR_OFFSETS order (up, left, right,
+// down; ref:rules.py:76), 0x100 when off the grid, plus their flat indices.
+struct Nbrs {
+  int code[4];
+  int flat[4];
+};
+
+__device__ __forceinline__ Nbrs load_nbrs(const View& vw, int H, int W, int ar, int ac) {
+  Nbrs nb;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int r = ar + near_dr(k), c = ac + near_dc(k);
+    const bool in = r >= 0 && r < H && c >= 0 && c < W;
+    nb.flat[k] = r * W + c;
+    nb.code[k] = in ? (int)vw.rd(nb.flat[k]) : 0x100;
+  }
+  return nb;
+}
+
+// NEAR_OFFSETS slot of the directional offsets up, right, down, left
+// (ref:rules.py:80-89, ref:goals.py:287-296)
+__device__ __forceinline__ int dir_slot(int d) { return d == 0 ? 0 : d == 1 ? 2 : d == 2 ? 3 : 1; }
+
+__device__ __forceinline__ int nbr_code(const Nbrs& nb, int k) {
+  return k == 0 ? nb.code[0] : k == 1 ? nb.code[1] : k == 2 ? nb.code[2] : nb.code[3];
+}
+
+// Rules gated on MOVE / PICK_UP (only the slots in `slots`, stored order).
+__device__ XMG_RARE int agent_rules(View vw, Nbrs& nb, const uint32_t* rules, uint32_t slots, int pocket) {
+  for (; slots; slots &= slots - 1) {
     const uint32_t rw = rules[__ffs(slots) - 1];
     const int kind = rw & 0xff, a = (rw >> 8) & 0xff, out = rw >> 24;
-    if (kind == 0 || kind > 11 || !((cRuleGate[kind] >> ev) & 1)) continue;
     if (kind == 1) {  // AGENT_HOLD
       if (pocket == a) pocket = (out >> 4) == kFloor ? 0 : out;
-    } else if (kind == 2) {  // AGENT_NEAR: first NEAR_OFFSETS neighbour holding a
-      for (int k = 0; k < 4; ++k) {
-        const int r = ar + near_dr(k), c = ac + near_dc(k);
-        if (r >= 0 && r < H && c >= 0 && c < W && vw.rd(r * W + c) == a) {
-          vw.wr(r * W + c, (uint8_t)out);
-          break;
+      continue;
+    }
+    // AGENT_NEAR: first neighbour holding a; AGENT_NEAR_{UP,RIGHT,DOWN,LEFT}: one slot
+    int k = -1;
+    if (kind == 2) {
+      k = nb.code[0] == a ? 0 : nb.code[1] == a ? 1 : nb.code[2] == a ? 2 : nb.code[3] == a ? 3 : -1;
+    } else if (kind >= 8 && kind <= 11) {
+      const int q = dir_slot(kind - 8);
+      if (nbr_code(nb, q) == a) k = q;
+    }
+    if (k >= 0) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (t == k) {
+          nb.code[t] = out;
+          vw.wr(nb.flat[t], (uint8_t)out);
         }
-      }
-    } else if (kind >= 8) {  // AGENT_NEAR_{UP,RIGHT,DOWN,LEFT}
-      const int r = ar + dir_dr(kind - 8), c = ac + dir_dc(kind - 8);
-      if (r >= 0 && r < H && c >= 0 && c < W && vw.rd(r * W + c) == a) vw.wr(r * W + c, (uint8_t)out);
     }
   }
   return pocket;
@@ -228,23 +262,16 @@ __device__ XMG_RARE int agent_rules(View vw, const uint32_t* rules, uint32_t slo
 
 // Agent-relative goals (ref:goals.py:361-378); the TILE_* kinds never pass the
 // gate of a MOVE / PICK_UP event.
-__device__ bool agent_goal(const View& vw, uint32_t goal, int ev, int H, int W, int ar, int ac, int pocket) {
+__device__ __forceinline__ bool agent_goal(const Nbrs& nb, int own, uint32_t goal, int ev, int ar, int ac,
+                                           int pocket) {
   const int kind = goal & 0xff, a1 = (goal >> 8) & 0xff, a2 = (goal >> 16) & 0xff;
   if (kind == 0 || kind > 14 || !((cGoalGate[kind] >> ev) & 1)) return false;
   switch (kind) {
     case 1: return pocket == a1;
-    case 2: return vw.rd(ar * W + ac) == a1;
+    case 2: return own == a1;
     case 5: return ar == a1 && ac == a2;
-    case 3:
-      for (int k = 0; k < 4; ++k) {
-        const int r = ar + near_dr(k), c = ac + near_dc(k);
-        if (r >= 0 && r < H && c >= 0 && c < W && vw.rd(r * W + c) == a1) return true;
-      }
-      return false;
-    case 11: case 12: case 13: case 14: {
-      const int r = ar + dir_dr(kind - 11), c = ac + dir_dc(kind - 11);
-      return r >= 0 && r < H && c >= 0 && c < W && vw.rd(r * W + c) == a1;
-    }
+    case 3: return nb.code[0] == a1 || nb.code[1] == a1 || nb.code[2] == a1 || nb.code[3] == a1;
+    case 11: case 12: case 13: case 14: return nbr_code(nb, dir_slot(kind - 11)) == a1;
     default: return false;
   }
 }
@@ -258,6 +285,7 @@ __device__ __forceinline__ void obs_see(const uint8_t* stage, int sbase, uint8_t
                                         int W, int Vrt) {
   const int V = VV ? VV : Vrt;
   const int h = V / 2;
+  // origin (view cell (0, 0)) and the world steps of i (rows) and j (columns)
   int r0, c0, dri, dci, drj, dcj;
   switch (d) {
     case 0: r0 = r - (V - 1); c0 = c - h; dri = 1; dci = 0; drj = 0; dcj = 1; break;
@@ -265,28 +293,36 @@ __device__ __forceinline__ void obs_see(const uint8_t* stage, int sbase, uint8_t
     case 2: r0 = r + (V - 1); c0 = c + h; dri = -1; dci = 0; drj = 0; dcj = -1; break;
     default: r0 = r + h; c0 = c - (V - 1); dri = 0; dci = 1; drj = -1; dcj = 0; break;
   }
-  const uint8_t* sp = stage - sbase;
+  // the facing makes i move along one world axis and j along the other:
+  // validity is a product of a mask over i and a mask over j
+  uint32_t mi = 0, mj = 0;
+  for (int t = 0; t < V; ++t) {
+    const int wi = dri ? r0 + t * dri : c0 + t * dci;  // world coordinate moved by i
+    const int wj = drj ? r0 + t * drj : c0 + t * dcj;  // world coordinate moved by j
+    mi |= (uint32_t)((unsigned)wi < (unsigned)(dri ? H : W)) << t;
+    mj |= (uint32_t)((unsigned)wj < (unsigned)(drj ? H : W)) << t;
+  }
+  const int di = dri * W + dci, dj = drj * W + dcj;  // flat steps
+  const uint8_t* p0 = stage - sbase + (r0 * W + c0);
   uint16_t* o = reinterpret_cast<uint16_t*>(dst);
   if constexpr (VV != 0) {
 #pragma unroll
     for (int i = 0; i < VV; ++i) {
+      const bool vi = (mi >> i) & 1;
 #pragma unroll
       for (int j = 0; j < VV; ++j) {
-        const int wr = r0 + i * dri + j * drj, wc = c0 + i * dci + j * dcj;
         uint32_t code = 0;
-        if ((unsigned)wr < (unsigned)H && (unsigned)wc < (unsigned)W) code = sp[wr * W + wc];
-        o[i * VV + j] = (uint16_t)((code >> 4) | ((code & 15u) << 8));
+        if (vi && ((mj >> j) & 1)) code = p0[i * di + j * dj];
+        o[i * VV + j] = (uint16_t)(((code * 0x1001u) >> 4) & 0x0F0Fu);  // (tile, color) bytes
       }
     }
   } else {
-    for (int i = 0; i < V; ++i) {
+    for (int i = 0; i < V; ++i)
       for (int j = 0; j < V; ++j) {
-        const int wr = r0 + i * dri + j * drj, wc = c0 + i * dci + j * dcj;
         uint32_t code = 0;
-        if ((unsigned)wr < (unsigned)H && (unsigned)wc < (unsigned)W) code = sp[wr * W + wc];
-        o[i * V + j] = (uint16_t)((code >> 4) | ((code & 15u) << 8));
+        if (((mi >> i) & (mj >> j)) & 1) code = p0[i * di + j * dj];
+        o[i * V + j] = (uint16_t)(((code * 0x1001u) >> 4) & 0x0F0Fu);
       }
-    }
   }
 }
 
@@ -309,7 +345,21 @@ __device__ bool seg_crosses_cell(int p0r, int p0c, int dr, int dc, int cr, int c
   return lo_n * hi_d < hi_n * lo_d;
 }
 
-__device__ bool cell_visible(const View& vw, int W, int r0, int c0, int r1, int c1) {
+__device__ __noinline__ bool cell_visible_p(const uint8_t* stage, int sbase, int slo, int shi, const uint8_t* g, int W,
+                                            int r0, int c0, int r1, int c1);
+
+__device__ __forceinline__ bool cell_visible(const View& vw, int W, int r0, int c0, int r1, int c1) {
+  return cell_visible_p(vw.stage, vw.sbase, vw.slo, vw.shi, vw.g, W, r0, c0, r1, c1);
+}
+
+__device__ __noinline__ bool cell_visible_p(const uint8_t* stage, int sbase, int slo, int shi, const uint8_t* g, int W,
+                                            int r0, int c0, int r1, int c1) {
+  View vw;
+  vw.stage = const_cast<uint8_t*>(stage);
+  vw.g = const_cast<uint8_t*>(g);
+  vw.sbase = sbase;
+  vw.slo = slo;
+  vw.shi = shi;
   if (r0 == r1 && c0 == c1) return true;
   const int p0r = 2 * r0 + 1, p0c = 2 * c0 + 1, dr = 2 * (r1 - r0), dc = 2 * (c1 - c0);
   for (int rr = min(r0, r1); rr <= max(r0, r1); ++rr)
@@ -406,17 +456,18 @@ __device__ void draw_all(const WarpScratch& ws, int lane, int F, uint64_t kc_hi,
   const int jobs = nO + nD + 1;
   for (int j = lane; j < jobs; j += 32) {
     uint64_t* dst;
-    Words4 w;
+    uint64_t ctr, kh, kl;
     if (j < nO) {
-      w = philox((uint64_t)j, 0, kDomDraw, 0, kc_hi, kc_lo);
+      ctr = (uint64_t)j; kh = kc_hi; kl = kc_lo;
       dst = ws.wd + 4 * j;
     } else if (j < nO + nD) {
-      w = philox((uint64_t)(j - nO), 0, kDomDraw, 0, kd_hi, kd_lo);
+      ctr = (uint64_t)(j - nO); kh = kd_hi; kl = kd_lo;
       dst = ws.misc + 4 * (j - nO);
     } else {
-      w = philox(0, 0, kDomDraw, 0, ka_hi, ka_lo);
+      ctr = 0; kh = ka_hi; kl = ka_lo;
       dst = ws.misc + 24;
     }
+    const Words4 w = philox<5>(ctr, 0, kDomDraw, 0, kh, kl);
     dst[0] = w.w0; dst[1] = w.w1; dst[2] = w.w2; dst[3] = w.w3;
   }
   __syncwarp();
@@ -494,34 +545,40 @@ struct TrialKeys {
   uint64_t st_hi, st_lo, k0h, k0l, k1h, k1l, k2h, k2l, task_word;
 };
 
-__device__ __forceinline__ TrialKeys derive_trial_keys(uint64_t ek_hi, uint64_t ek_lo, bool resample) {
+__device__ __noinline__ void derive_trial_keys(uint64_t ek_hi, uint64_t ek_lo, bool resample, TrialKeys* out) {
   TrialKeys k;
-  const Words4 ks = philox(0, 0, kDomSplit, 0, ek_hi, ek_lo);
-  const Words4 st = philox(1, 0, kDomSplit, 0, ek_hi, ek_lo);
+  const Words4 ks = philox<2>(0, 0, kDomSplit, 0, ek_hi, ek_lo);
+  const Words4 st = philox<2>(1, 0, kDomSplit, 0, ek_hi, ek_lo);
   k.st_hi = st.w0;
   k.st_lo = st.w1;
-  const Words4 a = philox(0, 0, kDomSplit, 0, ks.w0, ks.w1);
-  const Words4 b = philox(1, 0, kDomSplit, 0, ks.w0, ks.w1);
-  const Words4 c = philox(2, 0, kDomSplit, 0, ks.w0, ks.w1);
-  k.k0h = a.w0; k.k0l = a.w1;
-  k.k1h = b.w0; k.k1l = b.w1;
-  k.k2h = c.w0; k.k2l = c.w1;
+  uint64_t sub[6];
+#pragma unroll 1
+  for (int i = 0; i < 3; ++i) {
+    const Words4 w = philox<2>((uint64_t)i, 0, kDomSplit, 0, ks.w0, ks.w1);
+    sub[2 * i] = w.w0;
+    sub[2 * i + 1] = w.w1;
+  }
+  k.k0h = sub[0]; k.k0l = sub[1];
+  k.k1h = sub[2]; k.k1l = sub[3];
+  k.k2h = sub[4]; k.k2l = sub[5];
   k.task_word = 0;
   if (resample) {
     // extension (not in the reference): a fresh task per trial, drawn as
     // Benchmark.sample_ruleset(split(ek, 2)) = rows[word0 % M] (ref:benchio.py:57-58)
-    const Words4 tk = philox(2, 0, kDomSplit, 0, ek_hi, ek_lo);
-    k.task_word = philox(0, 0, kDomDraw, 0, tk.w0, tk.w1).w0;
+    const Words4 tk = philox<2>(2, 0, kDomSplit, 0, ek_hi, ek_lo);
+    k.task_word = philox<2>(0, 0, kDomDraw, 0, tk.w0, tk.w1).w0;
   }
-  return k;
+  *out = k;
 }
 
 // Rebuild one env's trial with the scenario builders ref:scenarios.py:291-412
 // (batched: ref:vecenv.py:242-291).  Called by all 32 lanes with the same
 // arguments; writes the new grid to `gdst` (and leaves it in ws.grid) and
 // returns the new pose / goal / task on every lane.
-__device__ XMG_RARE ResetOut warp_build(const xmg_env_desc* dp, uint8_t* wbase, int hwp, int lg, int lane,
-                                        const TrialKeys& key, int task_in, uint32_t goal_in, uint8_t* gdst) {
+__device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, int hwp, int lg, int lane,
+                                        const TrialKeys* keyp, int task_in, uint32_t goal_in, uint8_t* gdst,
+                                        ResetOut* outp) {
+  const TrialKeys key = *keyp;
   const xmg_env_desc& d = *dp;  // CTA copy in shared memory
   const WarpScratch ws = make_scratch(wbase, hwp, lg);
   const int H = d.height, W = d.width, HW = H * W;
@@ -543,8 +600,9 @@ __device__ XMG_RARE ResetOut warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
     for (int i = lane; i < HW; i += 32) gdst[i] = ws.grid[i];
     res.r = 1; res.c = 1; res.d = 1;
     res.goal = 2u | ((uint32_t)kGreenGoal << 8);
+    if (lane == 0) *outp = res;
     __syncwarp();
-    return res;
+    return;
   }
   const uint64_t k0h = key.k0h, k0l = key.k0l, k1h = key.k1h, k1l = key.k1l, k2h = key.k2h, k2l = key.k2l;
 
@@ -552,7 +610,7 @@ __device__ XMG_RARE ResetOut warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
   const bool two_rooms = sc == XMG_SCENARIO_DOOR_KEY || sc == XMG_SCENARIO_UNLOCK || sc == XMG_SCENARIO_UNLOCK_PICKUP;
   if (two_rooms) {  // ref:scenarios.py:341-353, 373-385
     Words4 w = {0, 0, 0, 0};
-    if (lane == 0) w = philox(0, 0, kDomDraw, 0, k0h, k0l);
+    if (lane == 0) w = philox<2>(0, 0, kDomDraw, 0, k0h, k0l);
     const uint64_t w0 = shfl64(w.w0, 0), w1 = shfl64(w.w1, 0);
     int door_row;
     if (sc == XMG_SCENARIO_DOOR_KEY) {
@@ -631,8 +689,8 @@ __device__ XMG_RARE ResetOut warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
   res.r = spawn_cell / W;
   res.c = spawn_cell - res.r * W;
   for (int i = lane; i < HW; i += 32) gdst[i] = ws.grid[i];
+  if (lane == 0) *outp = res;
   __syncwarp();
-  return res;
 }
 
 // ------------------------------------------------------- the step: two kernels
@@ -659,9 +717,41 @@ __host__ __device__ inline int count_index(uint32_t parity, int kind, int q) {
 }
 constexpr uint32_t kQPut = 1u << 31, kQReset = 1u << 30, kQEnv = (1u << 30) - 1;
 
+// capacity of one sub-queue: every env of the CTAs (128 envs, step_main) or
+// warp chunks (32 envs, step_stream) feeding it
 __host__ __device__ inline int64_t queue_cap(int64_t n) {
-  const int64_t blocks = (n + kThreads - 1) / kThreads;
-  return (blocks + kQueues - 1) / kQueues * kThreads;
+  const int64_t blocks = (n + kThreads - 1) / kThreads, chunks = (n + 31) / 32;
+  const int64_t a = (blocks + kQueues - 1) / kQueues * kThreads, b = (chunks + kQueues - 1) / kQueues * 32;
+  return a > b ? a : b;
+}
+
+// Entry slots of sub-queue (parity, kind, q): double-buffered like the counts,
+// so step t + 1's step_main appends while step t's step_rare still drains.
+__host__ __device__ inline int64_t queue_base(int64_t n, uint32_t parity, int kind, int q) {
+  return kWorkHeader + ((int64_t)(parity & 1) * 2 * kQueues + kind * kQueues + q) * queue_cap(n);
+}
+
+// Chunk bookkeeping after the queues (chunk = the 32 envs of one step_main warp):
+//   pending[nchunks]  queued envs of the chunk step_rare has not finished yet
+//   dirty[nchunks]    epoch of the last step that queued envs of the chunk
+// Only the chunk's own warp reads and writes its dirty word, so the tag needs
+// no clearing.
+__host__ __device__ inline int64_t num_chunks(int64_t n) { return (n + kThreads - 1) / kThreads * kWarps; }
+__host__ __device__ inline int64_t pending_base(int64_t n) { return kWorkHeader + 4 * kQueues * queue_cap(n); }
+__host__ __device__ inline int64_t dirty_base(int64_t n) { return pending_base(n) + num_chunks(n); }
+__host__ __device__ inline int64_t work_words(int64_t n) { return pending_base(n) + 2 * num_chunks(n); }
+
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ ulonglong2 ld_cg_u64x2(const ulonglong2* p) {  // fresh from L2, not CSE'd
+  ulonglong2 v;
+  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ int load_action(const void* a, int dtype, int64_t e) {
@@ -725,15 +815,32 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
                                                                 const uint32_t* abort_flag, uint32_t epoch,
                                                                 int64_t n) {
   extern __shared__ __align__(128) uint8_t smem[];
-  // clear the counts the previous step consumed; this step appends to the others
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // Launched as a programmatic dependent of the previous kernel (the previous
+  // step's step_rare, or this step's validation), so it runs concurrently with
+  // the previous step_rare: with a validation it waits for the verdict, and
+  // per 32-env chunk it waits only where the previous step queued envs (below).
+  if (abort_flag != nullptr) {  // this epoch's validation verdict (published by its last CTA)
+    if (lane == 0)
+      for (uint32_t spins = 0; ld_acquire(abort_flag + 1) != epoch; ++spins) {
+        if (spins > (1u << 25)) __trap();
+        __nanosleep(64);
+      }
+    __syncwarp();
+  }
+  // the previous step_rare has read these counts (it reads them before it
+  // lets this grid launch); this step appends to the other parity
   if (blockIdx.x == 0)
-    for (int i = threadIdx.x; i < 2 * kQueues; i += blockDim.x) s.work[count_index(epoch + 1, 0, 0) + i] = 0;
+    for (int i = tid; i < 2 * kQueues; i += blockDim.x) s.work[count_index(epoch + 1, 0, 0) + i] = 0;
   if (batch_rejected(abort_flag, epoch)) return;
 
   const int H = d.height, W = d.width, HW = H * W, V = d.view_size, R = d.rule_width;
   const MainGeo geo = make_main_geo(V, MAXCH, R);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t e0 = (int64_t)blockIdx.x * kThreads;
+  const int64_t tile = blockIdx.x;
+  const int64_t e0 = tile * kThreads;
+  const int64_t chunk = tile * kWarps + warp;
+  uint32_t* pending = s.work + pending_base(n) + chunk;
+  uint32_t* dirty = s.work + dirty_base(n) + chunk;
   const int64_t e = e0 + tid;
   const bool valid = e < n;
 
@@ -748,9 +855,24 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
   // ---- load: the 16-byte state word and the action
   ulonglong2 ag = make_ulonglong2(0, 0);
   int act = 1;
+  const uint32_t was_dirty = e0 + warp * 32 < n ? *dirty : 0u;  // issued together with the state loads
   if (valid) {
     ag = reinterpret_cast<const ulonglong2*>(s.agent)[e];
     act = load_action(actions, act_dtype, e);
+  }
+  if (was_dirty == epoch - 1 && e0 + warp * 32 < n) {
+    // the previous step queued envs of this chunk: wait until its step_rare has
+    // released them all, then reload the state word it may have rewritten
+    if (lane == 0) {
+      // bounded: a lost release is a bug, trap (launch error) rather than hang
+      for (uint32_t spins = 0; ld_acquire(pending) != 0; ++spins) {
+        if (spins > (1u << 25)) __trap();
+        __nanosleep(128);
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncwarp();
+    if (valid) ag = ld_cg_u64x2(reinterpret_cast<const ulonglong2*>(s.agent) + e);
   }
   int r = (int)(ag.x & 0xff), c = (int)((ag.x >> 8) & 0xff), dir = (int)((ag.x >> 16) & 3);
   int pocket = (int)((ag.x >> 24) & 0xff);
@@ -810,16 +932,21 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
     // gates, in stored order) and goal; TOGGLE gates no rule and no goal.
     bool goal = false;
     if (ev == 0 || ev == 1) {
+      Nbrs nb = load_nbrs(vw, H, W, r, c);
       const int nr = R > 0 ? (int)(rbuf[1] & 0xff) : 0;
-      if (nr && R > 32) {
-        for (int s0 = 0; s0 < nr; s0 += 32)
-          pocket = agent_rules(vw, rbuf + kRowHeader + s0, nr - s0 >= 32 ? 0xffffffffu : (1u << (nr - s0)) - 1u, ev,
-                               H, W, r, c, pocket);
-      } else if (nr) {
-        const uint32_t slots = rbuf[2 + ev];
-        if (slots) pocket = agent_rules(vw, rbuf + kRowHeader, slots, ev, H, W, r, c, pocket);
+      if (nr) {
+        if (R <= 32) {
+          const uint32_t slots = rbuf[2 + ev];
+          if (slots) pocket = agent_rules(vw, nb, rbuf + kRowHeader, slots, pocket);
+        } else {  // wide tables: gate every slot here
+          for (int s0 = 0; s0 < nr; ++s0) {
+            const int kind = rbuf[kRowHeader + s0] & 0xff;
+            if (kind >= 1 && kind <= 11 && ((cRuleGate[kind] >> ev) & 1))
+              pocket = agent_rules(vw, nb, rbuf + kRowHeader + s0, 1u, pocket);
+          }
+        }
       }
-      goal = agent_goal(vw, goal_word, ev, H, W, r, c, pocket);
+      goal = agent_goal(nb, vw.rd(r * W + c), goal_word, ev, r, c, pocket);
     }
     // ---- counters and reward, ref:vecenv.py:351-357
     sc += 1;
@@ -839,7 +966,11 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
   // ---- defer the rare work: warp-aggregated append to this CTA's sub-queue
   const uint32_t qm = __ballot_sync(0xffffffffu, qflags != 0);
   if (qm) {
-    const int k = blockIdx.x % kQueues;
+    const int k = (int)(tile % kQueues);
+    if (lane == 0) {
+      atomicAdd(pending, (uint32_t)__popc(qm));
+      *dirty = epoch;
+    }
     // PUT_DOWN and reset entries go to their own queues
 #pragma unroll
     for (int kind = 0; kind < 2; ++kind) {
@@ -851,14 +982,14 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
       if (lane == leader) base = atomicAdd(s.work + count_index(epoch, kind, k), (uint32_t)__popc(km));
       base = __shfl_sync(0xffffffffu, base, leader);
       if (qflags == want) {
-        const int64_t slot = (int64_t)(kind * kQueues + k) * queue_cap(n) + base + __popc(km & ((1u << lane) - 1));
-        s.work[kWorkHeader + slot] = (uint32_t)e;
+        s.work[queue_base(n, epoch, kind, k) + base + __popc(km & ((1u << lane) - 1))] = (uint32_t)e;
       }
     }
   }
 
   // ---- episode statistics of the trials decided here
-  if (o.stats != nullptr) warp_stats(o.stats, blockIdx.x, rew, last ? 1.0 : 0.0, last ? (double)sc : 0.0);
+  if (o.stats != nullptr) warp_stats(o.stats, (int)tile, rew, last ? 1.0 : 0.0, last ? (double)sc : 0.0);
+
 
   // ---- observation: assembled in smem, one TMA bulk store per warp
   // (envs queued for step_rare get theirs rewritten there)
@@ -915,8 +1046,8 @@ __device__ __forceinline__ uint16_t obs_cell(const uint8_t* G, int r, int c, int
   return (uint16_t)((code >> 4) | ((code & 15) << 8));
 }
 
-__device__ __forceinline__ void warp_obs(const uint8_t* G, uint8_t* gobs, int lane, int r, int c, int d, int H, int W,
-                                         int V, bool see) {
+__device__ __noinline__ void warp_obs(const uint8_t* G, uint8_t* gobs, int lane, int r, int c, int d, int H, int W,
+                                      int V, bool see) {
   for (int cell = lane; cell < V * V; cell += 32)
     reinterpret_cast<uint16_t*>(gobs)[cell] = obs_cell(G, r, c, d, H, W, V, cell, see);
 }
@@ -968,6 +1099,9 @@ __device__ __forceinline__ void cells_set(Cells<KMAX>& cl, int p, int v, int lan
 // `dir` (0 up, 1 right, 2 down, 3 left, -1: the first of NEAR_OFFSETS up,
 // left, right, down) -- ref:rules.py:192-213, ref:goals.py:380-394.  Returns
 // p (or -1) and the neighbour cell on every lane.
+__device__ __noinline__ int2 tile_match(uint32_t am, uint32_t bm, int lane, int dir, int W, uint32_t col0,
+                                        uint32_t colL);
+
 template <int KMAX>
 __device__ __forceinline__ int bit_tile_scan(const Cells<KMAX>& cl, int lane, int a, int b, int dir, int W,
                                              uint32_t col0, uint32_t colL, int& nb) {
@@ -983,13 +1117,22 @@ __device__ __forceinline__ int bit_tile_scan(const Cells<KMAX>& cl, int lane, in
   }
   nb = -1;
   if (!__any_sync(0xffffffffu, am != 0)) return -1;
+  const int2 pq = tile_match(am, bm, lane, dir, W, col0, colL);
+  nb = pq.y;
+  return pq.x;
+}
+
+// The matching half of bit_tile_scan: (p, neighbour) or (-1, -1).
+__device__ __noinline__ int2 tile_match(uint32_t am, uint32_t bm, int lane, int dir, int W, uint32_t col0,
+                                        uint32_t colL) {
+  int nb = -1;
   const uint32_t up = am & shl_cells(bm, W, lane);             // b at p - W
   const uint32_t left = am & shl_cells(bm, 1, lane) & ~col0;   // b at p - 1, same row
   const uint32_t right = am & shr_cells(bm, 1, lane) & ~colL;  // b at p + 1, same row
   const uint32_t down = am & shr_cells(bm, W, lane);           // b at p + W
   const uint32_t any = dir < 0 ? (up | left | right | down) : dir == 0 ? up : dir == 1 ? right : dir == 2 ? down : left;
   const uint32_t wm = __ballot_sync(0xffffffffu, any != 0);
-  if (!wm) return -1;
+  if (!wm) return make_int2(-1, -1);
   const int k = __ffs(wm) - 1;
   const int bit = __ffs(__shfl_sync(0xffffffffu, any, k)) - 1;
   const int p = 32 * k + bit;
@@ -1001,7 +1144,7 @@ __device__ __forceinline__ int bit_tile_scan(const Cells<KMAX>& cl, int lane, in
   } else {
     nb = dir == 0 ? p - W : dir == 1 ? p + 1 : dir == 2 ? p + W : p - 1;
   }
-  return p;
+  return make_int2(p, nb);
 }
 
 // One PUT_DOWN event of one env, resolved by the whole warp: the rule pass
@@ -1070,28 +1213,460 @@ __device__ __forceinline__ int warp_put_event(uint8_t* G, Cells<KMAX>& cl, uint8
   return (int)hit | ((int)dirty << 1);
 }
 
-// The trial keys of one env derived by the warp in two levels (lanes 0-2,
-// then lanes 0-3): ref:vecenv.py:225-226, ref:scenarios.py:293.
-__device__ __forceinline__ TrialKeys warp_trial_keys(int lane, uint64_t ek_hi, uint64_t ek_lo, bool resample) {
-  Words4 w = {0, 0, 0, 0};
-  if (lane < 3) w = philox((uint64_t)lane, 0, kDomSplit, 0, ek_hi, ek_lo);  // ks, st, task key
-  const uint64_t ks_hi = shfl64(w.w0, 0), ks_lo = shfl64(w.w1, 0);
-  TrialKeys k;
-  k.st_hi = shfl64(w.w0, 1);
-  k.st_lo = shfl64(w.w1, 1);
-  const uint64_t tk_hi = shfl64(w.w0, 2), tk_lo = shfl64(w.w1, 2);
-  Words4 v = {0, 0, 0, 0};
-  if (lane < 3) v = philox((uint64_t)lane, 0, kDomSplit, 0, ks_hi, ks_lo);  // k0, k1, k2
-  else if (lane == 3 && resample) v = philox(0, 0, kDomDraw, 0, tk_hi, tk_lo);
-  k.k0h = shfl64(v.w0, 0); k.k0l = shfl64(v.w1, 0);
-  k.k1h = shfl64(v.w0, 1); k.k1l = shfl64(v.w1, 1);
-  k.k2h = shfl64(v.w0, 2); k.k2l = shfl64(v.w1, 2);
-  k.task_word = shfl64(v.w0, 3);
-  return k;
+
+// ------------------------------------------------------- step_stream
+// Persistent streaming step for grids of <= 256 cells.  A warp owns chunks of
+// 32 consecutive envs; their grids (32*H*W bytes), 16-byte state words and
+// actions are contiguous in HBM, so lane 0 moves each chunk into the warp's
+// shared memory with three TMA bulk copies (cp.async.bulk + mbarrier),
+// double-buffered: chunk k+2 is in flight while chunk k is computed.  With
+// the whole grid staged, PUT_DOWN events are resolved in place by the warp
+// (bit-parallel scans, warp_put_event); only finished trials are deferred to
+// step_rare.  No CTA-wide barrier after the prologue.
+constexpr int kStreamWarps = 4;
+
+struct StreamGeo {
+  int chunk_grid, stage, ob, rbw, warp_bytes;
+  int64_t total;
+};
+
+__host__ __device__ inline StreamGeo make_stream_geo(int HW, int V, int R) {
+  StreamGeo g;
+  g.chunk_grid = 32 * HW;                      // multiple of 16
+  g.stage = g.chunk_grid + 32 * 16 + 32 * 8;   // grids | state words | actions (<= 8 B each)
+  g.ob = 2 * V * V;
+  g.rbw = 16 * ((kRowHeader + R + 3) / 4);     // per-lane rule row
+  g.warp_bytes = 2 * g.stage + round16(32 * g.ob) + 32 * g.rbw + 16;  // + 2 mbarriers
+  g.total = (int64_t)kStreamWarps * g.warp_bytes;
+  return g;
 }
 
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst), b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(kStreamWarps * 32) step_stream(const xmg_env_desc d, const xmg_state s,
+                                                                const xmg_out o, const void* actions, int act_dtype,
+                                                                const uint32_t* abort_flag, uint32_t epoch,
+                                                                int64_t n) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < 2 * kQueues; i += blockDim.x) s.work[count_index(epoch + 1, 0, 0) + i] = 0;
+  if (batch_rejected(abort_flag, epoch)) return;
+
+  const int H = d.height, W = d.width, HW = H * W, V = d.view_size, R = d.rule_width;
+  const StreamGeo geo = make_stream_geo(HW, V, R);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * kStreamWarps + warp, tw = (int64_t)gridDim.x * kStreamWarps;
+  const int64_t nchunks = (n + 31) / 32;
+  const int asz = act_dtype == XMG_ACT_U8 ? 1 : act_dtype == XMG_ACT_I32 ? 4 : 8;
+  const bool act_tma = (reinterpret_cast<uintptr_t>(actions) & 15) == 0;  // else per-lane loads
+  uint8_t* wb = smem + warp * geo.warp_bytes;
+  uint8_t* obs_stage = wb + 2 * geo.stage;
+  uint32_t* rbuf = reinterpret_cast<uint32_t*>(obs_stage + round16(32 * geo.ob) + lane * geo.rbw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(obs_stage + round16(32 * geo.ob) + 32 * geo.rbw);
+  // this lane's word of the first / last column bitmaps (PUT_DOWN scans)
+  uint32_t col0 = 0, colL = 0;
+  for (int p = (32 * lane + W - 1) / W * W; p < 32 * lane + 32 && p < HW; p += W) col0 |= 1u << (p - 32 * lane);
+  for (int p = (32 * lane) / W * W + W - 1; p < 32 * lane + 32 && p < HW; p += W) colL |= 1u << (p - 32 * lane);
+
+  auto issue = [&](int64_t c, int st) {  // lane 0: TMA bulk loads of full chunk c into stage st
+    uint8_t* sb = wb + st * geo.stage;
+    const uint32_t abytes = 32u * asz;
+    mbar_expect(bars + st, (uint32_t)geo.chunk_grid + 512u + (act_tma ? abytes : 0u));
+    bulk_g2s(sb, s.grids + c * (int64_t)geo.chunk_grid, (uint32_t)geo.chunk_grid, bars + st);
+    bulk_g2s(sb + geo.chunk_grid, s.agent + 2 * 32 * c, 512u, bars + st);
+    if (act_tma)
+      bulk_g2s(sb + geo.chunk_grid + 512, reinterpret_cast<const uint8_t*>(actions) + 32 * c * asz, abytes,
+               bars + st);
+  };
+  const int64_t nfull = n / 32;  // chunks fully inside [0, n)
+  if (lane == 0) {
+    mbar_init(bars);
+    mbar_init(bars + 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (gw < nfull) issue(gw, 0);
+    if (gw + tw < nfull) issue(gw + tw, 1);
+  }
+  __syncwarp();
+
+  int k = 0;
+  for (int64_t c = gw; c < nchunks; c += tw, ++k) {
+    const int st = k & 1;
+    uint8_t* sb = wb + st * geo.stage;
+    const int64_t e = 32 * c + lane;
+    const bool valid = e < n;
+    if (c < nfull) {
+      mbar_wait(bars + st, (uint32_t)((k >> 1) & 1));
+    } else {  // the tail chunk: each lane fetches its own env
+      if (valid) {
+        const uint8_t* g = s.grids + e * (int64_t)HW;
+        for (int i = 0; i < HW; ++i) sb[lane * HW + i] = g[i];
+        reinterpret_cast<ulonglong2*>(sb + geo.chunk_grid)[lane] = reinterpret_cast<const ulonglong2*>(s.agent)[e];
+        for (int i = 0; i < asz; ++i)
+          sb[geo.chunk_grid + 512 + lane * asz + i] = reinterpret_cast<const uint8_t*>(actions)[e * asz + i];
+      }
+      __syncwarp();
+    }
+    // ---- this lane's env: state word, action, staged grid
+    const ulonglong2 ag = valid ? reinterpret_cast<const ulonglong2*>(sb + geo.chunk_grid)[lane]
+                                : make_ulonglong2(0, 0);
+    int act = 1;
+    if (valid) {
+      if (act_tma || c >= nfull) {
+        const uint8_t* ap = sb + geo.chunk_grid + 512 + lane * asz;
+        act = asz == 1 ? (int)ap[0] : asz == 4 ? *reinterpret_cast<const int32_t*>(ap)
+                                               : (int)*reinterpret_cast<const int64_t*>(ap);
+      } else {
+        act = load_action(actions, act_dtype, e);
+      }
+    }
+    View vw;
+    vw.g = s.grids + (valid ? e : 0) * (int64_t)HW;
+    vw.stage = sb + lane * HW;
+    vw.sbase = 0;
+    vw.slo = 0;
+    vw.shi = HW;
+    int r = (int)(ag.x & 0xff), c0 = (int)((ag.x >> 8) & 0xff), dir = (int)((ag.x >> 16) & 3);
+    int pocket = (int)((ag.x >> 24) & 0xff);
+    uint32_t sc = (uint32_t)(ag.x >> 32);
+    const uint32_t goal_word = (uint32_t)ag.y;
+    const int task = (int)(ag.y >> 32);
+    // the rule row of actions that can raise a MOVE / PICK_UP / PUT_DOWN event
+    if (valid && R > 0 && (act == 0 || act == 3 || act == 4)) {
+      const uint32_t* src = d.task_rows + (int64_t)task * d.row_words;
+      for (int q = 0; q < (kRowHeader + R + 3) >> 2; ++q) cp_async16(rbuf + 4 * q, src + 4 * q);
+      cp_async_wait_all();
+    }
+    int ev = -1;
+    bool goal = false;
+    if (valid) {
+      // ---- action, ref:vecenv.py:306-342 / ref:env.py:148-191
+      const int tr = r + dir_dr(dir), tc = c0 + dir_dc(dir);
+      const bool inside = tr >= 0 && tr < H && tc >= 0 && tc < W;
+      const int tflat = tr * W + tc;
+      const int tcode = inside ? vw.stage[tflat] : 0, tt = tcode >> 4;
+      switch (act) {
+        case 0:
+          if (inside && ((kWalkable >> tt) & 1)) { r = tr; c0 = tc; ev = 0; }
+          break;
+        case 1: dir = (dir + 3) & 3; break;
+        case 2: dir = (dir + 1) & 3; break;
+        case 3:
+          if (inside && pocket == 0 && ((kPickable >> tt) & 1)) {
+            pocket = tcode; vw.wr(tflat, kFloorCode); ev = 1;
+          }
+          break;
+        case 4:
+          if (inside && pocket != 0 && tt == kFloor) {
+            vw.wr(tflat, (uint8_t)pocket); pocket = 0; ev = 2;
+          }
+          break;
+        default:
+          if (inside) {
+            const int col = tcode & 15;
+            if (tt == kClosed || (tt == kLocked && pocket == kKey * 16 + col)) {
+              vw.wr(tflat, (uint8_t)(kOpen * 16 + col)); ev = 3;
+            }
+          }
+      }
+      // ---- MOVE / PICK_UP: agent-relative rules and goal (ref:vecenv.py:344-349)
+      if (ev == 0 || ev == 1) {
+        Nbrs nb = load_nbrs(vw, H, W, r, c0);
+        const int nr = R > 0 ? (int)(rbuf[1] & 0xff) : 0;
+        if (nr) {
+          if (R <= 32) {
+            const uint32_t slots = rbuf[2 + ev];
+            if (slots) pocket = agent_rules(vw, nb, rbuf + kRowHeader, slots, pocket);
+          } else {
+            for (int s0 = 0; s0 < nr; ++s0) {
+              const int kind = rbuf[kRowHeader + s0] & 0xff;
+              if (kind >= 1 && kind <= 11 && ((cRuleGate[kind] >> ev) & 1))
+                pocket = agent_rules(vw, nb, rbuf + kRowHeader + s0, 1u, pocket);
+            }
+          }
+        }
+        goal = agent_goal(nb, vw.stage[r * W + c0], goal_word, ev, r, c0, pocket);
+      }
+    }
+    // ---- PUT_DOWN: grid-wide rules and goal, one env at a time by the warp
+    uint32_t pm = __ballot_sync(0xffffffffu, ev == 2);
+    if (pm) {
+      __syncwarp();
+      while (pm) {
+        const int t = __ffs(pm) - 1;
+        pm &= pm - 1;
+        uint8_t* G = sb + t * HW;
+        const uint64_t agx = __shfl_sync(0xffffffffu, (unsigned long long)pack_agent(r, c0, dir, pocket, sc), t);
+        const uint32_t gw_t = __shfl_sync(0xffffffffu, goal_word, t);
+        const uint32_t* rt = reinterpret_cast<const uint32_t*>(obs_stage + round16(32 * geo.ob) + t * geo.rbw);
+        const int nr = R > 0 ? (int)(rt[1] & 0xff) : 0;
+        Cells<KMAX> cl;
+        cells_load<KMAX>(cl, G, HW, lane);
+        const int res = warp_put_event<KMAX>(G, cl, s.grids + (32 * c + t) * (int64_t)HW, lane, H, W,
+                                             (int)(agx & 0xff), (int)((agx >> 8) & 0xff), rt + kRowHeader, nr,
+                                             gw_t, col0, colL);
+        if (lane == t) goal = res & 1;
+      }
+    }
+    // ---- counters and reward, ref:vecenv.py:351-357
+    float rew = 0.f;
+    bool last = false;
+    if (valid) {
+      sc += 1;
+      last = goal || sc >= (uint32_t)d.budget;
+      if (goal) rew = goal_reward(sc, d.budget);
+      o.reward[e] = rew;
+      o.discount[e] = last ? 0.f : 1.f;
+      o.step_type[e] = last ? 2 : 1;
+      s.agent[2 * e] = pack_agent(r, c0, dir, pocket, sc);
+    }
+    // ---- finished trials go to step_rare's reset queue
+    const uint32_t qm = __ballot_sync(0xffffffffu, last);
+    if (qm) {
+      const int kq = (int)(c % kQueues);
+      const int leader = __ffs(qm) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(s.work + count_index(epoch, 1, kq), (uint32_t)__popc(qm));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (last)
+        s.work[queue_base(n, epoch, 1, kq) + base + __popc(qm & ((1u << lane) - 1))] =
+            (uint32_t)e;
+    }
+    if (o.stats != nullptr) warp_stats(o.stats, (int)(c / 4), rew, last ? 1.0 : 0.0, last ? (double)sc : 0.0);
+    // ---- observation: staged in smem, one TMA bulk store per warp
+    if (o.obs != nullptr) {
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // previous store drained
+      __syncwarp();
+      if (valid) {
+        uint8_t* dst = obs_stage + lane * geo.ob;
+        if (d.see_through_walls) {
+          if (V == 5) obs_see<5>(vw.stage, 0, dst, r, c0, dir, H, W, V);
+          else obs_see<0>(vw.stage, 0, dst, r, c0, dir, H, W, V);
+        } else {
+          obs_occluded(vw, dst, r, c0, dir, H, W, V);
+        }
+      }
+      const int nvalid = (int)min((int64_t)32, n - 32 * c);
+      const uint32_t bytes = (uint32_t)(nvalid * geo.ob), bulk = bytes & ~15u;
+      uint8_t* gdst = o.obs + 32 * c * geo.ob;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0 && bulk) {
+        const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(obs_stage);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(saddr), "r"(bulk)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      for (uint32_t q = bulk + lane; q < bytes; q += 32) gdst[q] = obs_stage[q];
+    }
+    // ---- refill this stage with chunk c + 2 tw
+    __syncwarp();
+    if (lane == 0 && c + 2 * tw < nfull) issue(c + 2 * tw, st);
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// ------------------------------------------------------- warp-level PUT_DOWN
+// One PUT_DOWN event is resolved by a whole warp on a shared-memory copy G of
+// the env's grid.  Rules are evaluated speculatively in parallel, lane s on
+// rule slot s0 + s against the current grid: the first slot that fires is the
+// one the sequential pass (ref:rules.py:162-213) would apply first, since no
+// earlier slot changed anything; it is applied and evaluation restarts after
+// it.  Events fire at most a few rules, so this is one or two rounds.  TILE
+// rules scan a candidate list (every cell that is neither floor nor wall, in
+// row-major order, built with ballots); generated rule inputs are objects, so
+// only a scan for a floor / wall code falls back to the full grid.
+
+// `b` at the neighbour of cell pos in the direction the variant tries
+// (dir -1: first of NEAR_OFFSETS up, left, right, down; 0 up 1 right 2 down 3 left)
+__device__ __forceinline__ int nb_match(const uint8_t* G, int H, int W, int pos, int b, int dir) {
+  const int r = pos / W, c = pos - r * W;
+  const bool up = r > 0 && G[pos - W] == b, left = c > 0 && G[pos - 1] == b;
+  const bool right = c + 1 < W && G[pos + 1] == b, down = r + 1 < H && G[pos + W] == b;
+  if (dir < 0) return up ? pos - W : left ? pos - 1 : right ? pos + 1 : down ? pos + W : -1;
+  if (dir == 0) return up ? pos - W : -1;
+  if (dir == 1) return right ? pos + 1 : -1;
+  if (dir == 2) return down ? pos + W : -1;
+  return left ? pos - 1 : -1;
+}
+
+__device__ __forceinline__ bool is_cand(int code) { return code != kFloorCode && code != kWallCode; }
+
+// candidate list of G into cand[] (pos << 8 | code); returns the count
+__device__ __forceinline__ int warp_cands(const uint8_t* G, int HW, uint32_t* cand, int lane) {
+  int nc = 0;
+  for (int base = 0; base < HW; base += 32) {
+    const int p = base + lane;
+    const int code = p < HW ? G[p] : kFloorCode;
+    const uint32_t m = __ballot_sync(0xffffffffu, is_cand(code));
+    if (is_cand(code)) cand[nc + __popc(m & ((1u << lane) - 1u))] = ((uint32_t)p << 8) | (uint32_t)code;
+    nc += __popc(m);
+  }
+  __syncwarp();
+  return nc;
+}
+
+// first cell (row-major) holding `a` with `b` at the neighbour of `dir`, by one lane
+__device__ __forceinline__ int lane_find(const uint8_t* G, const uint32_t* cand, int nc, int H, int W, int a, int b,
+                                         int dir, int& q) {
+  if (is_cand(a)) {
+    for (int i = 0; i < nc; ++i) {
+      const uint32_t en = cand[i];
+      if ((int)(en & 0xff) != a) continue;
+      q = nb_match(G, H, W, (int)(en >> 8), b, dir);
+      if (q >= 0) return (int)(en >> 8);
+    }
+  } else {
+    for (int p = 0; p < H * W; ++p) {
+      if (G[p] != a) continue;
+      q = nb_match(G, H, W, p, b, dir);
+      if (q >= 0) return p;
+    }
+  }
+  q = -1;
+  return -1;
+}
+
+// The PUT_DOWN rule pass then the goal (ref:goals.py:347-394) of one env,
+// whole warp; rewritten cells go to G and through to `genv` in global
+// memory.  Returns goal | dirty << 1 on every lane.
+__device__ __noinline__ int warp_put_env(uint8_t* G, uint8_t* genv, uint32_t* cand, int lane, int H, int W, int ar,
+                                         int ac, const uint32_t* rules, int nr, uint32_t goal) {
+  const int HW = H * W;
+  int nc = warp_cands(G, HW, cand, lane);
+  bool dirty = false;
+  for (int s0 = 0; s0 < nr;) {
+    const int sl = s0 + lane;
+    int p = -1, q = -1, out = 0;
+    if (sl < nr) {
+      const uint32_t rw = rules[sl];
+      const int kind = rw & 0xff, a = (rw >> 8) & 0xff, b = (rw >> 16) & 0xff;
+      out = (int)(rw >> 24);
+      if (kind == 2 || (kind >= 8 && kind <= 11)) {  // AGENT_NEAR family
+        for (int k = 0; k < 4; ++k) {
+          const int kk = kind == 2 ? k : dir_slot(kind - 8);
+          const int r = ar + near_dr(kk), c = ac + near_dc(kk);
+          if (r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a) { p = r * W + c; break; }
+          if (kind != 2) break;
+        }
+      } else if (kind >= 3 && kind <= 7) {  // TILE_NEAR family
+        p = lane_find(G, cand, nc, H, W, a, b, kind == 3 ? -1 : kind - 4, q);
+      }
+    }
+    const uint32_t fired = __ballot_sync(0xffffffffu, p >= 0);
+    if (fired == 0) {
+      s0 += 32;
+      continue;
+    }
+    const int w = __ffs(fired) - 1;
+    p = __shfl_sync(0xffffffffu, p, w);
+    q = __shfl_sync(0xffffffffu, q, w);
+    out = __shfl_sync(0xffffffffu, out, w);
+    const int old = G[p];
+    __syncwarp();
+    if (lane == 0) {
+      G[p] = (uint8_t)out;
+      genv[p] = (uint8_t)out;
+      if (q >= 0) {
+        G[q] = kFloorCode;
+        genv[q] = kFloorCode;
+      }
+    }
+    __syncwarp();
+    if (!is_cand(old) && is_cand(out)) {
+      nc = warp_cands(G, HW, cand, lane);  // a new candidate cell: rebuild (rare)
+    } else {
+      for (int i = lane; i < nc; i += 32) {  // keep the list in step with G (positions unchanged)
+        const int pos = (int)(cand[i] >> 8);
+        if (pos == p) cand[i] = ((uint32_t)p << 8) | (uint32_t)out;
+        else if (pos == q) cand[i] = ((uint32_t)q << 8) | kFloorCode;
+      }
+      __syncwarp();
+    }
+    dirty = true;
+    s0 += w + 1;
+  }
+  bool hit = false;
+  const int kind = goal & 0xff, a1 = (goal >> 8) & 0xff, a2 = (goal >> 16) & 0xff, a3 = goal >> 24;
+  if (kind != 0 && kind <= 14 && ((cGoalGate[kind] >> 2) & 1)) {
+    switch (kind) {
+      case 2: hit = G[ar * W + ac] == a1; break;
+      case 5: hit = ar == a1 && ac == a2; break;
+      case 6: hit = a2 < H && a3 < W && G[a2 * W + a3] == a1; break;
+      case 3:
+        for (int k = 0; k < 4; ++k) {
+          const int r = ar + near_dr(k), c = ac + near_dc(k);
+          hit |= r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a1;
+        }
+        break;
+      case 11: case 12: case 13: case 14: {
+        const int r = ar + dir_dr(kind - 11), c = ac + dir_dc(kind - 11);
+        hit = r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a1;
+        break;
+      }
+      default: {  // TILE_NEAR goals: any matching cell, lanes over candidates / cells
+        const int dir = kind == 4 ? -1 : kind - 7;
+        bool any = false;
+        if (is_cand(a1)) {
+          for (int i = lane; i < nc; i += 32) {
+            const uint32_t en = cand[i];
+            any |= (int)(en & 0xff) == a1 && nb_match(G, H, W, (int)(en >> 8), a2, dir) >= 0;
+          }
+        } else {
+          for (int p = lane; p < HW; p += 32) any |= G[p] == a1 && nb_match(G, H, W, p, a2, dir) >= 0;
+        }
+        hit = __any_sync(0xffffffffu, any);
+      }
+    }
+  }
+  return (int)hit | ((int)dirty << 1);
+}
+
+#ifdef XMG_TRACE
+// debug builds: per-warp phase timestamps of step_rare (globaltimer, ns)
+__device__ unsigned long long g_trace[1 << 16][8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define XMG_TR(gw, k, v) \
+  if ((threadIdx.x & 31) == 0 && (gw) < (1 << 16)) g_trace[gw][k] = (v)
+#else
+#define XMG_TR(gw, k, v)
+#endif
+
+// Every lane's writes for the envs the warp just finished are made visible,
+// then each `mine` lane releases its env's chunk for the next step_main.
+__device__ __forceinline__ void release_envs(uint32_t* pending, bool mine, int64_t e) {
+  __threadfence();
+  __syncwarp();
+  if (mine) atomicSub(pending + e / 32, 1u);
+}
+
+constexpr int kPutBatch = 8;  // PUT_DOWN envs a step_rare warp prefetches together
+
 struct RareGeo {
-  int hwp, lg, ws, rbw, keys;
+  int hwp, lg, ws, rbw, keys, pgb, put;
   int64_t total;
 };
 
@@ -1107,10 +1682,12 @@ __host__ __device__ inline RareGeo make_rare_geo(int H, int W, int R) {
   g.lg = log2_buckets(H * W);
   g.rbw = round16(4 * (kRowHeader + R));
   g.keys = 32 * (int)sizeof(TrialKeys);
+  g.pgb = round16(H * W + 32);                      // one prefetched grid (16-byte chunks, unaligned start)
+  g.put = kPutBatch * (g.pgb + g.rbw + 16) + 4 * g.hwp;  // grids | rule rows | state words | candidates
   // per warp: wd: u64[hwp] | fc: u16[hwp] | slot: u16[hwp] | bk: u32[2^lg] | grid: u8[hwp] | misc: 64 u64
   //           | rules | 32 trial keys | env description
   g.ws = 8 * g.hwp + 2 * g.hwp + 2 * g.hwp + 4 * (1 << g.lg) + g.hwp + 512 + g.rbw + g.keys +
-         round16((int)sizeof(xmg_env_desc));
+         round16((int)sizeof(xmg_env_desc)) + g.put;
   g.total = (int64_t)kWarps * g.ws;
   return g;
 }
@@ -1118,11 +1695,13 @@ __host__ __device__ inline RareGeo make_rare_geo(int H, int W, int R) {
 // Rebuild env e's trial (ref:vecenv.py:359-361 -> :224-291), whole warp.
 __device__ __forceinline__ void warp_reset_env(const xmg_env_desc& d, const xmg_env_desc* sd, const xmg_state& s,
                                                const xmg_out& o, uint8_t* wbase, const RareGeo& geo, int lane,
-                                               int64_t e, const TrialKeys& key, int task, bool reset_mode) {
+                                               int64_t e, const TrialKeys* key, int task, bool reset_mode,
+                                               ResetOut* rs) {
   const int H = d.height, W = d.width, HW = H * W, V = d.view_size, ob = 2 * V * V;
   const WarpScratch ws = make_scratch(wbase, geo.hwp, geo.lg);
   const uint32_t g_in = d.scenario == XMG_SCENARIO_XLAND ? d.task_rows[(int64_t)task * d.row_words] : 0u;
-  const ResetOut ro = warp_build(sd, wbase, geo.hwp, geo.lg, lane, key, task, g_in, s.grids + e * (int64_t)HW);
+  warp_build(sd, wbase, geo.hwp, geo.lg, lane, key, task, g_in, s.grids + e * (int64_t)HW, rs);
+  const ResetOut ro = *rs;
   if (lane == 0) {
     reinterpret_cast<ulonglong2*>(s.rng)[e] = make_ulonglong2(ro.st_hi, ro.st_lo);
     reinterpret_cast<ulonglong2*>(s.agent)[e] = make_ulonglong2(
@@ -1142,22 +1721,26 @@ __device__ __forceinline__ void warp_reset_env(const xmg_env_desc& d, const xmg_
 __device__ __forceinline__ void warp_reset_group(const xmg_env_desc& d, const xmg_env_desc* sd, const xmg_state& s,
                                                  const xmg_out& o, uint8_t* wbase, const RareGeo& geo,
                                                  TrialKeys* keys, int lane, bool mine, int64_t e,
-                                                 const uint64_t* reset_keys) {
+                                                 const uint64_t* reset_keys, int gw = 0) {
   const bool resample = d.resample_tasks && d.scenario == XMG_SCENARIO_XLAND;
   int task = 0;
   if (mine) {
     const ulonglong2 ek = reinterpret_cast<const ulonglong2*>(reset_keys ? reset_keys : s.rng)[e];
     task = (int)(reinterpret_cast<const ulonglong2*>(s.agent)[e].y >> 32);
-    keys[lane] = derive_trial_keys(ek.x, ek.y, resample);
+    derive_trial_keys(ek.x, ek.y, resample, keys + lane);
   }
   uint32_t m = __ballot_sync(0xffffffffu, mine);
   __syncwarp();
+#ifdef XMG_TRACE
+  XMG_TR(gw, 7, gtime());
+#endif
   while (m) {
     const int src = __ffs(m) - 1;
     m &= m - 1;
     const int64_t es = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)e, src);
     const int ts = __shfl_sync(0xffffffffu, task, src);
-    warp_reset_env(d, sd, s, o, wbase, geo, lane, es, keys[src], ts, reset_keys != nullptr);
+    warp_reset_env(d, sd, s, o, wbase, geo, lane, es, keys + src, ts, reset_keys != nullptr,
+                   reinterpret_cast<ResetOut*>(make_scratch(wbase, geo.hwp, geo.lg).misc + 40));
   }
 }
 
@@ -1173,17 +1756,25 @@ template <int KMAX>
 __global__ void __launch_bounds__(kThreads, XMG_MINB_RARE) step_rare(const xmg_env_desc d, const xmg_state s,
                                                                      const xmg_out o, const uint64_t* reset_keys,
                                                                      const uint32_t* abort_flag, uint32_t epoch,
-                                                                     int64_t n) {
+                                                                     int64_t n, int track) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gw = blockIdx.x * kWarps + warp, tw = gridDim.x * kWarps;
+#ifdef XMG_TRACE
+  const unsigned long long t_start = gtime();
+  XMG_TR(gw, 0, t_start);
+#endif
   const bool reset_mode = reset_keys != nullptr;
   const int q = gw % kQueues, j = gw / kQueues, per_q = tw / kQueues;
   int64_t cnt_put = 0, cnt_reset = 0;
   if (!reset_mode) {
     cnt_put = s.work[count_index(epoch, 0, q)];
     cnt_reset = s.work[count_index(epoch, 1, q)];
-    if (j >= cnt_put && j >= cnt_reset) return;  // nothing queued for this warp
+    const bool idle = j >= cnt_put && j >= cnt_reset;
+    // the counts are read (and used): the next step's step_main may launch
+    // (it clears them), and waits per tile on `pending` for the envs below
+    if (track) griddep_launch();
+    if (idle) return;  // nothing queued for this warp
   } else if (gw >= n) {
     return;
   }
@@ -1193,11 +1784,12 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB_RARE) step_rare(const xmg_e
   const RareGeo geo = make_rare_geo(H, W, R);
   uint8_t* wbase = smem + warp * geo.ws;
   const WarpScratch ws = make_scratch(wbase, geo.hwp, geo.lg);
-  uint32_t* rules_s = reinterpret_cast<uint32_t*>(wbase + geo.ws - geo.rbw - geo.keys -
-                                                  round16((int)sizeof(xmg_env_desc)));
-  TrialKeys* keys = reinterpret_cast<TrialKeys*>(wbase + geo.ws - geo.keys - round16((int)sizeof(xmg_env_desc)));
+  uint8_t* tail = wbase + geo.ws - geo.put;  // PUT_DOWN prefetch area
+  uint32_t* rules_s = reinterpret_cast<uint32_t*>(tail - geo.rbw - geo.keys - round16((int)sizeof(xmg_env_desc)));
+  TrialKeys* keys = reinterpret_cast<TrialKeys*>(tail - geo.keys - round16((int)sizeof(xmg_env_desc)));
   // this warp's copy of the description, for the out-of-line paths
-  xmg_env_desc* sdesc = reinterpret_cast<xmg_env_desc*>(wbase + geo.ws - round16((int)sizeof(xmg_env_desc)));
+  xmg_env_desc* sdesc = reinterpret_cast<xmg_env_desc*>(tail - round16((int)sizeof(xmg_env_desc)));
+  (void)rules_s;
   if (lane == 0) *sdesc = d;
   __syncwarp();
   const bool see = d.see_through_walls != 0;
@@ -1211,68 +1803,117 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB_RARE) step_rare(const xmg_e
     return;
   }
 
-  // ---- PUT_DOWN events
+  // ---- PUT_DOWN events: entries j, j + per_q, ... of sub-queue q, kPutBatch
+  // at a time prefetched into shared memory (one env per lane), then
+  // resolved one by one by the whole warp
   if (j < cnt_put) {
-    // this lane's word of the first / last column bitmaps
-    uint32_t col0 = 0, colL = 0;
-    for (int p = (32 * lane + W - 1) / W * W; p < 32 * lane + 32 && p < HW; p += W) col0 |= 1u << (p - 32 * lane);
-    for (int p = (32 * lane) / W * W + W - 1; p < 32 * lane + 32 && p < HW; p += W)
-      if (p >= 32 * lane) colL |= 1u << (p - 32 * lane);
-    const uint32_t* qp = s.work + kWorkHeader + (int64_t)q * qcap;
-    for (int64_t i = j; i < cnt_put; i += per_q) {
-      const int64_t e = qp[i];
-      uint8_t* genv = s.grids + e * (int64_t)HW;
-      const ulonglong2 ag = reinterpret_cast<const ulonglong2*>(s.agent)[e];
-      for (int k = lane; k < HW; k += 32) ws.grid[k] = genv[k];
-      const int task = (int)(ag.y >> 32);
-      if (R > 0) {
-        const uint32_t* row = d.task_rows + (int64_t)task * d.row_words;
-        for (int k = lane; k < kRowHeader + R; k += 32) rules_s[k] = row[k];
+    const uint32_t* qp = s.work + queue_base(n, epoch, 0, q);
+    uint8_t* pg = tail;                                                  // kPutBatch grids
+    uint32_t* pr = reinterpret_cast<uint32_t*>(tail + kPutBatch * geo.pgb);  // kPutBatch rule rows
+    ulonglong2* pa = reinterpret_cast<ulonglong2*>(tail + kPutBatch * (geo.pgb + geo.rbw));  // state words
+    uint32_t* pc = reinterpret_cast<uint32_t*>(tail + kPutBatch * (geo.pgb + geo.rbw + 16));  // candidates
+    const bool resample = d.resample_tasks && d.scenario == XMG_SCENARIO_XLAND;
+    for (int64_t i0 = j; i0 < cnt_put; i0 += (int64_t)kPutBatch * per_q) {
+      const int64_t it = i0 + (int64_t)lane * per_q;
+      const bool mine = lane < kPutBatch && it < cnt_put;
+      int64_t e_l = 0;
+      int off_l = 0;
+      if (mine) {
+        e_l = qp[it];
+        const uintptr_t g0 = reinterpret_cast<uintptr_t>(s.grids + e_l * (int64_t)HW);
+        const uintptr_t a0 = g0 & ~uintptr_t(15);
+        off_l = (int)(g0 - a0);
+        const int nch = (off_l + HW + 15) >> 4;
+        for (int k = 0; k < nch; ++k) cp_async16(pg + lane * geo.pgb + 16 * k, reinterpret_cast<const void*>(a0 + 16 * k));
+        const ulonglong2 ag = reinterpret_cast<const ulonglong2*>(s.agent)[e_l];
+        pa[lane] = ag;
+        if (R > 0) {
+          const uint32_t* row = d.task_rows + (int64_t)(ag.y >> 32) * d.row_words;
+          for (int k = 0; k < (kRowHeader + R + 3) >> 2; ++k) cp_async16(pr + lane * (geo.rbw / 4) + 4 * k, row + 4 * k);
+        }
+        cp_async_wait_all();
       }
       __syncwarp();
-      const int r = (int)(ag.x & 0xff), c = (int)((ag.x >> 8) & 0xff), dir = (int)((ag.x >> 16) & 3);
-      const uint32_t sc = (uint32_t)(ag.x >> 32);
-      const int nr = R > 0 ? (int)(rules_s[1] & 0xff) : 0;
-      Cells<KMAX> cl;
-      cells_load<KMAX>(cl, ws.grid, HW, lane);
-      const int res = warp_put_event<KMAX>(ws.grid, cl, genv, lane, H, W, r, c, rules_s + kRowHeader, nr,
-                                           (uint32_t)ag.y, col0, colL);
-      const bool last = (res & 1) || sc >= (uint32_t)d.budget;
-      const float rew = (res & 1) ? goal_reward(sc, d.budget) : 0.f;
-      if (lane == 0) {
-        o.reward[e] = rew;
-        o.discount[e] = last ? 0.f : 1.f;
-        o.step_type[e] = last ? 2 : 1;
-        if (o.stats != nullptr && (rew != 0.f || last)) {
-          const int slot = (int)(e / kThreads);
-          atomicAdd(o.stats + 3 * slot, (double)rew);
-          if (last) {
-            atomicAdd(o.stats + 3 * slot + 1, 1.0);
-            atomicAdd(o.stats + 3 * slot + 2, (double)sc);
+#ifdef XMG_TRACE
+      if (i0 == j) XMG_TR(gw, 4, gtime());
+#endif
+      uint32_t m = __ballot_sync(0xffffffffu, mine), lastm = 0;
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const int64_t e = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)e_l, src);
+        const int off = __shfl_sync(0xffffffffu, off_l, src);
+        const ulonglong2 ag = pa[src];
+        const int r = (int)(ag.x & 0xff), c = (int)((ag.x >> 8) & 0xff), dir = (int)((ag.x >> 16) & 3);
+        const uint32_t sc = (uint32_t)(ag.x >> 32);
+        const uint32_t* rt = pr + src * (geo.rbw / 4);
+        const int nr = R > 0 ? (int)(rt[1] & 0xff) : 0;
+        uint8_t* G = pg + src * geo.pgb + off;
+        const int res = warp_put_env(G, s.grids + e * (int64_t)HW, pc, lane, H, W, r, c, rt + kRowHeader, nr,
+                                     (uint32_t)ag.y);
+        const bool last = (res & 1) || sc >= (uint32_t)d.budget;
+#ifdef XMG_TRACE
+        if (i0 == j && src == 0) XMG_TR(gw, 5, gtime());
+#endif
+        if (lane == 0) {
+          const float rew = (res & 1) ? goal_reward(sc, d.budget) : 0.f;
+          o.reward[e] = rew;
+          o.discount[e] = last ? 0.f : 1.f;
+          o.step_type[e] = last ? 2 : 1;
+          if (o.stats != nullptr && (rew != 0.f || last)) {
+            const int slot = (int)(e / kThreads);
+            atomicAdd(o.stats + 3 * slot, (double)rew);
+            if (last) {
+              atomicAdd(o.stats + 3 * slot + 1, 1.0);
+              atomicAdd(o.stats + 3 * slot + 2, (double)sc);
+            }
           }
         }
-      }
-      if (last) {
-        const ulonglong2 ek = reinterpret_cast<const ulonglong2*>(s.rng)[e];
-        const TrialKeys key = warp_trial_keys(lane, ek.x, ek.y, d.resample_tasks && d.scenario == XMG_SCENARIO_XLAND);
-        __syncwarp();
-        warp_reset_env(d, sdesc, s, o, wbase, geo, lane, e, key, task, false);
-      } else if ((res & 2) && o.obs != nullptr) {
         // a rule changed the grid: the observation step_main wrote is stale
-        warp_obs(ws.grid, o.obs + e * ob, lane, r, c, dir, H, W, V, see);
+        if ((res & 2) && !last && o.obs != nullptr) warp_obs(G, o.obs + e * ob, lane, r, c, dir, H, W, V, see);
+        if (last) lastm |= 1u << src;
       }
-      __syncwarp();
+#ifdef XMG_TRACE
+      if (i0 == j) XMG_TR(gw, 6, gtime());
+#endif
+      // ---- trials the PUT_DOWN finished: keys derived one env per lane, then
+      // the envs rebuilt by the whole warp
+      if (lastm) {
+        if ((lastm >> lane) & 1) {
+          const ulonglong2 ek = reinterpret_cast<const ulonglong2*>(s.rng)[e_l];
+          derive_trial_keys(ek.x, ek.y, resample, keys + lane);
+        }
+        __syncwarp();
+        while (lastm) {
+          const int src = __ffs(lastm) - 1;
+          lastm &= lastm - 1;
+          const int64_t es = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)e_l, src);
+          const int ts = (int)(pa[src].y >> 32);
+          warp_reset_env(d, sdesc, s, o, wbase, geo, lane, es, keys + src, ts, false,
+                         reinterpret_cast<ResetOut*>(ws.misc + 40));
+        }
+      }
+      if (track) release_envs(s.work + pending_base(n), mine, e_l);
     }
   }
+#ifdef XMG_TRACE
+  XMG_TR(gw, 1, gtime());
+  XMG_TR(gw, 3, (unsigned long long)cnt_put | ((unsigned long long)cnt_reset << 32));
+#endif
   // ---- trial resets, 32 at a time (entries i0 + lane * per_q)
   if (j < cnt_reset) {
-    const uint32_t* qp = s.work + kWorkHeader + (int64_t)(kQueues + q) * qcap;
+    const uint32_t* qp = s.work + queue_base(n, epoch, 1, q);
     for (int64_t i0 = j; i0 < cnt_reset; i0 += 32 * (int64_t)per_q) {
       const int64_t i = i0 + (int64_t)lane * per_q;
       const bool mine = i < cnt_reset;
-      warp_reset_group(d, sdesc, s, o, wbase, geo, keys, lane, mine, mine ? (int64_t)qp[i] : 0, nullptr);
+      const int64_t e = mine ? (int64_t)qp[i] : 0;
+      warp_reset_group(d, sdesc, s, o, wbase, geo, keys, lane, mine, e, nullptr, gw);
+      if (track) release_envs(s.work + pending_base(n), mine, e);
     }
   }
+#ifdef XMG_TRACE
+  XMG_TR(gw, 2, gtime());
+#endif
 }
 
 // ------------------------------------------------------- helper kernels
@@ -1307,18 +1948,54 @@ __global__ void random_actions_kernel(const uint64_t* keys, int64_t n, int64_t t
   }
 }
 
-__global__ void validate_kernel(const void* a, int dtype, int64_t n, uint32_t epoch, uint32_t* flag) {
-  bool bad = false;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t v;
-    switch (dtype) {
-      case XMG_ACT_U8: v = reinterpret_cast<const uint8_t*>(a)[i]; break;
-      case XMG_ACT_I32: v = reinterpret_cast<const int32_t*>(a)[i]; break;
-      default: v = reinterpret_cast<const int64_t*>(a)[i];
-    }
-    bad |= v < 0 || v >= 6;
+// One small grid (it runs beside the previous step's step_rare): 16-byte
+// loads, every byte / word checked against [0, 6).
+__device__ __forceinline__ bool bad_action(const uint8_t* a, int dtype, int64_t i) {
+  int64_t v;
+  switch (dtype) {
+    case XMG_ACT_U8: v = a[i]; break;
+    case XMG_ACT_I32: v = reinterpret_cast<const int32_t*>(a)[i]; break;
+    default: v = reinterpret_cast<const int64_t*>(a)[i];
   }
+  return v < 0 || v >= 6;
+}
+
+__global__ void validate_kernel(const void* a, int dtype, int64_t n, uint32_t epoch, uint32_t* flag) {
+  griddep_launch();  // the step's step_main may launch; it waits for this grid to finish
+  const uint8_t* p = reinterpret_cast<const uint8_t*>(a);
+  const int es = dtype == XMG_ACT_U8 ? 1 : dtype == XMG_ACT_I32 ? 4 : 8;
+  const int64_t bytes = n * es;
+  // elements before the first 16-byte boundary, and the 16-byte body
+  const int64_t head = (int64_t)((16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15) / es;
+  const int64_t nvec = head * es < bytes ? (bytes - head * es) / 16 : 0;
+  const uint4* body = reinterpret_cast<const uint4*>(p + head * es);
+  const int64_t tail0 = head + nvec * 16 / es;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  for (int64_t i = tid; i < nvec; i += nt) {
+    const uint4 v = body[i];
+    if (dtype == XMG_ACT_U8) {  // bytes >= 6 (unsigned: negative int8 can't occur in uint8)
+      const uint32_t six = 0x06060606u;
+      bad |= (__vcmpgeu4(v.x, six) | __vcmpgeu4(v.y, six) | __vcmpgeu4(v.z, six) | __vcmpgeu4(v.w, six)) != 0;
+    } else if (dtype == XMG_ACT_I32) {
+      bad |= v.x >= 6u || v.y >= 6u || v.z >= 6u || v.w >= 6u;  // unsigned compare catches negatives
+    } else {
+      bad |= (v.y != 0u || v.x >= 6u) || (v.w != 0u || v.z >= 6u);
+    }
+  }
+  for (int64_t i = tid; i < head && i < n; i += nt) bad |= bad_action(p, dtype, i);
+  for (int64_t i = tail0 + tid; i < n; i += nt) bad |= bad_action(p, dtype, i);
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicMax(flag, epoch);
+  // the last CTA to finish publishes flag[1] = epoch (and re-arms the counter)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(flag + 2, 1u) == gridDim.x - 1) {
+      flag[2] = 0;
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag + 1), "r"(epoch) : "memory");
+    }
+  }
 }
 
 // ------------------------------------------------------- host side
@@ -1354,6 +2031,16 @@ cudaError_t allow_smem(K kernel, int64_t dyn) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem - (int)fa.sharedSizeBytes);
 }
 
+// XMG_PDL=0 turns the programmatic (overlapped) launches off
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* v = getenv("XMG_PDL");
+    on = (v && !strcmp(v, "0")) ? 0 : 1;
+  }
+  return on == 1;
+}
+
 template <int MAXCH>
 int launch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
                 const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st) {
@@ -1363,8 +2050,20 @@ int launch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, con
   std::call_once(once, [] { attr_err = allow_smem(step_main<MAXCH>, kMaxDynSmem - 1024); });
   if (attr_err != cudaSuccess) return fail(std::string("step_main attributes: ") + cudaGetErrorString(attr_err));
   const int64_t blocks = (n + kThreads - 1) / kThreads;
-  step_main<MAXCH><<<(unsigned)blocks, kThreads, (size_t)geo.total, st>>>(*d, *s, *o, actions, dtype, flag, epoch,
-                                                                         n);
+  // programmatic dependent of the previous kernel on the stream (the previous
+  // step's step_rare, or this step's validation)
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = (size_t)geo.total;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t err = cudaLaunchKernelEx(&cfg, step_main<MAXCH>, *d, *s, *o, actions, dtype, flag, epoch, n);
+  if (err != cudaSuccess) return fail(std::string("step_main: ") + cudaGetErrorString(err));
   return check_launch("step_main");
 }
 
@@ -1375,27 +2074,45 @@ int kmax_of(const xmg_env_desc* d) {
 
 template <int KMAX>
 int launch_rare_k(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const uint64_t* keys,
-                  const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st) {
+                  const uint32_t* flag, uint32_t epoch, int64_t n, int track, cudaStream_t st) {
   const RareGeo geo = make_rare_geo(d->height, d->width, d->rule_width);
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] { attr_err = allow_smem(step_rare<KMAX>, kMaxDynSmem - 1024); });
   if (attr_err != cudaSuccess) return fail(std::string("step_rare attributes: ") + cudaGetErrorString(attr_err));
-  // one warp per 64 envs (the queues hold ~1.5% of the envs per step in
-  // steady state); a multiple of 32 CTAs so every sub-queue gets equal warps
-  int64_t blocks = (n + 4 * 64 - 1) / (4 * 64);
-  blocks = (blocks + 31) / 32 * 32;
-  step_rare<KMAX><<<(unsigned)blocks, kThreads, (size_t)geo.total, st>>>(*d, *s, *o, keys, flag, epoch, n);
+  // one resident wave (warps stride over their sub-queue's entries); a
+  // multiple of 32 CTAs so every sub-queue gets equal warps
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_rare<KMAX>, kThreads, (size_t)geo.total) !=
+          cudaSuccess || per_sm < 1)
+    return fail("step_rare does not fit on an SM");
+  static int cap = -1;  // XMG_RARE_CTAS: resident step_rare CTAs per SM (tuning)
+  if (cap < 0) {
+    const char* v = getenv("XMG_RARE_CTAS");
+    cap = v ? atoi(v) : 0;
+  }
+  if (cap > 0 && per_sm > cap) per_sm = cap;
+  int64_t blocks = (int64_t)per_sm * sms / 32 * 32;
+  const int64_t need = ((n + 4 * 64 - 1) / (4 * 64) + 31) / 32 * 32;  // <= one warp per 64 envs
+  if (blocks > need) blocks = need;
+  if (blocks < 32) blocks = 32;
+  step_rare<KMAX><<<(unsigned)blocks, kThreads, (size_t)geo.total, st>>>(*d, *s, *o, keys, flag, epoch, n, track);
   return check_launch("step_rare");
 }
 
 int launch_rare(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const uint64_t* keys,
-                const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st) {
+                const uint32_t* flag, uint32_t epoch, int64_t n, int track, cudaStream_t st) {
   switch (kmax_of(d)) {
-    case 4: return launch_rare_k<4>(d, s, o, keys, flag, epoch, n, st);
-    case 8: return launch_rare_k<8>(d, s, o, keys, flag, epoch, n, st);
-    case 20: return launch_rare_k<20>(d, s, o, keys, flag, epoch, n, st);
-    default: return launch_rare_k<32>(d, s, o, keys, flag, epoch, n, st);
+    case 4: return launch_rare_k<4>(d, s, o, keys, flag, epoch, n, track, st);
+    case 8: return launch_rare_k<8>(d, s, o, keys, flag, epoch, n, track, st);
+    case 20: return launch_rare_k<20>(d, s, o, keys, flag, epoch, n, track, st);
+    default: return launch_rare_k<32>(d, s, o, keys, flag, epoch, n, track, st);
   }
 }
 
@@ -1420,8 +2137,49 @@ int validate_desc(const xmg_env_desc* d, const xmg_state* s, int64_t n) {
   return 0;
 }
 
+template <int KMAX>
+int launch_stream(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
+                  const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st) {
+  const StreamGeo geo = make_stream_geo(d->height * d->width, d->view_size, d->rule_width);
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  static int sms = 148;
+  std::call_once(once, [] {
+    attr_err = allow_smem(step_stream<KMAX>, kMaxDynSmem - 1024);
+    int dev = 0;
+    if (attr_err == cudaSuccess) attr_err = cudaGetDevice(&dev);
+    if (attr_err == cudaSuccess) attr_err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  });
+  if (attr_err != cudaSuccess) return fail(std::string("step_stream attributes: ") + cudaGetErrorString(attr_err));
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_stream<KMAX>, kStreamWarps * 32,
+                                                    (size_t)geo.total) != cudaSuccess || per_sm < 1)
+    return fail("step_stream does not fit on an SM");
+  const int64_t nchunks = (n + 31) / 32;
+  int64_t blocks = (int64_t)per_sm * sms;
+  const int64_t need = (nchunks + kStreamWarps - 1) / kStreamWarps;
+  if (blocks > need) blocks = need;
+  step_stream<KMAX><<<(unsigned)blocks, kStreamWarps * 32, (size_t)geo.total, st>>>(*d, *s, *o, actions, dtype, flag,
+                                                                                  epoch, n);
+  return check_launch("step_stream");
+}
+
+bool use_stream(const xmg_env_desc* d) {
+  static int mode = -1;  // XMG_MAIN=stream|window (default: window)
+  if (mode < 0) {
+    const char* m = getenv("XMG_MAIN");
+    mode = (m && !strcmp(m, "stream")) ? 1 : 0;
+  }
+  return mode == 1 && d->height * d->width <= 256 &&
+         make_stream_geo(d->height * d->width, d->view_size, d->rule_width).total <= kMaxDynSmem - 1024;
+}
+
 int dispatch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
                   const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st) {
+  if (use_stream(d)) {
+    if (d->height * d->width <= 128) return launch_stream<4>(d, s, o, actions, dtype, flag, epoch, n, st);
+    return launch_stream<8>(d, s, o, actions, dtype, flag, epoch, n, st);
+  }
   switch (pick_maxch(d)) {
     case 6: return launch_main<6>(d, s, o, actions, dtype, flag, epoch, n, st);
     case 8: return launch_main<8>(d, s, o, actions, dtype, flag, epoch, n, st);
@@ -1490,8 +2248,25 @@ int32_t xmg_validate_actions(const void* actions, int32_t dtype, int64_t n, uint
   if (n <= 0) return 0;
   if (dtype < 0 || dtype > 2) return fail("unknown action dtype");
   if (!flag) return fail("null flag");
-  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 8);
-  validate_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(actions, dtype, n, epoch, flag);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, sms));
+  // may overlap the previous step's step_rare (it only reads the actions)
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(256);
+  cfg.stream = (cudaStream_t)stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t err = cudaLaunchKernelEx(&cfg, validate_kernel, actions, (int)dtype, n, epoch, flag);
+  if (err != cudaSuccess) return fail(std::string("validate_kernel: ") + cudaGetErrorString(err));
   return check_launch("validate_kernel");
 }
 
@@ -1499,7 +2274,7 @@ int32_t xmg_reset(const xmg_env_desc* desc, const xmg_state* state, const uint64
                   const xmg_out* out, void* stream) {
   if (validate_desc(desc, state, n)) return -1;
   if (!out || !keys) return fail("null out/keys");
-  return launch_rare(desc, state, out, keys, nullptr, 0, n, (cudaStream_t)stream);
+  return launch_rare(desc, state, out, keys, nullptr, 0, n, 0, (cudaStream_t)stream);
 }
 
 int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* actions, int32_t action_dtype,
@@ -1507,8 +2282,13 @@ int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* a
   if (validate_desc(desc, state, n)) return -1;
   if (!out || !actions) return fail("null out/actions");
   if (action_dtype < 0 || action_dtype > 2) return fail("unknown action dtype");
+  if ((reinterpret_cast<uintptr_t>(state->grids) & 15) ||
+      (reinterpret_cast<uintptr_t>(state->agent) & 15) || (out->obs && (reinterpret_cast<uintptr_t>(out->obs) & 15)))
+    return fail("actions / grids / agent / obs buffers must be 16-byte aligned");
   if (dispatch_main(desc, state, out, actions, action_dtype, abort_flag, epoch, n, (cudaStream_t)stream)) return -1;
-  return launch_rare(desc, state, out, nullptr, abort_flag, epoch, n, (cudaStream_t)stream);
+  // step_main (window mode) records the tiles step_rare must release
+  const int track = use_stream(desc) ? 0 : 1;
+  return launch_rare(desc, state, out, nullptr, abort_flag, epoch, n, track, (cudaStream_t)stream);
 }
 
 int64_t xmg_step_smem_bytes(const xmg_env_desc* desc) {
@@ -1518,6 +2298,18 @@ int64_t xmg_step_smem_bytes(const xmg_env_desc* desc) {
   return a > b ? a : b;
 }
 
-int64_t xmg_work_words(int64_t n) { return kWorkHeader + 2 * kQueues * queue_cap(n); }
+int64_t xmg_work_words(int64_t n) { return work_words(n); }
+
+#ifdef XMG_TRACE
+int32_t xmg_debug_trace(unsigned long long* host_out, int64_t rows) {
+  return cudaMemcpyFromSymbol(host_out, g_trace, (size_t)rows * 8 * sizeof(unsigned long long)) == cudaSuccess ? 0
+                                                                                                              : -1;
+}
+int32_t xmg_debug_trace_clear(void) {
+  void* ptr = nullptr;
+  if (cudaGetSymbolAddress(&ptr, g_trace) != cudaSuccess) return -1;
+  return cudaMemset(ptr, 0, sizeof(g_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 }  // extern "C"

@@ -226,7 +226,9 @@ class VecEnv:
         self.agent = torch.from_numpy(agent.view(np.int64)).to(dev)
         self.rng = torch.zeros((n, 2), dtype=torch.int64, device=dev)
         self.work = torch.zeros(int(_lib.lib().xmg_work_words(n)), dtype=torch.int32, device=dev)
-        self._flag = torch.zeros(1, dtype=torch.int32, device=dev)  # epoch of the last rejected batch
+        # validation flag block (include/xmg.h XMG_FLAG_WORDS): [0] epoch of the
+        # last rejected batch, [1] epoch of the last finished validation
+        self._flag = torch.zeros(4, dtype=torch.int32, device=dev)
         self.epoch = 0          # steps issued on this state (queue parity, rejection tags)
         self._checked_epoch = 0
 
@@ -359,7 +361,7 @@ class VecEnv:
 
     def check(self) -> None:
         """Raise InvalidAction if a device-validated batch was rejected (syncs)."""
-        flagged = int(self._flag.item()) & 0xFFFFFFFF  # syncs the stream
+        flagged = int(self._flag[0].item()) & 0xFFFFFFFF  # syncs the stream
         if flagged > self._checked_epoch:
             self._checked_epoch = flagged
             raise InvalidAction(f"action outside [0, 5] at step {flagged}; that batch was not applied")

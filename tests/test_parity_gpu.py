@@ -142,6 +142,31 @@ def test_invalid_device_actions_mutate_nothing():
         strict.step(bad)
 
 
+@pytest.mark.parametrize("dtype", [torch.uint8, torch.int32, torch.int64])
+def test_validation_catches_every_position(dtype):
+    """Device-side validation (vectorised body, scalar head / tail) rejects a
+    single bad action anywhere, for each dtype and a misaligned view."""
+    from paper_2312_12044_b200 import EnvParams, InvalidAction, VecEnv, key_from_seed
+    n = 1000
+    vec = VecEnv(EnvParams(), n)
+    vec.reset(key_from_seed(0))
+    store = torch.zeros(n + 8, dtype=dtype, device="cuda")
+    for shift in (0, 1, 3):
+        acts = store[shift:shift + n]
+        acts.fill_(5)
+        vec.step(acts)
+        vec.check()  # all valid
+        for pos in (0, 1, 2, 15, 16, 17, 500, n - 17, n - 2, n - 1):
+            for badv in ((6, 255) if dtype == torch.uint8 else (6, -1, 1 << 20)):
+                acts.fill_(2)
+                acts[pos] = badv
+                g = vec.grids.clone()
+                vec.step(acts)
+                with pytest.raises(InvalidAction):
+                    vec.check()
+                assert torch.equal(vec.grids, g), (shift, pos, badv)
+
+
 def test_shards_reproduce_the_global_batch():
     """Env-range shards with global key offsets == one big batch
     (ref tests/test_harness.py:105-122, tests/test_acceptance.py:494-517)."""
