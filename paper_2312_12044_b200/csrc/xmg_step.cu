@@ -232,23 +232,21 @@ __device__ __forceinline__ int nbr_code(const Nbrs& nb, int k) {
 }
 
 // Rules gated on MOVE / PICK_UP (only the slots in `slots`, stored order).
+// Select-based, so lanes holding different rule kinds stay converged.
 __device__ XMG_RARE int agent_rules(View vw, Nbrs& nb, const uint32_t* rules, uint32_t slots, int pocket) {
   for (; slots; slots &= slots - 1) {
     const uint32_t rw = rules[__ffs(slots) - 1];
     const int kind = rw & 0xff, a = (rw >> 8) & 0xff, out = rw >> 24;
-    if (kind == 1) {  // AGENT_HOLD
-      if (pocket == a) pocket = (out >> 4) == kFloor ? 0 : out;
-      continue;
-    }
-    // AGENT_NEAR: first neighbour holding a; AGENT_NEAR_{UP,RIGHT,DOWN,LEFT}: one slot
-    int k = -1;
-    if (kind == 2) {
-      k = nb.code[0] == a ? 0 : nb.code[1] == a ? 1 : nb.code[2] == a ? 2 : nb.code[3] == a ? 3 : -1;
-    } else if (kind >= 8 && kind <= 11) {
-      const int q = dir_slot(kind - 8);
-      if (nbr_code(nb, q) == a) k = q;
-    }
-    if (k >= 0) {
+    // AGENT_HOLD
+    pocket = (kind == 1 && pocket == a) ? ((out >> 4) == kFloor ? 0 : out) : pocket;
+    // AGENT_NEAR: first neighbour holding a (slots up, left, right, down);
+    // AGENT_NEAR_{UP,RIGHT,DOWN,LEFT}: the one slot of that direction
+    const uint32_t m = (uint32_t)(nb.code[0] == a) | ((uint32_t)(nb.code[1] == a) << 1) |
+                       ((uint32_t)(nb.code[2] == a) << 2) | ((uint32_t)(nb.code[3] == a) << 3);
+    const uint32_t allow = kind == 2 ? 0xFu : (kind >= 8 && kind <= 11) ? (0x2841u >> (4 * (kind - 8))) & 0xFu : 0u;
+    const uint32_t hit = m & allow;
+    if (hit) {
+      const int k = __ffs(hit) - 1;
 #pragma unroll
       for (int t = 0; t < 4; ++t)
         if (t == k) {
@@ -266,14 +264,12 @@ __device__ __forceinline__ bool agent_goal(const Nbrs& nb, int own, uint32_t goa
                                            int pocket) {
   const int kind = goal & 0xff, a1 = (goal >> 8) & 0xff, a2 = (goal >> 16) & 0xff;
   if (kind == 0 || kind > 14 || !((cGoalGate[kind] >> ev) & 1)) return false;
-  switch (kind) {
-    case 1: return pocket == a1;
-    case 2: return own == a1;
-    case 5: return ar == a1 && ac == a2;
-    case 3: return nb.code[0] == a1 || nb.code[1] == a1 || nb.code[2] == a1 || nb.code[3] == a1;
-    case 11: case 12: case 13: case 14: return nbr_code(nb, dir_slot(kind - 11)) == a1;
-    default: return false;
-  }
+  // select-based (no per-kind branches)
+  const uint32_t m = (uint32_t)(nb.code[0] == a1) | ((uint32_t)(nb.code[1] == a1) << 1) |
+                     ((uint32_t)(nb.code[2] == a1) << 2) | ((uint32_t)(nb.code[3] == a1) << 3);
+  const uint32_t allow = kind == 3 ? 0xFu : (kind >= 11 && kind <= 14) ? (0x2841u >> (4 * (kind - 11))) & 0xFu : 0u;
+  return (m & allow) != 0 || (kind == 1 && pocket == a1) || (kind == 2 && own == a1) ||
+         (kind == 5 && ar == a1 && ac == a2);
 }
 
 // ------------------------------------------------------- observation
@@ -809,7 +805,9 @@ __device__ __forceinline__ bool batch_rejected(const uint32_t* flag, uint32_t ep
   return flag != nullptr && *reinterpret_cast<volatile const uint32_t*>(flag) == epoch;
 }
 
-template <int MAXCH>
+// FULL: small grids are staged whole, issued before the state word arrives
+// (one DRAM round trip per env instead of two: state word -> view window).
+template <int MAXCH, bool FULL>
 __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_desc d, const xmg_state s,
                                                                 const xmg_out o, const void* actions, int act_dtype,
                                                                 const uint32_t* abort_flag, uint32_t epoch,
@@ -851,6 +849,7 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
   vw.stage = smem + tid * geo.stg;
   vw.sbase = vw.slo = vw.shi = 0;
   uint32_t* rbuf = reinterpret_cast<uint32_t*>(rb_base + tid * geo.rb);
+  if (FULL && valid) stage_issue<MAXCH>(vw, 0, HW, HW);
 
   // ---- load: the 16-byte state word and the action
   ulonglong2 ag = make_ulonglong2(0, 0);
@@ -873,6 +872,10 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
     }
     __syncwarp();
     if (valid) ag = ld_cg_u64x2(reinterpret_cast<const ulonglong2*>(s.agent) + e);
+    if (FULL && valid) {  // the early grid copy may predate step_rare's writes
+      cp_async_wait_all();
+      stage_issue<MAXCH>(vw, 0, HW, HW);
+    }
   }
   int r = (int)(ag.x & 0xff), c = (int)((ag.x >> 8) & 0xff), dir = (int)((ag.x >> 16) & 3);
   int pocket = (int)((ag.x >> 24) & 0xff);
@@ -887,9 +890,11 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
     // ---- stage the post-action window (MOVE: both candidate poses) and,
     // for actions that can raise an event, the env's rule row
     const int nd = act == 1 ? ((dir + 3) & 3) : (act == 2 ? ((dir + 1) & 3) : dir);
-    int lo, hi;
-    window_span(r, c, nd, act == 0 ? 1 : 0, H, W, V, lo, hi);
-    stage_issue<MAXCH>(vw, lo, hi, HW);
+    if (!FULL) {
+      int lo, hi;
+      window_span(r, c, nd, act == 0 ? 1 : 0, H, W, V, lo, hi);
+      stage_issue<MAXCH>(vw, lo, hi, HW);
+    }
     const bool rules_needed = R > 0 && (act == 0 || act == 3);
     if (rules_needed) {
       const uint32_t* src = d.task_rows + (int64_t)task * d.row_words;
@@ -903,31 +908,18 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
     const bool inside = tr >= 0 && tr < H && tc >= 0 && tc < W;
     const int tflat = tr * W + tc;
     const int tcode = inside ? vw.rd(tflat) : 0, tt = tcode >> 4;
-    int ev = -1;
-    switch (act) {
-      case 0:
-        if (inside && ((kWalkable >> tt) & 1)) { r = tr; c = tc; ev = 0; }
-        break;
-      case 1: dir = nd; break;
-      case 2: dir = nd; break;
-      case 3:
-        if (inside && pocket == 0 && ((kPickable >> tt) & 1)) {
-          pocket = tcode; vw.wr(tflat, kFloorCode); ev = 1;
-        }
-        break;
-      case 4:
-        if (inside && pocket != 0 && tt == kFloor) {
-          vw.wr(tflat, (uint8_t)pocket); pocket = 0; ev = 2;
-        }
-        break;
-      default:
-        if (inside) {
-          const int col = tcode & 15;
-          if (tt == kClosed || (tt == kLocked && pocket == kKey * 16 + col)) {
-            vw.wr(tflat, (uint8_t)(kOpen * 16 + col)); ev = 3;
-          }
-        }
-    }
+    // select-based: lanes with different actions stay converged
+    const bool mv = act == 0 && inside && ((kWalkable >> tt) & 1);
+    const bool pk = act == 3 && inside && pocket == 0 && ((kPickable >> tt) & 1);
+    const bool pt = act == 4 && inside && pocket != 0 && tt == kFloor;
+    const bool tg = act == 5 && inside && (tt == kClosed || (tt == kLocked && pocket == kKey * 16 + (tcode & 15)));
+    const int ev = mv ? 0 : pk ? 1 : pt ? 2 : tg ? 3 : -1;
+    const int wval = pk ? kFloorCode : pt ? pocket : kOpen * 16 + (tcode & 15);
+    r = mv ? tr : r;
+    c = mv ? tc : c;
+    dir = nd;  // nd == dir unless turning
+    pocket = pk ? tcode : pt ? 0 : pocket;
+    if (pk || pt || tg) vw.wr(tflat, (uint8_t)wval);
     // ---- MOVE / PICK_UP: agent-relative rules (only the slots their event
     // gates, in stored order) and goal; TOGGLE gates no rule and no goal.
     bool goal = false;
@@ -2041,13 +2033,13 @@ bool pdl_enabled() {
   return on == 1;
 }
 
-template <int MAXCH>
+template <int MAXCH, bool FULL>
 int launch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
                 const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st) {
   const MainGeo geo = make_main_geo(d->view_size, MAXCH, d->rule_width);
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] { attr_err = allow_smem(step_main<MAXCH>, kMaxDynSmem - 1024); });
+  std::call_once(once, [] { attr_err = allow_smem(step_main<MAXCH, FULL>, kMaxDynSmem - 1024); });
   if (attr_err != cudaSuccess) return fail(std::string("step_main attributes: ") + cudaGetErrorString(attr_err));
   const int64_t blocks = (n + kThreads - 1) / kThreads;
   // programmatic dependent of the previous kernel on the stream (the previous
@@ -2062,7 +2054,7 @@ int launch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, con
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t err = cudaLaunchKernelEx(&cfg, step_main<MAXCH>, *d, *s, *o, actions, dtype, flag, epoch, n);
+  const cudaError_t err = cudaLaunchKernelEx(&cfg, step_main<MAXCH, FULL>, *d, *s, *o, actions, dtype, flag, epoch, n);
   if (err != cudaSuccess) return fail(std::string("step_main: ") + cudaGetErrorString(err));
   return check_launch("step_main");
 }
@@ -2164,6 +2156,18 @@ int launch_stream(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, c
   return check_launch("step_stream");
 }
 
+// whole-grid staging: 16-byte chunks of a grid at any alignment
+inline int full_chunks(int hw) { return (hw + 30) / 16; }
+
+bool use_full(const xmg_env_desc* d) {
+  static int mode = -1;  // XMG_STAGE=full (<= 12 chunks) | window (default: measured faster at C3)
+  if (mode < 0) {
+    const char* m = getenv("XMG_STAGE");
+    mode = (m && !strcmp(m, "full")) ? 1 : 0;
+  }
+  return mode == 1 && full_chunks(d->height * d->width) <= 12;
+}
+
 bool use_stream(const xmg_env_desc* d) {
   static int mode = -1;  // XMG_MAIN=stream|window (default: window)
   if (mode < 0) {
@@ -2180,12 +2184,18 @@ int dispatch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, c
     if (d->height * d->width <= 128) return launch_stream<4>(d, s, o, actions, dtype, flag, epoch, n, st);
     return launch_stream<8>(d, s, o, actions, dtype, flag, epoch, n, st);
   }
+  if (use_full(d)) {
+    const int fc = full_chunks(d->height * d->width);
+    if (fc <= 6) return launch_main<6, true>(d, s, o, actions, dtype, flag, epoch, n, st);
+    if (fc <= 8) return launch_main<8, true>(d, s, o, actions, dtype, flag, epoch, n, st);
+    return launch_main<12, true>(d, s, o, actions, dtype, flag, epoch, n, st);
+  }
   switch (pick_maxch(d)) {
-    case 6: return launch_main<6>(d, s, o, actions, dtype, flag, epoch, n, st);
-    case 8: return launch_main<8>(d, s, o, actions, dtype, flag, epoch, n, st);
-    case 12: return launch_main<12>(d, s, o, actions, dtype, flag, epoch, n, st);
-    case 16: return launch_main<16>(d, s, o, actions, dtype, flag, epoch, n, st);
-    default: return launch_main<32>(d, s, o, actions, dtype, flag, epoch, n, st);
+    case 6: return launch_main<6, false>(d, s, o, actions, dtype, flag, epoch, n, st);
+    case 8: return launch_main<8, false>(d, s, o, actions, dtype, flag, epoch, n, st);
+    case 12: return launch_main<12, false>(d, s, o, actions, dtype, flag, epoch, n, st);
+    case 16: return launch_main<16, false>(d, s, o, actions, dtype, flag, epoch, n, st);
+    default: return launch_main<32, false>(d, s, o, actions, dtype, flag, epoch, n, st);
   }
 }
 
