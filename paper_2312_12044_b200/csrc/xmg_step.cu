@@ -117,6 +117,26 @@ constexpr int kThreads = 128;  // envs per CTA
 constexpr int kRowHeader = 4;  // task row: goal, counts, MOVE slot mask, PICK_UP slot mask
 constexpr int kMaxDynSmem = 227 * 1024 - 1024;  // leave room for the static shared desc copy
 constexpr int kWarps = kThreads / 32;
+#ifdef XMG_TRACE
+// debug builds: per-warp phase timestamps of step_rare (globaltimer, ns);
+// columns 0..7 step_rare phases, 8..23 the first warp_build of the warp
+__device__ unsigned long long g_trace[1 << 16][24];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define XMG_TR(gw, k, v) \
+  if ((threadIdx.x & 31) == 0 && (gw) < (1 << 16)) g_trace[gw][k] = (v)
+#define XMG_TRB(k)                                                                                  \
+  {                                                                                                 \
+    const int gw_ = blockIdx.x * kWarps + (threadIdx.x >> 5);                                       \
+    if ((threadIdx.x & 31) == 0 && gw_ < (1 << 16) && g_trace[gw_][8 + (k)] == 0) g_trace[gw_][8 + (k)] = gtime(); \
+  }
+#else
+#define XMG_TR(gw, k, v)
+#define XMG_TRB(k)
+#endif
 #ifndef XMG_MINB
 #define XMG_MINB 6  // min resident CTAs per SM the register allocation targets
 #endif
@@ -476,59 +496,156 @@ __device__ __forceinline__ bool col_ok(int mode, int cell, int W, int x) {
   return mode == 1 ? c < x : c > x;
 }
 
-// Rank of every (filtered) free cell in the stable argsort of its draw word
-// (ref:core.py:328-333, ref:vecenv.py:261-265: ties broken by index).  The
-// words are uniform, so a counting sort on their top `lg` bits puts < 1
-// other cell in a bucket on average; the rank is the bucket's offset plus an
-// exact (word, index) comparison inside the bucket.  Places `nobj` objects at
-// ranks 0..nobj-1 and records in misc[32] the cell of rank
-// spawn_base + spawn_word % (count - spawn_base) (ref:scenarios.py:281-288).
+// Warp radix-select over the draw words (ref:core.py:328-333,
+// ref:vecenv.py:261-265: cells ordered by (word, index), a stable argsort).
+// Element f (free-cell index) is owned by lane (f >> 2) & 31, bit
+// 4 * (f >> 7) + (f & 3) of that lane's masks (the lane that drew its
+// Philox block in draw_all).  Returns the element of rank t among the
+// elements of `cand` (cnt of them, warp-uniform), on every lane.  Uniform
+// 64-bit words leave one candidate after ~log2(cnt) bits; equal words fall
+// back to index order.
+__device__ int warp_select(const uint64_t* wd, int lane, int F, uint32_t cand, int cnt, int t) {
+  const int K = (F + 127) >> 7;
+  for (int b = 63; b >= 0 && cnt > 1; --b) {
+    uint32_t z = 0;
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int bit = 4 * k + i;
+        const int f = 128 * k + 4 * lane + i;
+        if (((cand >> bit) & 1) && !((wd[f] >> b) & 1)) z |= 1u << bit;
+      }
+    }
+    const int zeros = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(z));
+    if (t < zeros) {
+      cand = z;
+      cnt = zeros;
+    } else {
+      cand &= ~z;
+      t -= zeros;
+      cnt -= zeros;
+    }
+  }
+  // the survivors share one word: the t-th of them in index order
+  for (int k = 0;; ++k) {
+    const uint32_t nib = (cand >> (4 * k)) & 0xFu;
+    const int c = __popc(nib);
+    int inc = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, off);
+      if (lane >= off) inc += v;
+    }
+    const int tot = __shfl_sync(0xffffffffu, inc, 31), pre = inc - c;
+    if (t < tot) {
+      int f = -1;
+      if (t >= pre && t < inc) {
+        uint32_t m = nib;
+        for (int r = t - pre; r > 0; --r) m &= m - 1;
+        f = 128 * k + 4 * lane + (__ffs(m) - 1);
+      }
+      const uint32_t who = __ballot_sync(0xffffffffu, f >= 0);
+      return __shfl_sync(0xffffffffu, f, __ffs(who) - 1);
+    }
+    t -= tot;
+  }
+}
+
+// warp_select with the lane's top-32-bit keys in registers (KR blocks of 4,
+// F <= 128 * KR) and branch-free digit masks; two words sharing their top
+// half (rare) fall back to the exact 64-bit select.
+template <int KR>
+__device__ __forceinline__ int warp_select_fast(const uint64_t* wd, int lane, int F, uint32_t cand, int cnt, int t) {
+  uint32_t hi[4 * KR];
+#pragma unroll
+  for (int j = 0; j < 4 * KR; ++j) {
+    const int f = 128 * (j >> 2) + 4 * lane + (j & 3);
+    hi[j] = f < F ? (uint32_t)(wd[f] >> 32) : 0u;
+  }
+  uint32_t c = cand;
+  int tt = t, cc = cnt;
+  for (int b = 31; b >= 0 && cc > 1; --b) {
+    uint32_t z = 0;
+#pragma unroll
+    for (int j = 0; j < 4 * KR; ++j) z |= ((~hi[j] >> b) & 1u) << j;
+    z &= c;
+    const int zeros = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(z));
+    if (tt < zeros) {
+      c = z;
+      cc = zeros;
+    } else {
+      c &= ~z;
+      tt -= zeros;
+      cc -= zeros;
+    }
+  }
+  if (cc > 1) return warp_select(wd, lane, F, cand, cnt, t);
+  const uint32_t who = __ballot_sync(0xffffffffu, c != 0);
+  const int src = __ffs(who) - 1;
+  const int bit = __ffs(c) - 1;
+  const int f = 128 * (bit >> 2) + 4 * lane + (bit & 3);
+  return __shfl_sync(0xffffffffu, f, src);
+}
+
+__device__ __forceinline__ int select_rank(const uint64_t* wd, int lane, int F, uint32_t cand, int cnt, int t) {
+  if (F <= 128) return warp_select_fast<1>(wd, lane, F, cand, cnt, t);
+  if (F <= 256) return warp_select_fast<2>(wd, lane, F, cand, cnt, t);
+  if (F <= 512) return warp_select_fast<4>(wd, lane, F, cand, cnt, t);
+  return warp_select(wd, lane, F, cand, cnt, t);
+}
+
+// Places `nobj` objects on the (filtered) free cells of ranks 0..nobj-1 and
+// records in misc[32] the cell of rank spawn_base + spawn_word % (count -
+// spawn_base) (ref:scenarios.py:281-288), via warp_select: the element of
+// rank nobj - 1 bounds the object cells, which are then ordered exactly
+// among themselves.
 __device__ void rank_place(const WarpScratch& ws, int lane, int F, int W, int mode, int x, const uint8_t* objs,
                            int nobj, int spawn_base, uint64_t spawn_word) {
-  const int lg = ws.lg, nb = 1 << lg, sh = 64 - lg;
-  for (int i = lane; i < nb; i += 32) ws.bk[i] = 0;
-  __syncwarp();
-  for (int f = lane; f < F; f += 32)
-    if (col_ok(mode, ws.fc[f], W, x)) atomicAdd(&ws.bk[ws.wd[f] >> sh], 1u);
-  __syncwarp();
-  // exclusive scan of the bucket counts: lane owns nb/32 consecutive buckets
-  const int per = nb >> 5;
-  uint32_t loc = 0;
-  for (int k = 0; k < per; ++k) loc += ws.bk[lane * per + k];
-  uint32_t inc = loc;
+  const int K = (F + 127) >> 7;
+  uint32_t valid = 0;
+  for (int k = 0; k < K; ++k)
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, off);
-    if (lane >= off) inc += t;
-  }
-  const int total = __shfl_sync(0xffffffffu, (int)inc, 31);
-  uint32_t run = inc - loc;
-  for (int k = 0; k < per; ++k) {
-    const uint32_t v = ws.bk[lane * per + k];
-    ws.bk[lane * per + k] = run;
-    run += v;
-  }
-  __syncwarp();
-  // scatter: afterwards bk[b] is the end of bucket b
-  for (int f = lane; f < F; f += 32)
-    if (col_ok(mode, ws.fc[f], W, x)) ws.slot[atomicAdd(&ws.bk[ws.wd[f] >> sh], 1u)] = (uint16_t)f;
-  __syncwarp();
-  const int tail = total - spawn_base;
-  const int spawn_rank = tail > 0 ? spawn_base + (int)(spawn_word % (uint64_t)tail) : -1;
-  for (int f = lane; f < F; f += 32) {
-    const int cell = ws.fc[f];
-    if (!col_ok(mode, cell, W, x)) continue;
-    const uint64_t wf = ws.wd[f];
-    const int b = (int)(wf >> sh);
-    const int lo = b ? (int)ws.bk[b - 1] : 0, hi = (int)ws.bk[b];
-    int rank = lo;
-    for (int p = lo; p < hi; ++p) {
-      const int g = ws.slot[p];
-      const uint64_t wg = ws.wd[g];
-      rank += (wg < wf) | ((wg == wf) & (g < f));
+    for (int i = 0; i < 4; ++i) {
+      const int f = 128 * k + 4 * lane + i;
+      if (f < F && col_ok(mode, ws.fc[f], W, x)) valid |= 1u << (4 * k + i);
     }
-    if (rank < nobj) ws.grid[cell] = objs[rank];
-    if (rank == spawn_rank) reinterpret_cast<int*>(ws.misc + 32)[0] = cell;
+  const int total = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(valid));
+  const int no = nobj < total ? nobj : total;
+  uint32_t* list = reinterpret_cast<uint32_t*>(ws.slot);  // the object cells' element indices
+  if (no > 0) {
+    const int fb = select_rank(ws.wd, lane, F, valid, total, no - 1);
+    const uint64_t wb = ws.wd[fb];
+    int cnt = 0;
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int f = 128 * k + 4 * lane + i;
+        bool in = false;
+        if ((valid >> (4 * k + i)) & 1) {
+          const uint64_t w = ws.wd[f];
+          in = w < wb || (w == wb && f <= fb);
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, in);
+        if (in) list[cnt + __popc(m & ((1u << lane) - 1u))] = (uint32_t)f;
+        cnt += __popc(m);
+      }
+    __syncwarp();
+    for (int l = lane; l < no; l += 32) {  // exact rank among the no smallest
+      const int f = (int)list[l];
+      const uint64_t w = ws.wd[f];
+      int rank = 0;
+      for (int m = 0; m < no; ++m) {
+        const int g = (int)list[m];
+        const uint64_t wg = ws.wd[g];
+        rank += (wg < w) | ((wg == w) & (g < f));
+      }
+      ws.grid[ws.fc[f]] = objs[rank];
+    }
+  }
+  const int tail = total - spawn_base;
+  if (tail > 0) {
+    const int fs = select_rank(ws.wd, lane, F, valid, total, spawn_base + (int)(spawn_word % (uint64_t)tail));
+    if (lane == 0) reinterpret_cast<int*>(ws.misc + 32)[0] = ws.fc[fs];
   }
   __syncwarp();
 }
@@ -1633,19 +1750,6 @@ __device__ __noinline__ int warp_put_env(uint8_t* G, uint8_t* genv, uint32_t* ca
   return (int)hit | ((int)dirty << 1);
 }
 
-#ifdef XMG_TRACE
-// debug builds: per-warp phase timestamps of step_rare (globaltimer, ns)
-__device__ unsigned long long g_trace[1 << 16][8];
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define XMG_TR(gw, k, v) \
-  if ((threadIdx.x & 31) == 0 && (gw) < (1 << 16)) g_trace[gw][k] = (v)
-#else
-#define XMG_TR(gw, k, v)
-#endif
 
 // Every lane's writes for the envs the warp just finished are made visible,
 // then each `mine` lane releases its env's chunk for the next step_main.
@@ -2312,7 +2416,7 @@ int64_t xmg_work_words(int64_t n) { return work_words(n); }
 
 #ifdef XMG_TRACE
 int32_t xmg_debug_trace(unsigned long long* host_out, int64_t rows) {
-  return cudaMemcpyFromSymbol(host_out, g_trace, (size_t)rows * 8 * sizeof(unsigned long long)) == cudaSuccess ? 0
+  return cudaMemcpyFromSymbol(host_out, g_trace, (size_t)rows * 24 * sizeof(unsigned long long)) == cudaSuccess ? 0
                                                                                                               : -1;
 }
 int32_t xmg_debug_trace_clear(void) {

@@ -66,7 +66,7 @@ def burst(name="c3", around=506, k=4):
           + " ".join(f"{x:.0f}" for x in times), flush=True)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__":  # noqa
     for nm in (sys.argv[1:] or RUNS):
         if nm.startswith("burst:"):
             burst(nm.split(":")[1])

@@ -28,7 +28,7 @@ torch.cuda.synchronize()
 vec.step(acts[pre], validate=False)
 torch.cuda.synchronize()
 rows = 1 << 16
-buf = np.zeros((rows, 8), np.uint64)
+buf = np.zeros((rows, 24), np.uint64)
 L.xmg_debug_trace.argtypes = [C.c_void_p, C.c_int64]
 L.xmg_debug_trace(buf.ctypes.data, rows)
 act = buf[:, 0] > 0
@@ -61,3 +61,19 @@ if rs.any():
     kd = (buf[rs, 7].astype(np.int64) - buf[rs, 1].astype(np.int64)) / 1e3
     bd = (buf[rs, 2].astype(np.int64) - buf[rs, 7].astype(np.int64)) / 1e3
     print(f"reset keys    : median {np.median(kd):.2f} max {kd.max():.2f}; build+obs: median {np.median(bd):.2f} max {bd.max():.2f} us")
+wb = work & (buf[:, 8] > 0) & (buf[:, 14] > 0)
+if wb.any():
+    names = ["keys/setup", "free list", "draws", "rank/place", "copy out", "obs"]
+    prev = buf[wb, 8].astype(np.int64)
+    for k in range(1, 7):
+        cur = buf[wb, 8 + k].astype(np.int64)
+        dt = (cur - prev) / 1e3
+        print(f"build {names[k - 1]:11s}: median {np.median(dt):.2f} max {dt.max():.2f} us")
+        prev = cur
+wr = work & (buf[:, 11] > 0) & (buf[:, 16] > 0) & (buf[:, 21] > 0)
+if wr.any():
+    names = ["doors", "a-words..", "zero+hist", "scan", "scatter", "ranks"]
+    cols = [11, 16, 17, 18, 19, 20, 21]
+    for k in range(1, len(cols)):
+        dt = (buf[wr, cols[k]].astype(np.int64) - buf[wr, cols[k - 1]].astype(np.int64)) / 1e3
+        print(f"rank {names[k - 1]:10s}: median {np.median(dt):.2f} max {dt.max():.2f} us")
