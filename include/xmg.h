@@ -163,6 +163,13 @@ int32_t xmg_validate_actions(const void* actions, int32_t action_dtype, int64_t 
 int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* actions, int32_t action_dtype,
                  int64_t n, const xmg_out* out, const uint32_t* abort_flag, uint32_t epoch, void* stream);
 
+/* Profiling hook: while enabled, every xmg_step records CUDA events around
+ * its two kernels (this serialises them: standalone per-kernel times, for
+ * rooflines only).  xmg_profile_read synchronises, returns the summed
+ * milliseconds of each kernel and the step count, and clears the record. */
+int32_t xmg_profile(int32_t enable);
+int32_t xmg_profile_read(double* main_ms, double* rare_ms, int64_t* steps);
+
 /* Size in u32 words of xmg_state.work for n envs. */
 int64_t xmg_work_words(int64_t n);
 

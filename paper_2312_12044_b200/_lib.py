@@ -30,7 +30,7 @@ ACT_U8, ACT_I32, ACT_I64 = 0, 1, 2
 
 EXPORTS = ("xmg_abi_version", "xmg_last_error", "xmg_philox", "xmg_split_batch", "xmg_random_actions",
            "xmg_key_from_seed", "xmg_fold_in", "xmg_philox_host", "xmg_reset", "xmg_validate_actions",
-           "xmg_step", "xmg_step_smem_bytes", "xmg_work_words")
+           "xmg_step", "xmg_step_smem_bytes", "xmg_work_words", "xmg_profile", "xmg_profile_read")
 
 
 class NativeLibraryError(RuntimeError):
@@ -87,6 +87,8 @@ def _bind(L):
         "xmg_step": ([C.POINTER(EnvDesc), C.POINTER(State), vp, i32, i64, C.POINTER(Out), vp, C.c_uint32, vp], i32),
         "xmg_step_smem_bytes": ([C.POINTER(EnvDesc)], i64),
         "xmg_work_words": ([i64], i64),
+        "xmg_profile": ([i32], i32),
+        "xmg_profile_read": ([vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -35,6 +35,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <array>
+#include <vector>
 
 #include "../../include/xmg.h"
 
@@ -2108,6 +2110,26 @@ int check_launch(const char* what) {
   return 0;
 }
 
+// Profiling hook (xmg_profile): CUDA events around each step's two kernels.
+// Recording them serialises the kernels (no overlap), so the durations are
+// per-kernel standalone times, for rooflines; never used in timed runs.
+struct Prof {
+  std::mutex mu;
+  bool on = false;
+  std::vector<std::array<cudaEvent_t, 3>> events;
+};
+Prof g_prof;
+
+bool prof_events(cudaEvent_t* ev) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  std::array<cudaEvent_t, 3> e;
+  for (int k = 0; k < 3; ++k)
+    if (cudaEventCreate(&e[k]) != cudaSuccess) return false;
+  g_prof.events.push_back(e);
+  for (int k = 0; k < 3; ++k) ev[k] = e[k];
+  return true;
+}
+
 int pick_maxch(const xmg_env_desc* d) {
   const int need = needed_chunks(d->width, d->view_size);
   if (need <= 6) return 6;
@@ -2399,10 +2421,41 @@ int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* a
   if ((reinterpret_cast<uintptr_t>(state->grids) & 15) ||
       (reinterpret_cast<uintptr_t>(state->agent) & 15) || (out->obs && (reinterpret_cast<uintptr_t>(out->obs) & 15)))
     return fail("actions / grids / agent / obs buffers must be 16-byte aligned");
+  cudaEvent_t ev[3];
+  const bool prof = g_prof.on && prof_events(ev);
+  if (prof) cudaEventRecord(ev[0], (cudaStream_t)stream);
   if (dispatch_main(desc, state, out, actions, action_dtype, abort_flag, epoch, n, (cudaStream_t)stream)) return -1;
+  if (prof) cudaEventRecord(ev[1], (cudaStream_t)stream);
   // step_main (window mode) records the tiles step_rare must release
   const int track = use_stream(desc) ? 0 : 1;
-  return launch_rare(desc, state, out, nullptr, abort_flag, epoch, n, track, (cudaStream_t)stream);
+  const int rc = launch_rare(desc, state, out, nullptr, abort_flag, epoch, n, track, (cudaStream_t)stream);
+  if (prof) cudaEventRecord(ev[2], (cudaStream_t)stream);
+  return rc;
+}
+
+int32_t xmg_profile(int32_t enable) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  g_prof.on = enable != 0;
+  return 0;
+}
+
+int32_t xmg_profile_read(double* main_ms, double* rare_ms, int64_t* steps) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  double a = 0, b = 0;
+  for (auto& e : g_prof.events) {
+    if (cudaEventSynchronize(e[2]) != cudaSuccess) return fail("xmg_profile_read: event sync failed");
+    float x = 0, y = 0;
+    cudaEventElapsedTime(&x, e[0], e[1]);
+    cudaEventElapsedTime(&y, e[1], e[2]);
+    a += x;
+    b += y;
+    for (int k = 0; k < 3; ++k) cudaEventDestroy(e[k]);
+  }
+  if (main_ms) *main_ms = a;
+  if (rare_ms) *rare_ms = b;
+  if (steps) *steps = (int64_t)g_prof.events.size();
+  g_prof.events.clear();
+  return 0;
 }
 
 int64_t xmg_step_smem_bytes(const xmg_env_desc* desc) {
