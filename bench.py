@@ -358,9 +358,64 @@ def run_ours(args):
                "api": "VecEnv.step with pinned host actions in, full VecTimeStep out (double-buffered)"}
         del vec3
 
+    # ---- fused rollout: the same K steps (same actions,
+    # same phase) as xmg_rollout launches of `chunk` steps each, state on chip
+    # within a launch; per env-step only the trajectory record leaves the SM.
+    fused = None
+    if not args.no_fused:
+        params4, _, vec4 = make_workload(args.workload, dev, n, offset)
+        vec4.reset(key_from_seed(0))
+        vec4.enable_stats()
+        chunk = args.fused_chunk
+        if W + pre:
+            vec4.rollout(W + pre, policy_keys=pkeys, t0=0, record=())
+        v = params4.view_size
+        traj = None
+        modes = {}
+        for mode, rec in (("records", ("observations", "rewards", "discounts", "step_types")), ("stats_only", ())):
+            vec4.reset(key_from_seed(0))
+            if W + pre:
+                vec4.rollout(W + pre, policy_keys=pkeys, t0=0, record=())
+            traj = vec4.rollout(chunk, policy_keys=pkeys, t0=W + pre, record=rec) if rec else None  # warm / allocate
+            vec4.reset(key_from_seed(0))
+            if W + pre:
+                vec4.rollout(W + pre, policy_keys=pkeys, t0=0, record=())
+            torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            l0 = vec4.launches
+            f0.record(stream)
+            t = W + pre
+            while t < total:
+                k = min(chunk, total - t)
+                if rec:
+                    vec4.rollout(k, policy_keys=pkeys, t0=t, record=rec, out=traj if k == chunk else None)
+                else:
+                    vec4.rollout(k, policy_keys=pkeys, t0=t, record=())
+                t += k
+            f1.record(stream)
+            torch.cuda.synchronize(dev)
+            fms = f0.elapsed_time(f1)
+            tf = torch.tensor([fms], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(tf, op=dist.ReduceOp.MAX)
+            fms = float(tf.item())
+            bpe_f = (2 * v * v + 9) if rec else 0
+            ach = bpe_f * n * K / (fms / 1e3) / 1e9
+            modes[mode] = {"value": n * world * K / (fms / 1e3), "ms_per_step": fms / K, "launches": vec4.launches - l0,
+                           "record_bytes_per_env_step": bpe_f,
+                           "achieved_gbs": ach, "frac_of_hbm_peak": ach / peak if bpe_f else None}
+        del traj, vec4
+        fused = {"unit": "env-steps/s", "chunk_steps": chunk, **modes,
+                 "note": "xmg_rollout (one kernel per chunk of steps, state resident in shared memory / registers, "
+                         "random policy evaluated in-kernel), bit-identical to K VecEnv.step calls "
+                         "(tests/test_rollout_gpu.py); same K steps and phase as the timed window; records = "
+                         "obs + reward + discount + step type per env-step written to HBM"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        r = cpu_reference(args.workload, min(n, 1 << 14), 1024, os.cpu_count() or 1, budget_s=15.0)
+        r = cpu_reference(args.workload, min(n, 1 << 14), 1 << 20, os.cpu_count() or 1, budget_s=12.0)
         cpu = {"value": r["value"], "unit": "env-steps/s", "cores": os.cpu_count() or 1, "kind": "port",
                "sample": f"{r['envs']} envs x {r['steps']} steps of the same workload on the host "
                          f"({r['seconds']:.1f} s, OpenMP over all host threads)"}
@@ -376,6 +431,7 @@ def run_ours(args):
                        "l2": "inputs larger than L2" if n * params.height * params.width > 126e6
                              else "state resident in L2 (small workload)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "fused_rollout": fused,
             "clocks": clocks.summary(),
             "episode_stats": {"return_sum": float(tot[0]), "trials": float(tot[1]), "length_sum": float(tot[2])},
         }
@@ -395,6 +451,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=256)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fused", action="store_true")
+    ap.add_argument("--fused-chunk", type=int, default=32)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -170,6 +170,27 @@ int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* a
 int32_t xmg_profile(int32_t enable);
 int32_t xmg_profile_read(double* main_ms, double* rare_ms, int64_t* steps);
 
+/* Fused rollout: `steps` consecutive xmg_step calls in
+ * one kernel, bit-identical to them, with each env's state on chip for the
+ * whole rollout (ref harness.py:103-143 `rollout`, batched: the random-policy
+ * loop of ref harness.py:149-158 around VecEnv.step, vecenv.py:295-364).
+ * Actions: exactly one of
+ *   policy_keys [n][2]   the random policy, action of step t = word (t0 + t)
+ *                        of key i's draw stream mod 6 (ref harness.py:58-64,
+ *                        == xmg_random_actions), or
+ *   actions [steps][n]   u8 in [0, 6) (NOT validated here: the caller checks).
+ * traj: every pointer nullable; obs [steps][n][v][v][2], reward / discount /
+ * step_type [steps][n] (record t = what xmg_step t would return), stats as
+ * in xmg_out, one slot per 128 envs.  state.work is not used: a rollout may sit
+ * between xmg_step calls on the same state (same stream) without consuming
+ * an epoch. */
+int32_t xmg_rollout(const xmg_env_desc* desc, const xmg_state* state, const uint64_t* policy_keys,
+                    const uint8_t* actions, int64_t t0, int64_t steps, int64_t n, const xmg_out* traj,
+                    void* stream);
+
+/* Dynamic shared memory per 128-env CTA of the rollout kernel (<0: unsupported). */
+int64_t xmg_rollout_smem_bytes(const xmg_env_desc* desc);
+
 /* Size in u32 words of xmg_state.work for n envs. */
 int64_t xmg_work_words(int64_t n);
 

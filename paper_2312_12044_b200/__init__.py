@@ -15,7 +15,7 @@ from .env import Action, Environment, EnvParams, StepType, make, registered_envi
 from .layouts import Layout, plan_layout
 from .ruleset import (EMPTY_RULESET, MAX_INIT_OBJECTS, MAX_RULES, Benchmark, Ruleset, TaskTable, load_benchmark,
                       load_named, registered_benchmarks, save_benchmark)
-from .vecenv import EnvState, VecEnv, VecTimeStep, philox, policy_keys, random_actions, split_batch
+from .vecenv import EnvState, Trajectory, VecEnv, VecTimeStep, philox, policy_keys, random_actions, split_batch
 
 __version__ = "0.1.0"
 
@@ -23,7 +23,7 @@ __all__ = [
     "Action", "AgentState", "Benchmark", "Color", "Direction", "EMPTY_RULESET", "Entity", "EnvParams", "EnvState",
     "Environment", "FormatError", "Grid", "GridFull", "InvalidAction", "InvalidCode", "InvalidEncoding",
     "InvalidProportion", "Key", "Layout", "LayoutTooSmall", "MAX_INIT_OBJECTS", "MAX_RULES", "NativeLibraryError",
-    "Position", "Ruleset", "StepType", "TaskTable", "Tile", "UnknownBenchmark", "UnknownEnvironment", "VecEnv",
+    "Position", "Ruleset", "StepType", "TaskTable", "Tile", "Trajectory", "UnknownBenchmark", "UnknownEnvironment", "VecEnv",
     "VecTimeStep", "build", "fold_in", "key_from_seed", "load_benchmark", "load_named", "make", "pack_entity",
     "philox", "plan_layout", "policy_keys", "random_actions", "random_words", "randint", "registered_benchmarks",
     "registered_environments", "save_benchmark", "split", "split_batch", "unpack_entity",

@@ -1,0 +1,279 @@
+// xmg_rollout.cuh — the fused multi-step rollout (included by xmg_step.cu,
+// inside its anonymous namespace).
+//
+// T consecutive VecEnv.step calls (ref:vecenv.py:295-364) in ONE kernel, each
+// env's state resident on chip for the whole rollout: a warp owns 32
+// consecutive envs, their grids live in the warp's shared memory and their
+// pose / pocket / step count / goal / task / rng key in the lanes' registers.
+// Per step a lane applies its env's action, the agent-relative rules and goal
+// of MOVE / PICK_UP (the same select-based code as step_main), and the warp
+// resolves PUT_DOWN events (warp_put_env, speculative rule slots) and trial
+// resets (warp_build, radix-select) in place, so nothing is queued and no
+// state word crosses HBM between steps.  What leaves the SM per env-step is
+// the trajectory record the caller asked for: the observation (one TMA bulk
+// store of the warp's 32 records, double-buffered), reward, discount and step
+// type; with all of them NULL only the episode statistics are produced.
+//
+// Actions: the random policy of ref harness.py:58-64 evaluated in the kernel
+// (word t0 + t of the env's policy key mod 6, one Philox block per 4 steps),
+// or a caller-supplied [T][n] u8 tensor.  The result is bit-identical to T
+// calls of xmg_step with the same actions (tests/test_rollout_gpu.py).
+
+constexpr int kRollWarps = 4;
+constexpr int kRollLg = 2;  // unused bucket area of WarpScratch (4 << kRollLg bytes)
+
+struct RollGeo {
+  int hw, grids, rbw, rules, ob, obs, hwp, scratch, cand, keys, desc, warp_bytes;
+  int64_t total;
+};
+
+__host__ __device__ inline RollGeo make_roll_geo(int H, int W, int V, int R) {
+  RollGeo g;
+  g.hw = H * W;
+  g.grids = round16(32 * g.hw + 16);            // the 32 env grids (+ slack for 16-byte reads)
+  g.rbw = 16 * ((kRowHeader + R + 3) / 4);      // one lane's task row header + rules
+  g.rules = R > 0 ? 32 * g.rbw : 0;
+  g.ob = 2 * V * V;
+  g.obs = 2 * round16(32 * g.ob);               // double-buffered observation records
+  g.hwp = round16(g.hw + 16);
+  // WarpScratch of warp_build: wd u64[hwp] | fc u16[hwp] | slot u16[hwp] | bk | grid u8[hwp] | misc 64 u64
+  g.scratch = 12 * g.hwp + (4 << kRollLg) + g.hwp + 512;
+  g.cand = 4 * g.hwp;                           // PUT_DOWN candidate list
+  g.keys = 32 * (int)sizeof(TrialKeys);
+  g.desc = round16((int)sizeof(xmg_env_desc));
+  g.warp_bytes = g.grids + g.rules + g.obs + g.scratch + g.cand + g.keys + g.desc;
+  g.total = (int64_t)kRollWarps * g.warp_bytes;
+  return g;
+}
+
+// action of step t: four words of one Philox block, mod 6, packed in a u32
+__device__ __forceinline__ uint32_t policy_block(uint64_t kh, uint64_t kl, uint64_t blk) {
+  const Words4 w = philox<10>(blk, 0, kDomDraw, 0, kh, kl);
+  return (uint32_t)(w.w0 % 6) | ((uint32_t)(w.w1 % 6) << 8) | ((uint32_t)(w.w2 % 6) << 16) |
+         ((uint32_t)(w.w3 % 6) << 24);
+}
+
+__global__ void __launch_bounds__(kRollWarps * 32) rollout_kernel(const xmg_env_desc d, const xmg_state s,
+                                                                 const uint64_t* pkeys, const uint8_t* actions,
+                                                                 int64_t t0, int64_t T, int64_t n, const xmg_out o) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t chunk = (int64_t)blockIdx.x * kRollWarps + warp;
+  const int64_t e0 = 32 * chunk;
+  if (e0 >= n) return;  // warp-uniform
+  const int H = d.height, W = d.width, HW = H * W, V = d.view_size, R = d.rule_width;
+  const RollGeo geo = make_roll_geo(H, W, V, R);
+  uint8_t* wb = smem + warp * geo.warp_bytes;
+  uint8_t* grids = wb;
+  uint32_t* rules_s = reinterpret_cast<uint32_t*>(wb + geo.grids);
+  uint8_t* obs_s = wb + geo.grids + geo.rules;
+  uint8_t* scratch = obs_s + geo.obs;
+  uint32_t* cand = reinterpret_cast<uint32_t*>(scratch + geo.scratch);
+  TrialKeys* keys = reinterpret_cast<TrialKeys*>(scratch + geo.scratch + geo.cand);
+  xmg_env_desc* sdesc = reinterpret_cast<xmg_env_desc*>(scratch + geo.scratch + geo.cand + geo.keys);
+  ResetOut* rout = reinterpret_cast<ResetOut*>(make_scratch(scratch, geo.hwp, kRollLg).misc + 40);
+
+  const int nvalid = (int)min((int64_t)32, n - e0);
+  const int64_t e = e0 + lane;
+  const bool valid = lane < nvalid;
+  const bool xland = d.scenario == XMG_SCENARIO_XLAND;
+  const bool resample = d.resample_tasks && xland;
+  const bool see = d.see_through_walls != 0;
+  if (lane == 0) *sdesc = d;
+
+  // ---- state in: the 32 grids (contiguous in HBM), state words, rng keys
+  {
+    const uint8_t* src = s.grids + e0 * (int64_t)HW;
+    const int bytes = nvalid * HW;
+    if (((reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+      for (int i = lane; i < (bytes >> 4); i += 32)
+        reinterpret_cast<uint4*>(grids)[i] = reinterpret_cast<const uint4*>(src)[i];
+      for (int i = (bytes & ~15) + lane; i < bytes; i += 32) grids[i] = src[i];
+    } else {
+      for (int i = lane; i < bytes; i += 32) grids[i] = src[i];
+    }
+  }
+  ulonglong2 ag = make_ulonglong2(0, 0), rk = make_ulonglong2(0, 0), pk = make_ulonglong2(0, 0);
+  if (valid) {
+    ag = reinterpret_cast<const ulonglong2*>(s.agent)[e];
+    rk = reinterpret_cast<const ulonglong2*>(s.rng)[e];
+    if (pkeys) pk = reinterpret_cast<const ulonglong2*>(pkeys)[e];
+  }
+  int r = (int)(ag.x & 0xff), c = (int)((ag.x >> 8) & 0xff), dir = (int)((ag.x >> 16) & 3);
+  int pocket = (int)((ag.x >> 24) & 0xff);
+  uint32_t sc = (uint32_t)(ag.x >> 32);
+  uint32_t goal_word = (uint32_t)ag.y;
+  int task = (int)(ag.y >> 32);
+  uint32_t* rbuf = rules_s + lane * (geo.rbw / 4);
+  auto load_row = [&](int who, int tk) {  // whole warp: task row header + rules of lane `who`
+    if (R == 0) return;
+    const uint32_t* src = d.task_rows + (int64_t)tk * d.row_words;
+    uint32_t* dst = rules_s + who * (geo.rbw / 4);
+    for (int i = lane; i < kRowHeader + R; i += 32) dst[i] = src[i];
+  };
+  if (R > 0 && valid) {
+    const uint32_t* src = d.task_rows + (int64_t)task * d.row_words;
+    for (int i = 0; i < kRowHeader + R; ++i) rbuf[i] = src[i];
+  }
+  __syncwarp();
+
+  View vw;
+  vw.g = grids + lane * HW;
+  vw.stage = vw.g;
+  vw.sbase = vw.slo = 0;
+  vw.shi = HW;
+  double st_ret = 0.0, st_trials = 0.0, st_len = 0.0;
+  uint32_t acts4 = 0;
+
+  for (int64_t t = 0; t < T; ++t) {
+    // ---- action of this step
+    int act = 1;
+    const int64_t tt = t0 + t;
+    if (actions != nullptr) {
+      if (valid) act = actions[t * n + e];
+    } else {
+      if (t == 0 || (tt & 3) == 0) acts4 = valid ? policy_block(pk.x, pk.y, (uint64_t)(tt >> 2)) : 0x01010101u;
+      act = (int)((acts4 >> (8 * (tt & 3))) & 0xff);
+    }
+    int ev = -1;
+    bool goal = false;
+    if (valid) {
+      // ---- action, ref:vecenv.py:306-342 / ref:env.py:148-191 (select-based)
+      const int tr = r + dir_dr(dir), tc = c + dir_dc(dir);
+      const bool inside = tr >= 0 && tr < H && tc >= 0 && tc < W;
+      const int tflat = tr * W + tc;
+      const int tcode = inside ? vw.stage[tflat] : 0, ttile = tcode >> 4;
+      const bool mv = act == 0 && inside && ((kWalkable >> ttile) & 1);
+      const bool pkup = act == 3 && inside && pocket == 0 && ((kPickable >> ttile) & 1);
+      const bool pt = act == 4 && inside && pocket != 0 && ttile == kFloor;
+      const bool tg = act == 5 && inside && (ttile == kClosed || (ttile == kLocked && pocket == kKey * 16 + (tcode & 15)));
+      ev = mv ? 0 : pkup ? 1 : pt ? 2 : tg ? 3 : -1;
+      const int wval = pkup ? kFloorCode : pt ? pocket : kOpen * 16 + (tcode & 15);
+      r = mv ? tr : r;
+      c = mv ? tc : c;
+      dir = act == 1 ? ((dir + 3) & 3) : act == 2 ? ((dir + 1) & 3) : dir;
+      pocket = pkup ? tcode : pt ? 0 : pocket;
+      if (pkup || pt || tg) vw.stage[tflat] = (uint8_t)wval;
+      // ---- MOVE / PICK_UP: agent-relative rules (gated slots, stored order) and goal
+      if (ev == 0 || ev == 1) {
+        Nbrs nb = load_nbrs(vw, H, W, r, c);
+        const int nr = R > 0 ? (int)(rbuf[1] & 0xff) : 0;
+        if (nr) {
+          if (R <= 32) {
+            const uint32_t slots = rbuf[2 + ev];
+            if (slots) pocket = agent_rules(vw, nb, rbuf + kRowHeader, slots, pocket);
+          } else {
+            for (int s0 = 0; s0 < nr; ++s0) {
+              const int kind = rbuf[kRowHeader + s0] & 0xff;
+              if (kind >= 1 && kind <= 11 && ((cRuleGate[kind] >> ev) & 1))
+                pocket = agent_rules(vw, nb, rbuf + kRowHeader + s0, 1u, pocket);
+            }
+          }
+        }
+        goal = agent_goal(nb, vw.stage[r * W + c], goal_word, ev, r, c, pocket);
+      }
+    }
+    // ---- PUT_DOWN: grid-wide rules and goal, one env at a time by the warp
+    for (uint32_t pm = __ballot_sync(0xffffffffu, ev == 2); pm; pm &= pm - 1) {
+      const int src = __ffs(pm) - 1;
+      uint8_t* G = grids + src * HW;
+      const int ar = __shfl_sync(0xffffffffu, r, src), ac = __shfl_sync(0xffffffffu, c, src);
+      const uint32_t gw_src = __shfl_sync(0xffffffffu, goal_word, src);
+      const uint32_t* rt = rules_s + src * (geo.rbw / 4);
+      const int nr = R > 0 ? (int)(rt[1] & 0xff) : 0;
+      const int res = warp_put_env(G, G, cand, lane, H, W, ar, ac, rt + kRowHeader, nr, gw_src);
+      if (lane == src) goal = res & 1;
+    }
+    // ---- counters, reward, record, ref:vecenv.py:351-357
+    float rew = 0.f;
+    bool last = false;
+    if (valid) {
+      sc += 1;
+      last = goal || sc >= (uint32_t)d.budget;
+      if (goal) rew = goal_reward(sc, d.budget);
+      const int64_t oi = t * n + e;
+      if (o.reward) o.reward[oi] = rew;
+      if (o.discount) o.discount[oi] = last ? 0.f : 1.f;
+      if (o.step_type) o.step_type[oi] = last ? 2 : 1;
+      st_ret += (double)rew;
+      if (last) {
+        st_trials += 1.0;
+        st_len += (double)sc;
+      }
+    }
+    // ---- auto-reset of finished trials (ref:vecenv.py:359-361 -> :224-291)
+    uint32_t lm = __ballot_sync(0xffffffffu, last);
+    if (lm) {
+      if (last) derive_trial_keys(rk.x, rk.y, resample, keys + lane);
+      __syncwarp();
+      for (; lm; lm &= lm - 1) {
+        const int src = __ffs(lm) - 1;
+        const int tk = __shfl_sync(0xffffffffu, task, src);
+        const uint32_t g_in = xland ? d.task_rows[(int64_t)tk * d.row_words] : 0u;
+        warp_build(sdesc, scratch, geo.hwp, kRollLg, lane, keys + src, tk, g_in, grids + src * HW, rout);
+        const ResetOut ro = *rout;
+        if (lane == src) {
+          r = ro.r;
+          c = ro.c;
+          dir = ro.d;
+          pocket = 0;
+          sc = 0;
+          goal_word = ro.goal;
+          task = ro.task;
+          rk = make_ulonglong2(ro.st_hi, ro.st_lo);
+        }
+        if (resample) load_row(src, ro.task);
+        __syncwarp();
+      }
+    }
+    // ---- observation of the next playable state: staged, one bulk store per warp
+    if (o.obs != nullptr) {
+      uint8_t* ob = obs_s + (int)(t & 1) * (geo.obs / 2);
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // this buffer's last store
+      __syncwarp();
+      if (valid) {
+        uint8_t* dst = ob + lane * geo.ob;
+        if (see) {
+          if (V == 5) obs_see<5>(vw.stage, 0, dst, r, c, dir, H, W, V);
+          else obs_see<0>(vw.stage, 0, dst, r, c, dir, H, W, V);
+        } else {
+          obs_occluded(vw, dst, r, c, dir, H, W, V);
+        }
+      }
+      const uint32_t bytes = (uint32_t)(nvalid * geo.ob);
+      uint8_t* gdst = o.obs + (t * n + e0) * geo.ob;
+      const bool aligned = (reinterpret_cast<uintptr_t>(gdst) & 15) == 0;
+      const uint32_t bulk = aligned ? (bytes & ~15u) : 0u;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0 && bulk) {
+        const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(ob);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(saddr),
+                     "r"(bulk) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      for (uint32_t q = bulk + lane; q < bytes; q += 32) gdst[q] = ob[q];
+    }
+  }
+
+  // ---- state out
+  __syncwarp();
+  {
+    uint8_t* dst = s.grids + e0 * (int64_t)HW;
+    const int bytes = nvalid * HW;
+    if (((reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+      for (int i = lane; i < (bytes >> 4); i += 32)
+        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(grids)[i];
+      for (int i = (bytes & ~15) + lane; i < bytes; i += 32) dst[i] = grids[i];
+    } else {
+      for (int i = lane; i < bytes; i += 32) dst[i] = grids[i];
+    }
+  }
+  if (valid) {
+    reinterpret_cast<ulonglong2*>(s.agent)[e] =
+        make_ulonglong2(pack_agent(r, c, dir, pocket, sc), (uint64_t)goal_word | ((uint64_t)(uint32_t)task << 32));
+    reinterpret_cast<ulonglong2*>(s.rng)[e] = rk;
+  }
+  if (o.stats != nullptr) warp_stats(o.stats, (int)(chunk / kWarps), st_ret, st_trials, st_len);
+  if (lane == 0 && o.obs != nullptr) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}

@@ -2096,6 +2096,8 @@ __global__ void validate_kernel(const void* a, int dtype, int64_t n, uint32_t ep
   }
 }
 
+#include "xmg_rollout.cuh"
+
 // ------------------------------------------------------- host side
 thread_local std::string g_err;
 
@@ -2325,6 +2327,21 @@ int dispatch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, c
   }
 }
 
+int launch_rollout(const xmg_env_desc* d, const xmg_state* s, const uint64_t* pkeys, const uint8_t* actions,
+                   int64_t t0, int64_t steps, int64_t n, const xmg_out* o, cudaStream_t st) {
+  const RollGeo geo = make_roll_geo(d->height, d->width, d->view_size, d->rule_width);
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] { attr_err = allow_smem(rollout_kernel, kMaxDynSmem - 1024); });
+  if (attr_err != cudaSuccess) return fail(std::string("rollout_kernel attributes: ") + cudaGetErrorString(attr_err));
+  if (geo.total > kMaxDynSmem - 1024) return fail("grid too large for the rollout kernel's shared-memory state");
+  const int64_t chunks = (n + 31) / 32;
+  const int64_t blocks = (chunks + kRollWarps - 1) / kRollWarps;
+  rollout_kernel<<<(unsigned)blocks, kRollWarps * 32, (size_t)geo.total, st>>>(*d, *s, pkeys, actions, t0, steps, n,
+                                                                             *o);
+  return check_launch("rollout_kernel");
+}
+
 }  // namespace
 
 // ================================================================ C ABI
@@ -2466,6 +2483,25 @@ int64_t xmg_step_smem_bytes(const xmg_env_desc* desc) {
 }
 
 int64_t xmg_work_words(int64_t n) { return work_words(n); }
+
+int32_t xmg_rollout(const xmg_env_desc* desc, const xmg_state* state, const uint64_t* policy_keys,
+                    const uint8_t* actions, int64_t t0, int64_t steps, int64_t n, const xmg_out* traj,
+                    void* stream) {
+  if (validate_desc(desc, state, n)) return -1;
+  if (!traj) return fail("null trajectory record");
+  if ((policy_keys == nullptr) == (actions == nullptr)) return fail("exactly one of policy_keys / actions");
+  if (t0 < 0 || steps < 0) return fail("t0 and steps must be >= 0");
+  if (steps == 0) return 0;
+  if ((reinterpret_cast<uintptr_t>(state->agent) & 15) || (reinterpret_cast<uintptr_t>(state->rng) & 15) ||
+      (policy_keys && (reinterpret_cast<uintptr_t>(policy_keys) & 15)))
+    return fail("agent / rng / policy key buffers must be 16-byte aligned");
+  return launch_rollout(desc, state, policy_keys, actions, t0, steps, n, traj, (cudaStream_t)stream);
+}
+
+int64_t xmg_rollout_smem_bytes(const xmg_env_desc* desc) {
+  if (!desc) return -1;
+  return make_roll_geo(desc->height, desc->width, desc->view_size, desc->rule_width).total;
+}
 
 #ifdef XMG_TRACE
 int32_t xmg_debug_trace(unsigned long long* host_out, int64_t rows) {

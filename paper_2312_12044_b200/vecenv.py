@@ -128,6 +128,16 @@ class VecTimeStep:
                 self.rewards.cpu().numpy(), self.discounts.cpu().numpy(), self.step_types.cpu().numpy())
 
 
+@dataclass(eq=False)
+class Trajectory:
+    """Records of a fused rollout: entry t is the VecTimeStep step t returns
+    (any field None when not requested)."""
+    observations: torch.Tensor | None  # (T, N, v, v, 2) uint8
+    rewards: torch.Tensor | None       # (T, N) float32
+    discounts: torch.Tensor | None     # (T, N) float32
+    step_types: torch.Tensor | None    # (T, N) int8
+
+
 @dataclass(frozen=True)
 class EnvState:
     grid: Grid
@@ -358,6 +368,51 @@ class VecEnv:
         if self.strict and flag_ptr is not None:
             self.check()
         return VecTimeStep(*outs)
+
+    # -- fused rollout
+    def rollout(self, steps: int, policy_keys: torch.Tensor | None = None, actions: torch.Tensor | None = None,
+                t0: int = 0, record: Sequence[str] = ("observations", "rewards", "discounts", "step_types"),
+                out: Trajectory | None = None) -> Trajectory:
+        """``steps`` consecutive ``step`` calls in one kernel (state on chip for
+        the whole rollout), bit-identical to them.  Actions come from the
+        random policy of ref harness.py:58-64 (``policy_keys``: step t plays
+        word t0 + t of each env's key mod 6, as ``random_actions``) or from a
+        (steps, N) tensor ``actions``.  ``record`` picks the per-step fields
+        kept (ref harness.py:103-143 accumulates only statistics: pass
+        ``record=()`` and ``enable_stats()`` for that).  Does not consume an
+        epoch: rollouts and steps may be interleaved freely."""
+        n, v, dev = self.num_envs, self.params.view_size, self.device
+        if steps < 0 or t0 < 0:
+            raise ValueError("steps and t0 must be >= 0")
+        if (policy_keys is None) == (actions is None):
+            raise ValueError("pass exactly one of policy_keys / actions")
+        if policy_keys is not None:
+            if policy_keys.shape != (n, 2) or policy_keys.device != dev:
+                raise ValueError(f"policy_keys must be a ({n}, 2) tensor on {dev}")
+            policy_keys = policy_keys.to(torch.int64).contiguous()
+        else:
+            if not isinstance(actions, torch.Tensor):
+                actions = torch.as_tensor(np.asarray(actions))
+            if actions.shape != (steps, n):
+                raise InvalidAction(f"expected ({steps}, {n}) actions, got shape {tuple(actions.shape)}")
+            if bool(((actions < 0) | (actions >= 6)).any()):  # ref vecenv.py:297-301, before any mutation
+                raise InvalidAction("action outside [0, 5]")
+            actions = actions.to(dev, torch.uint8).contiguous()
+        unknown = set(record) - {"observations", "rewards", "discounts", "step_types"}
+        if unknown:
+            raise ValueError(f"unknown record fields {sorted(unknown)}")
+        if out is None:
+            out = Trajectory(
+                torch.empty((steps, n, v, v, 2), dtype=torch.uint8, device=dev) if "observations" in record else None,
+                torch.empty((steps, n), dtype=torch.float32, device=dev) if "rewards" in record else None,
+                torch.empty((steps, n), dtype=torch.float32, device=dev) if "discounts" in record else None,
+                torch.empty((steps, n), dtype=torch.int8, device=dev) if "step_types" in record else None)
+        o = _lib.Out(_ptr(out.observations), _ptr(out.rewards), _ptr(out.discounts), _ptr(out.step_types),
+                     _ptr(self.stats))
+        _lib.check(_lib.lib().xmg_rollout(C.byref(self._desc), C.byref(self._state), _ptr(policy_keys),
+                                          _ptr(actions), t0, steps, n, C.byref(o), _stream(dev)), "xmg_rollout")
+        self.launches += 1
+        return out
 
     def check(self) -> None:
         """Raise InvalidAction if a device-validated batch was rejected (syncs)."""

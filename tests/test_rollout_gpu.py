@@ -1,0 +1,133 @@
+"""GPU parity of the fused rollout kernel (xmg_rollout).
+
+The rollout is T VecEnv.step calls in one kernel; it must be bit-identical to
+them (and therefore to the oracle): every record of every step (observation,
+reward, discount, step type), the final state (grids, pose, pocket, step
+count, goal / task word, rng key) and the episode statistics.
+"""
+import numpy as np
+import pytest
+import torch
+
+from .helpers import benchmark_file, oracle_from_table
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(env_name, config, n, resample=False, see=None, **kw):
+    from paper_2312_12044_b200 import VecEnv, load_benchmark, make
+    _, params = make(env_name)
+    if see is not None:
+        from dataclasses import replace
+        params = replace(params, see_through_walls=see)
+    bm = load_benchmark(benchmark_file(config)) if config else None
+    a = VecEnv(params, n, bm, resample_tasks=resample, **kw)
+    b = VecEnv(params, n, bm, resample_tasks=resample, **kw)
+    return params, bm, a, b
+
+
+def _same_state(a, b, msg):
+    torch.testing.assert_close(a.grids, b.grids, rtol=0, atol=0, msg=f"grids {msg}")
+    assert torch.equal(a.agent, b.agent), f"agent word {msg}"
+    assert torch.equal(a.rng, b.rng), f"rng {msg}"
+
+
+@pytest.mark.parametrize("env_name,config,n,steps,resample,see", [
+    ("XLand-MiniGrid-R4-13x13", "medium", 4096, 600, False, None),
+    ("XLand-MiniGrid-R1-9x9", "trivial", 4096, 300, False, None),
+    ("XLand-MiniGrid-R9-25x25", "high", 1024, 400, False, None),
+    ("XLand-MiniGrid-R4-13x13", "medium", 1000, 520, True, None),     # resample-on-reset, ragged tail
+    ("XLand-MiniGrid-R2-13x13", "small", 999, 300, False, False),     # occluded view, odd n
+    ("MiniGrid-DoorKey-8x8", None, 2048, 250, False, None),
+    ("MiniGrid-UnlockPickUp", None, 1024, 400, False, None),
+    ("MiniGrid-FourRooms", None, 512, 300, False, None),
+    ("MiniGrid-Empty-8x8", None, 333, 200, False, None),
+])
+def test_rollout_equals_steps(env_name, config, n, steps, resample, see):
+    from paper_2312_12044_b200 import key_from_seed, policy_keys, random_actions
+    params, bm, a, b = _pair(env_name, config, n, resample, see)
+    root = key_from_seed(7)
+    a.reset(root)
+    b.reset(root)
+    sa, sb = a.enable_stats(), b.enable_stats()
+    pk = policy_keys(key_from_seed(1), n, device=a.device)
+    acts = random_actions(pk, 0, steps)
+    tr = b.rollout(steps, policy_keys=pk)
+    for t in range(steps):
+        ts = a.step(acts[t])
+        assert torch.equal(ts.observations, tr.observations[t]), f"obs t={t}"
+        assert torch.equal(ts.rewards, tr.rewards[t]), f"reward t={t}"
+        assert torch.equal(ts.discounts, tr.discounts[t]), f"discount t={t}"
+        assert torch.equal(ts.step_types, tr.step_types[t]), f"step type t={t}"
+    a.check()
+    _same_state(a, b, "after rollout")
+    torch.testing.assert_close(sa.sum(0), sb.sum(0), rtol=1e-12, atol=1e-9)
+    assert float(sa[:, 1].sum()) == float(sb[:, 1].sum())  # trial counts exact
+
+
+def test_rollout_vs_oracle_and_interleaving():
+    """Rollout chunks interleaved with single steps (the rollout consumes no
+    epoch) against the oracle on the same keys, tasks and actions."""
+    from paper_2312_12044_b200 import VecEnv, key_from_seed, load_benchmark, make, policy_keys, random_actions
+    _, params = make("XLand-MiniGrid-R4-13x13")
+    bm = load_benchmark(benchmark_file("medium"))
+    n = 2048
+    vec = VecEnv(params, n, bm)
+    ora = oracle_from_table(params, bm.task_table(), vec._ids_host)
+    root = key_from_seed(0)
+    vec.reset(root)
+    ora.reset(root)
+    pk = policy_keys(key_from_seed(1), n, device=vec.device)
+    acts_h = random_actions(pk, 0, 560).cpu().numpy()
+    t = 0
+    for kind, k in [("roll", 100), ("step", 3), ("roll", 1), ("step", 1), ("roll", 405), ("step", 50)]:
+        if kind == "roll":
+            tr = vec.rollout(k, policy_keys=pk, t0=t)
+            recs = [(tr.observations[i], tr.rewards[i], tr.discounts[i], tr.step_types[i]) for i in range(k)]
+        else:
+            recs = []
+            for i in range(k):
+                ts = vec.step(torch.from_numpy(acts_h[t + i]).cuda())
+                recs.append((ts.observations.clone(), ts.rewards.clone(), ts.discounts.clone(), ts.step_types.clone()))
+        for i in range(k):
+            o, r, d, s = ora.step(acts_h[t + i])
+            np.testing.assert_array_equal(recs[i][0].cpu().numpy(), o, err_msg=f"obs t={t + i}")
+            np.testing.assert_array_equal(recs[i][1].cpu().numpy(), r.astype(np.float32))
+            np.testing.assert_array_equal(recs[i][2].cpu().numpy(), d.astype(np.float32))
+            np.testing.assert_array_equal(recs[i][3].cpu().numpy(), s, err_msg=f"step type t={t + i}")
+        t += k
+        np.testing.assert_array_equal(vec.grids.cpu().numpy(), ora.grids, err_msg=f"grids t={t}")
+        np.testing.assert_array_equal(vec.rng.cpu().numpy().view(np.uint64), ora.rng)
+    vec.check()
+
+
+def test_rollout_explicit_actions_and_partial_records():
+    """A (T, N) action tensor instead of the policy keys; records subset;
+    stats-only mode; invalid actions rejected before any mutation."""
+    from paper_2312_12044_b200 import InvalidAction, key_from_seed
+    params, bm, a, b = _pair("XLand-MiniGrid-R4-13x13", "medium", 777)
+    root = key_from_seed(3)
+    a.reset(root)
+    b.reset(root)
+    g = torch.Generator().manual_seed(5)
+    acts = torch.randint(0, 6, (530, 777), generator=g, dtype=torch.int64)
+    sa, sb = a.enable_stats(), b.enable_stats()
+    tr = b.rollout(300, actions=acts[:300], record=("rewards", "step_types"))
+    assert tr.observations is None and tr.discounts is None
+    b.rollout(230, actions=acts[300:].cuda(), record=())
+    rews, sts = [], []
+    for t in range(530):
+        ts = a.step(acts[t].cuda())
+        if t < 300:
+            rews.append(ts.rewards.clone())
+            sts.append(ts.step_types.clone())
+    assert torch.equal(torch.stack(rews), tr.rewards)
+    assert torch.equal(torch.stack(sts), tr.step_types)
+    _same_state(a, b, "after explicit-action rollout")
+    torch.testing.assert_close(sa.sum(0), sb.sum(0), rtol=1e-12, atol=1e-9)
+    before = b.grids.clone()
+    bad = acts[:10].clone()
+    bad[4, 17] = 6
+    with pytest.raises(InvalidAction):
+        b.rollout(10, actions=bad)
+    assert torch.equal(before, b.grids)
