@@ -20,10 +20,13 @@
 // calls of xmg_step with the same actions (tests/test_rollout_gpu.py).
 
 constexpr int kRollWarps = 4;
+#ifndef XMG_ROLL_MINB
+#define XMG_ROLL_MINB 4  // resident CTAs per SM the register allocation targets (<= 128 registers)
+#endif
 constexpr int kRollLg = 2;  // unused bucket area of WarpScratch (4 << kRollLg bytes)
 
 struct RollGeo {
-  int hw, grids, rbw, rules, ob, obs, hwp, scratch, cand, keys, desc, warp_bytes;
+  int hw, grids, rbw, rules, ob, obs, hwp, scratch, desc, warp_bytes;
   int64_t total;
 };
 
@@ -34,14 +37,15 @@ __host__ __device__ inline RollGeo make_roll_geo(int H, int W, int V, int R) {
   g.rbw = 16 * ((kRowHeader + R + 3) / 4);      // one lane's task row header + rules
   g.rules = R > 0 ? 32 * g.rbw : 0;
   g.ob = 2 * V * V;
-  g.obs = 2 * round16(32 * g.ob);               // double-buffered observation records
+  // double-buffered observation records; between the bulk stores of two
+  // steps the same bytes hold the 32 lanes' trial keys of the resets
+  g.obs = max(2 * round16(32 * g.ob), round16(32 * (int)sizeof(TrialKeys)));
   g.hwp = round16(g.hw + 16);
-  // WarpScratch of warp_build: wd u64[hwp] | fc u16[hwp] | slot u16[hwp] | bk | grid u8[hwp] | misc 64 u64
+  // WarpScratch of warp_build: wd u64[hwp] | fc u16[hwp] | slot u16[hwp] | bk | grid u8[hwp] | misc 64 u64;
+  // the PUT_DOWN candidate list (u32[hw]) reuses wd (never live at once)
   g.scratch = 12 * g.hwp + (4 << kRollLg) + g.hwp + 512;
-  g.cand = 4 * g.hwp;                           // PUT_DOWN candidate list
-  g.keys = 32 * (int)sizeof(TrialKeys);
   g.desc = round16((int)sizeof(xmg_env_desc));
-  g.warp_bytes = g.grids + g.rules + g.obs + g.scratch + g.cand + g.keys + g.desc;
+  g.warp_bytes = g.grids + g.rules + g.obs + g.scratch + g.desc;
   g.total = (int64_t)kRollWarps * g.warp_bytes;
   return g;
 }
@@ -53,7 +57,7 @@ __device__ __forceinline__ uint32_t policy_block(uint64_t kh, uint64_t kl, uint6
          ((uint32_t)(w.w3 % 6) << 24);
 }
 
-__global__ void __launch_bounds__(kRollWarps * 32) rollout_kernel(const xmg_env_desc d, const xmg_state s,
+__global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel(const xmg_env_desc d, const xmg_state s,
                                                                  const uint64_t* pkeys, const uint8_t* actions,
                                                                  int64_t t0, int64_t T, int64_t n, const xmg_out o) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -68,9 +72,9 @@ __global__ void __launch_bounds__(kRollWarps * 32) rollout_kernel(const xmg_env_
   uint32_t* rules_s = reinterpret_cast<uint32_t*>(wb + geo.grids);
   uint8_t* obs_s = wb + geo.grids + geo.rules;
   uint8_t* scratch = obs_s + geo.obs;
-  uint32_t* cand = reinterpret_cast<uint32_t*>(scratch + geo.scratch);
-  TrialKeys* keys = reinterpret_cast<TrialKeys*>(scratch + geo.scratch + geo.cand);
-  xmg_env_desc* sdesc = reinterpret_cast<xmg_env_desc*>(scratch + geo.scratch + geo.cand + geo.keys);
+  uint32_t* cand = reinterpret_cast<uint32_t*>(scratch);      // aliases wd
+  TrialKeys* keys = reinterpret_cast<TrialKeys*>(obs_s);      // aliases the observation buffers
+  xmg_env_desc* sdesc = reinterpret_cast<xmg_env_desc*>(scratch + geo.scratch);
   ResetOut* rout = reinterpret_cast<ResetOut*>(make_scratch(scratch, geo.hwp, kRollLg).misc + 40);
 
   const int nvalid = (int)min((int64_t)32, n - e0);
@@ -117,11 +121,8 @@ __global__ void __launch_bounds__(kRollWarps * 32) rollout_kernel(const xmg_env_
   }
   __syncwarp();
 
-  View vw;
-  vw.g = grids + lane * HW;
-  vw.stage = vw.g;
-  vw.sbase = vw.slo = 0;
-  vw.shi = HW;
+  SView vw;
+  vw.stage = grids + lane * HW;
   double st_ret = 0.0, st_trials = 0.0, st_len = 0.0;
   uint32_t acts4 = 0;
 
@@ -204,6 +205,8 @@ __global__ void __launch_bounds__(kRollWarps * 32) rollout_kernel(const xmg_env_
     // ---- auto-reset of finished trials (ref:vecenv.py:359-361 -> :224-291)
     uint32_t lm = __ballot_sync(0xffffffffu, last);
     if (lm) {
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // obs buffers free
+      __syncwarp();
       if (last) derive_trial_keys(rk.x, rk.y, resample, keys + lane);
       __syncwarp();
       for (; lm; lm &= lm - 1) {
@@ -237,7 +240,11 @@ __global__ void __launch_bounds__(kRollWarps * 32) rollout_kernel(const xmg_env_
           if (V == 5) obs_see<5>(vw.stage, 0, dst, r, c, dir, H, W, V);
           else obs_see<0>(vw.stage, 0, dst, r, c, dir, H, W, V);
         } else {
-          obs_occluded(vw, dst, r, c, dir, H, W, V);
+          View ov;
+          ov.g = ov.stage = vw.stage;
+          ov.sbase = ov.slo = 0;
+          ov.shi = HW;
+          obs_occluded(ov, dst, r, c, dir, H, W, V);
         }
       }
       const uint32_t bytes = (uint32_t)(nvalid * geo.ob);

@@ -233,7 +233,15 @@ struct Nbrs {
   int flat[4];
 };
 
-__device__ __forceinline__ Nbrs load_nbrs(const View& vw, int H, int W, int ar, int ac) {
+// A grid staged whole in shared memory (the rollout kernel): no range checks.
+struct SView {
+  uint8_t* stage;
+  __device__ __forceinline__ uint8_t rd(int f) const { return stage[f]; }
+  __device__ __forceinline__ void wr(int f, uint8_t v) const { stage[f] = v; }
+};
+
+template <class VW>
+__device__ __forceinline__ Nbrs load_nbrs(const VW& vw, int H, int W, int ar, int ac) {
   Nbrs nb;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -255,7 +263,8 @@ __device__ __forceinline__ int nbr_code(const Nbrs& nb, int k) {
 
 // Rules gated on MOVE / PICK_UP (only the slots in `slots`, stored order).
 // Select-based, so lanes holding different rule kinds stay converged.
-__device__ XMG_RARE int agent_rules(View vw, Nbrs& nb, const uint32_t* rules, uint32_t slots, int pocket) {
+template <class VW>
+__device__ XMG_RARE int agent_rules(VW vw, Nbrs& nb, const uint32_t* rules, uint32_t slots, int pocket) {
   for (; slots; slots &= slots - 1) {
     const uint32_t rw = rules[__ffs(slots) - 1];
     const int kind = rw & 0xff, a = (rw >> 8) & 0xff, out = rw >> 24;
@@ -303,38 +312,50 @@ __device__ __forceinline__ void obs_see(const uint8_t* stage, int sbase, uint8_t
                                         int W, int Vrt) {
   const int V = VV ? VV : Vrt;
   const int h = V / 2;
-  // origin (view cell (0, 0)) and the world steps of i (rows) and j (columns)
-  int r0, c0, dri, dci, drj, dcj;
-  switch (d) {
-    case 0: r0 = r - (V - 1); c0 = c - h; dri = 1; dci = 0; drj = 0; dcj = 1; break;
-    case 1: r0 = r - h; c0 = c + (V - 1); dri = 0; dci = -1; drj = 1; dcj = 0; break;
-    case 2: r0 = r + (V - 1); c0 = c + h; dri = -1; dci = 0; drj = 0; dcj = -1; break;
-    default: r0 = r + h; c0 = c - (V - 1); dri = 0; dci = 1; drj = -1; dcj = 0; break;
-  }
+  // origin (view cell (0, 0)) and the world steps of i (rows) and j
+  // (columns), select-based (lanes facing different ways stay converged)
+  const bool d0 = d == 0, d1 = d == 1, d2 = d == 2;
+  const int r0 = d0 ? r - (V - 1) : d2 ? r + (V - 1) : d1 ? r - h : r + h;
+  const int c0 = d0 ? c - h : d2 ? c + h : d1 ? c + (V - 1) : c - (V - 1);
+  const int dri = d0 ? 1 : d2 ? -1 : 0, dci = d1 ? -1 : (d0 || d2) ? 0 : 1;
+  const int drj = d1 ? 1 : (d0 || d2) ? 0 : -1, dcj = d0 ? 1 : d2 ? -1 : 0;
   // the facing makes i move along one world axis and j along the other:
-  // validity is a product of a mask over i and a mask over j
-  uint32_t mi = 0, mj = 0;
-  for (int t = 0; t < V; ++t) {
-    const int wi = dri ? r0 + t * dri : c0 + t * dci;  // world coordinate moved by i
-    const int wj = drj ? r0 + t * drj : c0 + t * dcj;  // world coordinate moved by j
-    mi |= (uint32_t)((unsigned)wi < (unsigned)(dri ? H : W)) << t;
-    mj |= (uint32_t)((unsigned)wj < (unsigned)(drj ? H : W)) << t;
-  }
+  // validity is a product of a bit range over i and one over j
+  auto range_mask = [V](int b, int st, int lim) {  // t in [0, V) with 0 <= b + t*st < lim
+    int lo = st > 0 ? -b : b - lim + 1, hi = st > 0 ? lim - b : b + 1;
+    lo = max(lo, 0);
+    hi = min(hi, V);
+    return hi > lo ? ((1u << hi) - 1u) & ~((1u << lo) - 1u) : 0u;
+  };
+  const uint32_t mi = dri ? range_mask(r0, dri, H) : range_mask(c0, dci, W);
+  const uint32_t mj = drj ? range_mask(r0, drj, H) : range_mask(c0, dcj, W);
   const int di = dri * W + dci, dj = drj * W + dcj;  // flat steps
   const uint8_t* p0 = stage - sbase + (r0 * W + c0);
-  uint16_t* o = reinterpret_cast<uint16_t*>(dst);
+  // (tile, color) byte pairs as 16-bit values; written as one u16 plus
+  // (V*V - 1) / 2 u32 words (the record is 2-byte aligned: an odd-offset
+  // record leads with its u16, an even one ends with it)
+  const bool odd = (reinterpret_cast<uintptr_t>(dst) & 2) != 0;
   if constexpr (VV != 0) {
+    constexpr int NC = VV * VV;
+    uint32_t v[NC];
 #pragma unroll
     for (int i = 0; i < VV; ++i) {
       const bool vi = (mi >> i) & 1;
+      const uint8_t* pi = p0 + i * di;
 #pragma unroll
       for (int j = 0; j < VV; ++j) {
         uint32_t code = 0;
-        if (vi && ((mj >> j) & 1)) code = p0[i * di + j * dj];
-        o[i * VV + j] = (uint16_t)(((code * 0x1001u) >> 4) & 0x0F0Fu);  // (tile, color) bytes
+        if (vi && ((mj >> j) & 1)) code = pi[j * dj];
+        v[i * VV + j] = ((code * 0x1001u) >> 4) & 0x0F0Fu;
       }
     }
+    *reinterpret_cast<uint16_t*>(dst + (odd ? 0 : 2 * (NC - 1))) = (uint16_t)(odd ? v[0] : v[NC - 1]);
+    uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + (odd ? 2 : 0));
+#pragma unroll
+    for (int k = 0; k < (NC - 1) / 2; ++k)
+      d32[k] = odd ? (v[2 * k + 1] | (v[2 * k + 2] << 16)) : (v[2 * k] | (v[2 * k + 1] << 16));
   } else {
+    uint16_t* o = reinterpret_cast<uint16_t*>(dst);
     for (int i = 0; i < V; ++i)
       for (int j = 0; j < V; ++j) {
         uint32_t code = 0;
