@@ -413,6 +413,33 @@ def run_ours(args):
                          "(tests/test_rollout_gpu.py); same K steps and phase as the timed window; records = "
                          "obs + reward + discount + step type per env-step written to HBM"}
 
+    # ---- 224x224 image observations of the last step's
+    # records: xmg_image_obs, HBM-write bound (150528 B out per image)
+    image = None
+    if not args.no_image:
+        from paper_2312_12044_b200.render import image_observations
+        ni = min(n, 1 << 14)
+        obs_src = vec._alloc_out(True)[0][:ni]
+        img_out = torch.empty((ni, 224, 224, 3), dtype=torch.uint8, device=dev)
+        for _ in range(2):
+            image_observations(obs_src, out=img_out, check=False)
+        reps = 10
+        i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        i0.record(stream)
+        for _ in range(reps):
+            image_observations(obs_src, out=img_out, check=False)
+        i1.record(stream)
+        torch.cuda.synchronize(dev)
+        ims = i0.elapsed_time(i1) / reps
+        vv = params.view_size
+        ib = ni * (224 * 224 * 3 + 2 * vv * vv)
+        image = {"images_per_s": ni / (ims / 1e3), "images": ni, "ms_per_launch": ims,
+                 "bytes_per_image": 224 * 224 * 3 + 2 * vv * vv, "achieved_gbs": ib / (ims / 1e3) / 1e9,
+                 "frac_of_hbm_peak": ib / (ims / 1e3) / 1e9 / peak,
+                 "note": "xmg_image_obs on the timed window's last observations (ref render.py:225-243), "
+                         "output 2.4 GB > L2"}
+        del img_out
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         r = cpu_reference(args.workload, min(n, 1 << 14), 1 << 20, os.cpu_count() or 1, budget_s=12.0)
@@ -431,7 +458,7 @@ def run_ours(args):
                        "l2": "inputs larger than L2" if n * params.height * params.width > 126e6
                              else "state resident in L2 (small workload)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "fused_rollout": fused,
+            "fused_rollout": fused, "image_obs": image,
             "clocks": clocks.summary(),
             "episode_stats": {"return_sum": float(tot[0]), "trials": float(tot[1]), "length_sum": float(tot[2])},
         }
@@ -452,6 +479,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fused", action="store_true")
+    ap.add_argument("--no-image", action="store_true")
     ap.add_argument("--fused-chunk", type=int, default=32)
     args = ap.parse_args()
     if args.warmup < 3:

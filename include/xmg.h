@@ -191,6 +191,23 @@ int32_t xmg_rollout(const xmg_env_desc* desc, const xmg_state* state, const uint
 /* Dynamic shared memory per 128-env CTA of the rollout kernel (<0: unsupported). */
 int64_t xmg_rollout_smem_bytes(const xmg_env_desc* desc);
 
+/* ---- observation images (ref render.py) ---------------- */
+
+/* Sprite atlas for one pixel size: atlas[tile][color] = (px, px, 3) u8 RGB,
+ * 15 x 14 sprites, each equal to ref render.py:158-169 sprite(tile, color, px)
+ * (masks of :107-155 in IEEE double, no contraction).  px in [4, 224]. */
+int32_t xmg_sprites(int32_t px, uint8_t* atlas /*[15][14][px][px][3]*/, void* stream);
+
+/* ref render.py:225-243 image_observation for n observations (v, v, 2):
+ * out[i] = (224, 224, 3) u8, px = 224 / v (>= 4), the v*px square centred
+ * with an UNSEEN-shade margin.  `atlas` from xmg_sprites(224 / v).  Codes
+ * outside the enums (tile > 14, color > 13) draw as END_OF_MAP (the host
+ * wrapper rejects them first, like the reference).  out 16-byte aligned; the
+ * atlas allocation must extend >= 8 bytes before and after its 210*px*px*3
+ * bytes (unaligned word reads). */
+int32_t xmg_image_obs(const uint8_t* obs /*[n][v][v][2]*/, int64_t n, int32_t view, const uint8_t* atlas,
+                      uint8_t* out /*[n][224][224][3]*/, void* stream);
+
 /* Size in u32 words of xmg_state.work for n envs. */
 int64_t xmg_work_words(int64_t n);
 

@@ -204,3 +204,28 @@ class OracleVecEnv:
 
     def agent(self) -> np.ndarray:
         return np.stack([self.agent_r, self.agent_c, self.agent_dir, self.pocket], axis=1)
+
+
+# ------------------------------------------------------------ observation images
+IMAGE_SIDE = 224  # ref render.py:21
+
+
+def sprite(tile: int, color: int, px: int) -> np.ndarray:
+    """(px, px, 3) u8 sprite, ref render.py:158-169 (xmg_render_oracle.c)."""
+    L = lib()
+    out = np.empty((px, px, 3), np.uint8)
+    if L.xmgo_sprite(C.c_int32(tile), C.c_int32(color), C.c_int32(px), C.c_void_p(_p(out))) != 0:
+        raise ValueError(f"no sprite for tile {tile} color {color} at {px}px")
+    return out
+
+
+def image_observations(obs: np.ndarray) -> np.ndarray:
+    """(n, 224, 224, 3) images of (n, v, v, 2) observations, ref render.py:225-243."""
+    obs = np.ascontiguousarray(obs, dtype=np.uint8)
+    n, v = obs.shape[0], obs.shape[1]
+    out = np.empty((n, IMAGE_SIDE, IMAGE_SIDE, 3), np.uint8)
+    L = lib()
+    L.xmgo_image_observations.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]
+    if L.xmgo_image_observations(_p(obs), n, v, _p(out)) != 0:
+        raise ValueError("observation outside the renderer's range")
+    return out

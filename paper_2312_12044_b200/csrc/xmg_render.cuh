@@ -1,0 +1,184 @@
+// xmg_render.cuh — 224x224 RGB observation images on the device (included by
+// xmg_step.cu inside its anonymous namespace).
+//
+// ref:render.py (cited below): procedural sprites (_build_sprite :107-155),
+// cached per (tile, color, px) (:158-169), and image_observation (:225-243):
+// px = 224 // v, the v*px square centred with an UNSEEN-shade margin, cell
+// (r, c) drawn with sprite(obs[r][c]).
+//
+// Two kernels:
+//  * sprite_kernel builds the whole atlas [15 tiles][14 colors][px][px][3]
+//    for one px, one thread per pixel; the masks are evaluated in IEEE double
+//    with one rounding per operation in NumPy's order (explicit _rn
+//    intrinsics: no FMA contraction), so every pixel equals the reference's;
+//  * image_kernel writes images: an env's image is 224 rows x 42 chunks of
+//    16 bytes; each thread assembles a chunk, word by word, from unaligned
+//    4-byte reads of the atlas (L2-resident, 1.2 MB at px = 44) merged with
+//    byte_perm, and stores it with one coalesced 16-byte store.  HBM-write
+//    bound: 150528 bytes out per image, v*v*2 in.
+
+constexpr int kImageSide = 224;
+constexpr int kImageRow = 3 * kImageSide;          // 672 bytes
+constexpr int kImageChunks = kImageRow / 16;       // 42 per row
+constexpr int kImageBytes = kImageSide * kImageRow;  // 150528
+constexpr int kRenderThreads = 256;
+
+// ref:render.py:48-67: _COLOR_RGB, _BG, _GRID_LINE
+__constant__ uint8_t cColorRGB[14][3] = {
+    {0, 0, 0},      {12, 12, 12},  {0, 0, 0},       {220, 50, 50},  {60, 180, 75},
+    {65, 105, 225}, {145, 70, 200}, {235, 200, 50}, {150, 150, 150}, {25, 25, 25},
+    {240, 140, 40}, {245, 245, 245}, {150, 100, 60}, {240, 130, 180}};
+
+__device__ __forceinline__ double dsq(double a) { return __dmul_rn(a, a); }
+
+// One pixel of sprite (tile, color, px), packed 0x00BBGGRR.
+__device__ uint32_t sprite_pixel(int tile, int color, int px, int y, int x) {
+  const uint32_t rgb = cColorRGB[color][0] | (cColorRGB[color][1] << 8) | (cColorRGB[color][2] << 16);
+  auto pack = [](int r, int g, int b) { return (uint32_t)r | ((uint32_t)g << 8) | ((uint32_t)b << 16); };
+  const int R = cColorRGB[color][0], G = cColorRGB[color][1], B = cColorRGB[color][2];
+  const uint32_t half = pack(R / 2, G / 2, B / 2), tq = pack(R * 3 / 4, G * 3 / 4, B * 3 / 4);
+  const uint32_t bg = pack(30, 30, 30), black = 0;
+  // _shape_masks (:96-100): dy = (y - cy) / px, cy = cx = (px - 1) / 2.0
+  const double cy = __ddiv_rn((double)(px - 1), 2.0);
+  const double dy = __ddiv_rn(__dsub_rn((double)y, cy), (double)px);
+  const double dx = __ddiv_rn(__dsub_rn((double)x, cy), (double)px);
+  const double ady = fabs(dy), adx = fabs(dx);
+  const double r2 = __dadd_rn(dsq(dy), dsq(dx));
+  uint32_t out = bg;
+  switch (tile) {
+    case 0: case 2: out = black; break;                       // END_OF_MAP, EMPTY
+    case 1: out = pack(12, 12, 12); break;                    // UNSEEN
+    case 3:                                                   // FLOOR: tinted grid line
+      if (y == px - 1 || x == px - 1) out = pack((45 + R) / 2, (45 + G) / 2, (45 + B) / 2);
+      break;
+    case 4: out = rgb; break;                                 // WALL
+    case 5: if (r2 <= __dmul_rn(0.35, 0.35)) out = rgb; break;  // BALL
+    case 6: if (ady <= 0.30 && adx <= 0.30) out = rgb; break;   // SQUARE
+    case 7:                                                     // PYRAMID
+      if (dy >= -0.35 && dy <= 0.35 && adx <= __ddiv_rn(__dadd_rn(dy, 0.35), 2.0)) out = rgb;
+      break;
+    case 8: {                                                   // GOAL
+      const int e = px / 8 + 1, f = px - px / 8 - 1;
+      out = (y < e || y >= f || x < e || x >= f) ? rgb : half;
+      break;
+    }
+    case 9: {                                                   // KEY
+      if (adx <= 0.13 && dy >= -0.15 && dy <= 0.38) out = rgb;
+      const double ring = __dadd_rn(dsq(dx), dsq(__dadd_rn(dy, 0.22)));
+      if (ring <= __dmul_rn(0.18, 0.18) && ring >= __dmul_rn(0.08, 0.08)) out = rgb;
+      if (fabs(__dsub_rn(dy, 0.30)) <= 0.05 && dx >= 0.0 && dx <= 0.2) out = rgb;
+      break;
+    }
+    case 10: case 11: case 12: {                                // doors
+      const bool frame = ady >= 0.36 || adx >= 0.36;
+      if (frame) out = rgb;
+      if (tile == 10) {
+        if (!frame) out = half;
+        if (r2 <= __dmul_rn(0.07, 0.07)) out = black;
+      } else if (tile == 11) {
+        if (!frame) out = tq;
+        if (__dadd_rn(dsq(__dsub_rn(dx, 0.22)), dsq(dy)) <= __dmul_rn(0.06, 0.06)) out = black;
+      }
+      break;
+    }
+    case 13:                                                    // HEX
+      if (ady <= 0.32 && __dadd_rn(adx, __dmul_rn(0.5, ady)) <= 0.38) out = rgb;
+      break;
+    case 14: {                                                  // STAR
+      const bool spokes = adx <= 0.09 || ady <= 0.09;
+      const double l1 = __dadd_rn(adx, ady);
+      if (spokes && l1 <= 0.42) out = rgb;
+      if (l1 <= 0.16) out = rgb;
+      break;
+    }
+    default: break;
+  }
+  return out;
+}
+
+__global__ void sprite_kernel(int px, uint8_t* atlas) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)px * px;
+  if (i >= 210 * per) return;
+  const int s = (int)(i / per), p = (int)(i - s * per);
+  const uint32_t v = sprite_pixel(s / 14, s % 14, px, p / px, p % px);
+  uint8_t* o = atlas + 3 * i;
+  o[0] = (uint8_t)v;
+  o[1] = (uint8_t)(v >> 8);
+  o[2] = (uint8_t)(v >> 16);
+}
+
+// Unaligned 32-bit read from the (padded) atlas: two aligned words and a
+// funnel shift.
+__device__ __forceinline__ uint32_t ldu32(const uint8_t* p) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uint32_t* q = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+  return __funnelshift_r(__ldg(q), __ldg(q + 1), (uint32_t)(a & 3) * 8u);
+}
+
+constexpr uint32_t kShade = 0x0C0C0C0Cu;  // UNSEEN shade (12, 12, 12) bytes
+constexpr int kMarginCol = 255;
+
+// Images of n observations (v, v, 2).  Grid-stride over envs.  Each 4-byte
+// word w of an image row shows at most two cell columns (a sprite row is
+// 3*px >= 12 bytes): the per-CTA word table holds both columns (or the
+// margin), the byte offset of the word inside each column's sprite row, and
+// the byte_perm selector merging them; a word is then one or two unaligned
+// 4-byte atlas reads (L1/L2 resident) and a byte_perm.
+__global__ void __launch_bounds__(kRenderThreads) image_kernel(const uint8_t* __restrict__ obs, int64_t n, int v,
+                                                               int px, const uint8_t* __restrict__ atlas,
+                                                               uint8_t* __restrict__ out) {
+  __shared__ uint32_t wcol[kImageRow / 4];   // colA | colB << 8 | selector << 16
+  __shared__ int2 wrel[kImageRow / 4];       // byte offset of the word in colA's / colB's sprite row
+  __shared__ uint32_t base[56 * 56];         // atlas offset of cell (r, c)'s sprite (v <= 224 / 4)
+  const int off = (kImageSide - v * px) / 2, span = v * px, srow = 3 * px;
+  for (int w = threadIdx.x; w < kImageRow / 4; w += blockDim.x) {
+    int col[2], rel[2];
+    for (int k = 0; k < 2; ++k) {
+      const int b = 4 * w + 3 * k;  // first / last byte of the word
+      const int x = b / 3 - off;
+      col[k] = (x < 0 || x >= span) ? kMarginCol : x / px;
+      rel[k] = col[k] == kMarginCol ? 0 : 4 * w - 3 * (off + col[k] * px);
+    }
+    uint32_t sel = 0;
+    for (int j = 0; j < 4; ++j) {  // byte j from A (index j) unless it lies in colB's span
+      const int x = (4 * w + j) / 3 - off;
+      const int cj = (x < 0 || x >= span) ? kMarginCol : x / px;
+      sel |= (uint32_t)(cj == col[0] ? j : 4 + j) << (4 * j);
+    }
+    wcol[w] = (uint32_t)col[0] | ((uint32_t)col[1] << 8) | (sel << 16);
+    wrel[w] = make_int2(rel[0], rel[1]);
+  }
+  const uint32_t spr = (uint32_t)(srow * px);
+  for (int64_t e = blockIdx.x; e < n; e += gridDim.x) {
+    __syncthreads();  // tables ready / previous env's bases consumed
+    for (int k = threadIdx.x; k < v * v; k += blockDim.x) {
+      const int t = obs[(e * v * v + k) * 2], c = obs[(e * v * v + k) * 2 + 1];
+      base[k] = (t <= 14 && c <= 13) ? (uint32_t)(t * 14 + c) * spr : 0u;  // invalid codes: END_OF_MAP
+    }
+    __syncthreads();
+    uint8_t* img = out + e * (int64_t)kImageBytes;
+    for (int q = threadIdx.x; q < kImageSide * kImageChunks; q += blockDim.x) {
+      const int Y = q / kImageChunks, w0 = (q - Y * kImageChunks) * 4, yy = Y - off;
+      uint32_t o[4];
+      if (yy < 0 || yy >= span) {
+        o[0] = o[1] = o[2] = o[3] = kShade;
+      } else {
+        const int i = yy / px;
+        const uint8_t* rowp = atlas + (yy - i * px) * srow;  // sprite row yy % px of sprite 0
+        const uint32_t* brow = base + i * v;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t wc = wcol[w0 + k];
+          const int2 rl = wrel[w0 + k];
+          const int ca = wc & 0xff, cb = (wc >> 8) & 0xff;
+          const uint32_t a = ca == kMarginCol ? kShade : ldu32(rowp + brow[ca] + rl.x);
+          uint32_t b = a;
+          if (cb != ca) b = cb == kMarginCol ? kShade : ldu32(rowp + brow[cb] + rl.y);
+          o[k] = __byte_perm(a, b, wc >> 16);
+        }
+      }
+      *reinterpret_cast<uint4*>(img + Y * kImageRow + 4 * w0) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}

@@ -2118,6 +2118,7 @@ __global__ void validate_kernel(const void* a, int dtype, int64_t n, uint32_t ep
 }
 
 #include "xmg_rollout.cuh"
+#include "xmg_render.cuh"
 
 // ------------------------------------------------------- host side
 thread_local std::string g_err;
@@ -2517,6 +2518,32 @@ int32_t xmg_rollout(const xmg_env_desc* desc, const xmg_state* state, const uint
       (policy_keys && (reinterpret_cast<uintptr_t>(policy_keys) & 15)))
     return fail("agent / rng / policy key buffers must be 16-byte aligned");
   return launch_rollout(desc, state, policy_keys, actions, t0, steps, n, traj, (cudaStream_t)stream);
+}
+
+int32_t xmg_sprites(int32_t px, uint8_t* atlas, void* stream) {
+  if (px < 4 || px > kImageSide) return fail("tile_px must be in [4, 224]");
+  if (!atlas) return fail("null atlas");
+  const int64_t total = 210LL * px * px;
+  sprite_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(px, atlas);
+  return check_launch("sprite_kernel");
+}
+
+int32_t xmg_image_obs(const uint8_t* obs, int64_t n, int32_t view, const uint8_t* atlas, uint8_t* out,
+                      void* stream) {
+  if (view < 1 || kImageSide / view < 4) return fail("view size leaves tiles under 4px");
+  if (!obs || !atlas || !out) return fail("null buffer");
+  if (reinterpret_cast<uintptr_t>(out) & 15) return fail("image buffer must be 16-byte aligned");
+  if (n <= 0) return 0;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t blocks = std::min<int64_t>(n, (int64_t)sms * 8);
+  image_kernel<<<(unsigned)blocks, kRenderThreads, 0, (cudaStream_t)stream>>>(obs, n, view, kImageSide / view, atlas,
+                                                                              out);
+  return check_launch("image_kernel");
 }
 
 int64_t xmg_rollout_smem_bytes(const xmg_env_desc* desc) {
