@@ -59,6 +59,57 @@ class Ruleset:
             raise InvalidEncoding("ruleset exceeds padded widths")
         return Ruleset(self.goal, ar + (EMPTY_RULE,) * (max_rules - len(ar)), ao + (0,) * (max_objects - len(ao)))
 
+    def validate(self) -> "Ruleset":
+        """Reject malformed encodings (ref ruleset.py:61-69 -> rules.py:126-144,
+        goals.py:101-127): kinds in range, empty slots all zero, entity codes
+        with tile <= 14 and color <= 13, unused arguments zero."""
+        def code(c, what):
+            if not (0 <= c <= 255 and c >> 4 <= 14 and c & 15 <= 13):
+                raise InvalidEncoding(f"{what}: code {c} is not an entity")
+
+        def four(enc, what):
+            if len(enc) != 4 or any(not 0 <= v <= 255 for v in enc):
+                raise InvalidEncoding(f"{what} encoding must be four bytes, got {enc!r}")
+            return tuple(int(v) for v in enc)
+
+        kind, a1, a2, a3 = four(self.goal, "goal")
+        if kind == 0:
+            if (a1, a2, a3) != (0, 0, 0):
+                raise InvalidEncoding("empty goal must be all zeros")
+        elif kind > 14:
+            raise InvalidEncoding(f"unknown goal id {kind}")
+        elif kind == 5:  # AGENT_ON_POSITION: (row, col)
+            if a3 != 0:
+                raise InvalidEncoding("agent-on-position goal carries (row, col) only")
+        elif kind == 6:  # TILE_ON_POSITION
+            code(a1, "goal tile argument")
+        else:
+            code(a1, "goal argument a")
+            if kind in (4, 7, 8, 9, 10):  # tile-near pair goals
+                code(a2, "goal argument b")
+                if a3 != 0:
+                    raise InvalidEncoding("pair goal carries two entity arguments only")
+            elif (a2, a3) != (0, 0):
+                raise InvalidEncoding(f"goal id {kind} takes a single argument")
+        for r in self.rules:
+            kind, a, b, out = four(r, "rule")
+            if kind == 0:
+                if (a, b, out) != (0, 0, 0):
+                    raise InvalidEncoding("empty rule must be all zeros")
+                continue
+            if kind > 11:
+                raise InvalidEncoding(f"unknown rule id {kind}")
+            code(a, "rule input a")
+            code(out, "rule output")
+            if 3 <= kind <= 7:  # tile-near pair rules
+                code(b, "rule input b")
+            elif b != 0:
+                raise InvalidEncoding(f"rule id {kind} takes a single input, in_b must be 0")
+        for o in self.init_objects:
+            if o:
+                code(int(o), "initial object")
+        return self
+
     def to_row(self, max_rules: int = MAX_RULES, max_objects: int = MAX_INIT_OBJECTS) -> np.ndarray:
         p = self.padded(max_rules, max_objects)
         return np.array([*p.goal, *(b for r in p.rules for b in r), *p.init_objects], np.uint8)
