@@ -11,17 +11,15 @@
 //    for one px, one thread per pixel; the masks are evaluated in IEEE double
 //    with one rounding per operation in NumPy's order (explicit _rn
 //    intrinsics: no FMA contraction), so every pixel equals the reference's;
-//  * image_kernel writes images: an env's image is 224 rows x 42 chunks of
-//    16 bytes; each thread assembles a chunk, word by word, from unaligned
-//    4-byte reads of the atlas (L2-resident, 1.2 MB at px = 44) merged with
-//    byte_perm, and stores it with one coalesced 16-byte store.  HBM-write
-//    bound: 150528 bytes out per image, v*v*2 in.
+//  * image_kernel writes images: a CTA of 168 threads renders one image at a
+//    time, thread w owning 4-byte word w of every row; a word is one or two
+//    unaligned 4-byte reads of the atlas (L2-resident, 1.2 MB at px = 44)
+//    merged with byte_perm.  HBM-write bound: 150528 bytes out per image,
+//    v*v*2 in.
 
 constexpr int kImageSide = 224;
 constexpr int kImageRow = 3 * kImageSide;          // 672 bytes
-constexpr int kImageChunks = kImageRow / 16;       // 42 per row
 constexpr int kImageBytes = kImageSide * kImageRow;  // 150528
-constexpr int kRenderThreads = 256;
 
 // ref:render.py:48-67: _COLOR_RGB, _BG, _GRID_LINE
 __constant__ uint8_t cColorRGB[14][3] = {
@@ -119,66 +117,62 @@ __device__ __forceinline__ uint32_t ldu32(const uint8_t* p) {
 constexpr uint32_t kShade = 0x0C0C0C0Cu;  // UNSEEN shade (12, 12, 12) bytes
 constexpr int kMarginCol = 255;
 
-// Images of n observations (v, v, 2).  Grid-stride over envs.  Each 4-byte
-// word w of an image row shows at most two cell columns (a sprite row is
-// 3*px >= 12 bytes): the per-CTA word table holds both columns (or the
-// margin), the byte offset of the word inside each column's sprite row, and
-// the byte_perm selector merging them; a word is then one or two unaligned
-// 4-byte atlas reads (L1/L2 resident) and a byte_perm.
-__global__ void __launch_bounds__(kRenderThreads) image_kernel(const uint8_t* __restrict__ obs, int64_t n, int v,
-                                                               int px, const uint8_t* __restrict__ atlas,
-                                                               uint8_t* __restrict__ out) {
-  __shared__ uint32_t wcol[kImageRow / 4];   // colA | colB << 8 | selector << 16
-  __shared__ int2 wrel[kImageRow / 4];       // byte offset of the word in colA's / colB's sprite row
-  __shared__ uint32_t base[56 * 56];         // atlas offset of cell (r, c)'s sprite (v <= 224 / 4)
+// Images of n observations (v, v, 2).  One CTA per image at a time
+// (grid-stride over envs); thread w owns 4-byte word w of every image row
+// (168 words, 672 bytes: a row is one coalesced 672-byte store per CTA).  A
+// word shows at most two cell columns (a sprite row is 3*px >= 12 bytes): the
+// thread's column pair, byte offsets and byte_perm selector are fixed for
+// the whole image, so walking down the rows is a pointer increment of one
+// sprite row (3*px bytes) per row and two unaligned 4-byte atlas reads
+// (L1/L2 resident) per word.
+constexpr int kImageWords = kImageRow / 4;  // 168
+
+__global__ void __launch_bounds__(kImageWords) image_kernel(const uint8_t* __restrict__ obs, int64_t n, int v, int px,
+                                                           const uint8_t* __restrict__ atlas,
+                                                           uint8_t* __restrict__ out) {
+  __shared__ uint32_t base[56 * 56];  // atlas offset of cell (r, c)'s sprite (v <= 224 / 4)
+  const int w = threadIdx.x;
   const int off = (kImageSide - v * px) / 2, span = v * px, srow = 3 * px;
-  for (int w = threadIdx.x; w < kImageRow / 4; w += blockDim.x) {
-    int col[2], rel[2];
-    for (int k = 0; k < 2; ++k) {
-      const int b = 4 * w + 3 * k;  // first / last byte of the word
-      const int x = b / 3 - off;
-      col[k] = (x < 0 || x >= span) ? kMarginCol : x / px;
-      rel[k] = col[k] == kMarginCol ? 0 : 4 * w - 3 * (off + col[k] * px);
-    }
-    uint32_t sel = 0;
-    for (int j = 0; j < 4; ++j) {  // byte j from A (index j) unless it lies in colB's span
-      const int x = (4 * w + j) / 3 - off;
-      const int cj = (x < 0 || x >= span) ? kMarginCol : x / px;
-      sel |= (uint32_t)(cj == col[0] ? j : 4 + j) << (4 * j);
-    }
-    wcol[w] = (uint32_t)col[0] | ((uint32_t)col[1] << 8) | (sel << 16);
-    wrel[w] = make_int2(rel[0], rel[1]);
+  // this thread's word: first / last byte's cell column (or the margin), the
+  // word's byte offset inside each column's sprite row, the merge selector
+  int col[2], rel[2];
+  for (int k = 0; k < 2; ++k) {
+    const int x = (4 * w + 3 * k) / 3 - off;
+    col[k] = (x < 0 || x >= span) ? kMarginCol : x / px;
+    rel[k] = col[k] == kMarginCol ? 0 : 4 * w - 3 * (off + col[k] * px);
   }
+  uint32_t sel = 0;
+  for (int j = 0; j < 4; ++j) {  // byte j from the first column unless it lies in the second's span
+    const int x = (4 * w + j) / 3 - off;
+    const int cj = (x < 0 || x >= span) ? kMarginCol : x / px;
+    sel |= (uint32_t)(cj == col[0] ? j : 4 + j) << (4 * j);
+  }
+  const bool ma = col[0] == kMarginCol, mb = col[1] == kMarginCol, two = col[1] != col[0];
   const uint32_t spr = (uint32_t)(srow * px);
   for (int64_t e = blockIdx.x; e < n; e += gridDim.x) {
-    __syncthreads();  // tables ready / previous env's bases consumed
-    for (int k = threadIdx.x; k < v * v; k += blockDim.x) {
+    __syncthreads();  // previous image's bases consumed
+    for (int k = w; k < v * v; k += blockDim.x) {
       const int t = obs[(e * v * v + k) * 2], c = obs[(e * v * v + k) * 2 + 1];
       base[k] = (t <= 14 && c <= 13) ? (uint32_t)(t * 14 + c) * spr : 0u;  // invalid codes: END_OF_MAP
     }
     __syncthreads();
-    uint8_t* img = out + e * (int64_t)kImageBytes;
-    for (int q = threadIdx.x; q < kImageSide * kImageChunks; q += blockDim.x) {
-      const int Y = q / kImageChunks, w0 = (q - Y * kImageChunks) * 4, yy = Y - off;
-      uint32_t o[4];
-      if (yy < 0 || yy >= span) {
-        o[0] = o[1] = o[2] = o[3] = kShade;
-      } else {
-        const int i = yy / px;
-        const uint8_t* rowp = atlas + (yy - i * px) * srow;  // sprite row yy % px of sprite 0
-        const uint32_t* brow = base + i * v;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t wc = wcol[w0 + k];
-          const int2 rl = wrel[w0 + k];
-          const int ca = wc & 0xff, cb = (wc >> 8) & 0xff;
-          const uint32_t a = ca == kMarginCol ? kShade : ldu32(rowp + brow[ca] + rl.x);
-          uint32_t b = a;
-          if (cb != ca) b = cb == kMarginCol ? kShade : ldu32(rowp + brow[cb] + rl.y);
-          o[k] = __byte_perm(a, b, wc >> 16);
-        }
+    uint32_t* o = reinterpret_cast<uint32_t*>(out + e * (int64_t)kImageBytes) + w;
+    for (int Y = 0; Y < off; ++Y) o[Y * kImageWords] = kShade;
+    for (int Y = off + span; Y < kImageSide; ++Y) o[Y * kImageWords] = kShade;
+    o += off * kImageWords;
+    for (int i = 0; i < v; ++i) {
+      // rel may be negative (a word starting before its column): signed offsets
+      const uint8_t* pa = atlas + (ma ? 0 : (int64_t)base[i * v + col[0]] + rel[0]);
+      const uint8_t* pb = atlas + (mb ? 0 : (int64_t)base[i * v + col[1]] + rel[1]);
+#pragma unroll 4
+      for (int sy = 0; sy < px; ++sy) {
+        const uint32_t a = ma ? kShade : ldu32(pa);
+        const uint32_t b = two ? (mb ? kShade : ldu32(pb)) : a;
+        *o = __byte_perm(a, b, sel);
+        o += kImageWords;
+        pa += srow;
+        pb += srow;
       }
-      *reinterpret_cast<uint4*>(img + Y * kImageRow + 4 * w0) = make_uint4(o[0], o[1], o[2], o[3]);
     }
   }
 }

@@ -2540,9 +2540,9 @@ int32_t xmg_image_obs(const uint8_t* obs, int64_t n, int32_t view, const uint8_t
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int64_t blocks = std::min<int64_t>(n, (int64_t)sms * 8);
-  image_kernel<<<(unsigned)blocks, kRenderThreads, 0, (cudaStream_t)stream>>>(obs, n, view, kImageSide / view, atlas,
-                                                                              out);
+  const int64_t blocks = std::min<int64_t>(n, (int64_t)sms * 12);
+  image_kernel<<<(unsigned)blocks, kImageWords, 0, (cudaStream_t)stream>>>(obs, n, view, kImageSide / view, atlas,
+                                                                          out);
   return check_launch("image_kernel");
 }
 
