@@ -140,7 +140,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define XMG_TRB(k)
 #endif
 #ifndef XMG_MINB
-#define XMG_MINB 6  // min resident CTAs per SM the register allocation targets
+#define XMG_MINB 8  // min resident CTAs per SM the register allocation targets (64 registers; measured best at C3)
 #endif
 #ifndef XMG_MINB_RARE
 #define XMG_MINB_RARE 6  // step_rare: <= 80 registers, so the next step's kernels fit beside it
@@ -934,8 +934,10 @@ __host__ __device__ inline MainGeo make_main_geo(int V, int maxch, int R) {
   MainGeo g;
   g.ob = 2 * V * V;
   g.stg = 16 * maxch + 16;
-  g.rb = 16 * ((kRowHeader + R + 3) / 4);
-  g.total = (int64_t)kThreads * (g.stg + g.rb) + (int64_t)kWarps * round16(32 * g.ob);
+  // per-lane rule row; after the rule pass the warp's 32 rule rows hold its
+  // 32 observation records (the staging area of the bulk store)
+  g.rb = max(16 * ((kRowHeader + R + 3) / 4), round16(g.ob));
+  g.total = (int64_t)kThreads * (g.stg + g.rb);
   return g;
 }
 
@@ -983,7 +985,7 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
   const bool valid = e < n;
 
   uint8_t* rb_base = smem + kThreads * geo.stg;
-  uint8_t* obs_stage = rb_base + kThreads * geo.rb + warp * round16(32 * geo.ob);
+  uint8_t* obs_stage = rb_base + warp * 32 * geo.rb;  // aliases the warp's rule rows
   View vw;
   vw.g = s.grids + (valid ? e : 0) * (int64_t)HW;
   vw.stage = smem + tid * geo.stg;
@@ -1126,6 +1128,7 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
   // ---- observation: assembled in smem, one TMA bulk store per warp
   // (envs queued for step_rare get theirs rewritten there)
   if (o.obs != nullptr) {
+    __syncwarp();  // every lane is done with its rule row
     if (valid) {
       uint8_t* dst = obs_stage + lane * geo.ob;
       if (d.see_through_walls) {
@@ -2230,10 +2233,18 @@ int launch_rare_k(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, c
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_rare<KMAX>, kThreads, (size_t)geo.total) !=
-          cudaSuccess || per_sm < 1)
-    return fail("step_rare does not fit on an SM");
+  // resident CTAs per SM for this scratch size (cached: the query costs
+  // microseconds of host time per launch, which small batches feel)
+  static thread_local int64_t cached_smem = -1;
+  static thread_local int cached_per_sm = 0;
+  if (cached_smem != geo.total) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per_sm, step_rare<KMAX>, kThreads, (size_t)geo.total) !=
+        cudaSuccess)
+      cached_per_sm = 0;
+    cached_smem = geo.total;
+  }
+  int per_sm = cached_per_sm;
+  if (per_sm < 1) return fail("step_rare does not fit on an SM");
   static int cap = -1;  // XMG_RARE_CTAS: resident step_rare CTAs per SM (tuning)
   if (cap < 0) {
     const char* v = getenv("XMG_RARE_CTAS");
