@@ -145,10 +145,11 @@ def make_workload(name: str, device, n: int, offset: int):
     return params, bm, vec
 
 
-def cpu_reference(name: str, n_sample: int, steps: int, threads: int, budget_s: float = 20.0) -> dict:
+def cpu_reference(name: str, n_sample: int, steps: int, threads: int, budget_s: float = 20.0,
+                  min_s: float = 0.0) -> dict:
     """The oracle port (oracle/xmg_oracle.c, OpenMP) on host cores: the same
     workload restricted to `n_sample` envs, stepping until `steps` steps or
-    `budget_s` seconds.  Returns env-steps/s."""
+    `budget_s` seconds (and for at least `min_s` seconds).  Returns env-steps/s."""
     from helpers import benchmark_file, oracle_from_table
     from oracle import oracle as O
     from paper_2312_12044_b200 import make
@@ -168,9 +169,10 @@ def cpu_reference(name: str, n_sample: int, steps: int, threads: int, budget_s: 
     pk1 = np.array([k[1] for k in keys], np.uint64)
     done, t0 = 0, time.perf_counter()
     chunk = 16
-    while done < steps and time.perf_counter() - t0 < budget_s:
-        ora.rollout_random(pk0, pk1, done, min(chunk, steps - done), compute_obs=True)
-        done += min(chunk, steps - done)
+    while (done < steps or time.perf_counter() - t0 < min_s) and time.perf_counter() - t0 < budget_s:
+        k = chunk if done >= steps else min(chunk, steps - done)
+        ora.rollout_random(pk0, pk1, done, k, compute_obs=True)
+        done += k
     el = time.perf_counter() - t0
     return {"value": n_sample * done / el, "steps": done, "envs": n_sample, "seconds": el}
 
@@ -182,7 +184,9 @@ def run_reference(args):
     env_id, config, n_gpu, desc = WORKLOADS[args.workload]
     threads = os.cpu_count() or 1
     n_sample = min(n_gpu, 1 << 16)
-    r = cpu_reference(args.workload, n_sample, max(args.steps, 1), threads, budget_s=30.0)
+    # a bounded sample: at least the K requested steps, continued up to ~12 s
+    # of host work so the rate is stable (the whole run stays well within minutes)
+    r = cpu_reference(args.workload, n_sample, max(args.steps, 1), threads, budget_s=30.0, min_s=12.0)
     value = r["value"]
     sample = f"{r['envs']} envs x {r['steps']} steps of the {desc} workload ({r['seconds']:.1f} s)"
     line = {
