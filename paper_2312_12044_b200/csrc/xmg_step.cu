@@ -1786,6 +1786,13 @@ __device__ __forceinline__ void release_envs(uint32_t* pending, bool mine, int64
 }
 
 constexpr int kPutBatch = 8;  // PUT_DOWN envs a step_rare warp prefetches together
+#ifndef XMG_RARE_WARPS
+#define XMG_RARE_WARPS 4
+#endif
+constexpr int kRareWarps = XMG_RARE_WARPS;  // warps per step_rare CTA (each warp owns its scratch)
+constexpr int kRareWarpsPerSM = 20;         // resident step_rare warps per SM (see launch_rare_k)
+constexpr int kKeySlots = 16;  // trial keys derived in parallel per warp (resets go in half-warp groups)
+static_assert(kPutBatch <= kKeySlots, "a PUT_DOWN batch derives its finished trials' keys at once");
 
 struct RareGeo {
   int hwp, lg, ws, rbw, keys, pgb, put;
@@ -1801,16 +1808,16 @@ __host__ __device__ inline int log2_buckets(int hw) {  // >= 5, 2^lg >= hw
 __host__ __device__ inline RareGeo make_rare_geo(int H, int W, int R) {
   RareGeo g;
   g.hwp = round16(H * W + 16);
-  g.lg = log2_buckets(H * W);
+  g.lg = 2;  // the bucket area of WarpScratch is unused since the radix-select (keep 16 bytes)
   g.rbw = round16(4 * (kRowHeader + R));
-  g.keys = 32 * (int)sizeof(TrialKeys);
+  g.keys = kKeySlots * (int)sizeof(TrialKeys);
   g.pgb = round16(H * W + 32);                      // one prefetched grid (16-byte chunks, unaligned start)
   g.put = kPutBatch * (g.pgb + g.rbw + 16) + 4 * g.hwp;  // grids | rule rows | state words | candidates
   // per warp: wd: u64[hwp] | fc: u16[hwp] | slot: u16[hwp] | bk: u32[2^lg] | grid: u8[hwp] | misc: 64 u64
   //           | rules | 32 trial keys | env description
   g.ws = 8 * g.hwp + 2 * g.hwp + 2 * g.hwp + 4 * (1 << g.lg) + g.hwp + 512 + g.rbw + g.keys +
          round16((int)sizeof(xmg_env_desc)) + g.put;
-  g.total = (int64_t)kWarps * g.ws;
+  g.total = (int64_t)kRareWarps * g.ws;
   return g;
 }
 
@@ -1846,23 +1853,29 @@ __device__ __forceinline__ void warp_reset_group(const xmg_env_desc& d, const xm
                                                  const uint64_t* reset_keys, int gw = 0) {
   const bool resample = d.resample_tasks && d.scenario == XMG_SCENARIO_XLAND;
   int task = 0;
+  ulonglong2 ek = make_ulonglong2(0, 0);
   if (mine) {
-    const ulonglong2 ek = reinterpret_cast<const ulonglong2*>(reset_keys ? reset_keys : s.rng)[e];
+    ek = reinterpret_cast<const ulonglong2*>(reset_keys ? reset_keys : s.rng)[e];
     task = (int)(reinterpret_cast<const ulonglong2*>(s.agent)[e].y >> 32);
-    derive_trial_keys(ek.x, ek.y, resample, keys + lane);
   }
-  uint32_t m = __ballot_sync(0xffffffffu, mine);
-  __syncwarp();
 #ifdef XMG_TRACE
   XMG_TR(gw, 7, gtime());
 #endif
-  while (m) {
-    const int src = __ffs(m) - 1;
-    m &= m - 1;
-    const int64_t es = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)e, src);
-    const int ts = __shfl_sync(0xffffffffu, task, src);
-    warp_reset_env(d, sd, s, o, wbase, geo, lane, es, keys + src, ts, reset_keys != nullptr,
-                   reinterpret_cast<ResetOut*>(make_scratch(wbase, geo.hwp, geo.lg).misc + 40));
+  // kKeySlots lanes at a time derive their keys in parallel, then the warp
+  // rebuilds those envs one by one
+  for (int half = 0; half < 32; half += kKeySlots) {
+    const bool in = mine && lane >= half && lane < half + kKeySlots;
+    if (in) derive_trial_keys(ek.x, ek.y, resample, keys + (lane - half));
+    uint32_t m = __ballot_sync(0xffffffffu, in);
+    __syncwarp();
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const int64_t es = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)e, src);
+      const int ts = __shfl_sync(0xffffffffu, task, src);
+      warp_reset_env(d, sd, s, o, wbase, geo, lane, es, keys + (src - half), ts, reset_keys != nullptr,
+                     reinterpret_cast<ResetOut*>(make_scratch(wbase, geo.hwp, geo.lg).misc + 40));
+    }
   }
 }
 
@@ -1875,13 +1888,13 @@ __device__ __forceinline__ void warp_reset_group(const xmg_env_desc& d, const xm
 // vecenv.py:205-222), every env [0, n) rebuilt from keys[e] with a FIRST
 // record.
 template <int KMAX>
-__global__ void __launch_bounds__(kThreads, XMG_MINB_RARE) step_rare(const xmg_env_desc d, const xmg_state s,
+__global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRareWarps) step_rare(const xmg_env_desc d, const xmg_state s,
                                                                      const xmg_out o, const uint64_t* reset_keys,
                                                                      const uint32_t* abort_flag, uint32_t epoch,
                                                                      int64_t n, int track) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gw = blockIdx.x * kWarps + warp, tw = gridDim.x * kWarps;
+  const int gw = blockIdx.x * kRareWarps + warp, tw = gridDim.x * kRareWarps;
 #ifdef XMG_TRACE
   const unsigned long long t_start = gtime();
   XMG_TR(gw, 0, t_start);
@@ -2238,24 +2251,32 @@ int launch_rare_k(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, c
   static thread_local int64_t cached_smem = -1;
   static thread_local int cached_per_sm = 0;
   if (cached_smem != geo.total) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per_sm, step_rare<KMAX>, kThreads, (size_t)geo.total) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per_sm, step_rare<KMAX>, kRareWarps * 32,
+                                                      (size_t)geo.total) !=
         cudaSuccess)
       cached_per_sm = 0;
     cached_smem = geo.total;
   }
   int per_sm = cached_per_sm;
   if (per_sm < 1) return fail("step_rare does not fit on an SM");
-  static int cap = -1;  // XMG_RARE_CTAS: resident step_rare CTAs per SM (tuning)
+  // At most ~20 resident step_rare warps per SM: the kernel overlaps the next
+  // step's step_main, and beyond that it crowds step_main's CTAs out
+  // (measured at C3 / DoorKey: 20 warps 80 us/step, 21-24 warps 89-96 us).
+  // XMG_RARE_CTAS overrides the CTA count per SM (tuning).
+  static int cap = -1;
   if (cap < 0) {
     const char* v = getenv("XMG_RARE_CTAS");
-    cap = v ? atoi(v) : 0;
+    cap = v ? atoi(v) : kRareWarpsPerSM / kRareWarps;
   }
   if (cap > 0 && per_sm > cap) per_sm = cap;
-  int64_t blocks = (int64_t)per_sm * sms / 32 * 32;
-  const int64_t need = ((n + 4 * 64 - 1) / (4 * 64) + 31) / 32 * 32;  // <= one warp per 64 envs
+  // a multiple of kQueues warps, so every sub-queue gets the same number of warps
+  constexpr int64_t unit = kQueues / kRareWarps;
+  int64_t blocks = (int64_t)per_sm * sms / unit * unit;
+  const int64_t need = ((n + kRareWarps * 64 - 1) / (kRareWarps * 64) + unit - 1) / unit * unit;  // <= a warp / 64 envs
   if (blocks > need) blocks = need;
-  if (blocks < 32) blocks = 32;
-  step_rare<KMAX><<<(unsigned)blocks, kThreads, (size_t)geo.total, st>>>(*d, *s, *o, keys, flag, epoch, n, track);
+  if (blocks < unit) blocks = unit;
+  step_rare<KMAX><<<(unsigned)blocks, kRareWarps * 32, (size_t)geo.total, st>>>(*d, *s, *o, keys, flag, epoch, n,
+                                                                                track);
   return check_launch("step_rare");
 }
 
