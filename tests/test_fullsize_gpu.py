@@ -1,0 +1,77 @@
+"""GPU parity at BASELINE.json's full sizes (SURVEY.md 8(c) "Large N").
+
+C3 (XLand-R4-13x13 medium, 2^20 envs) and C4's per-GPU shard (R9-25x25 high,
+2^19 envs) are too large for the oracle, so per-env trajectories being
+batch-invariant (ref tests/test_acceptance.py:494-517) is used: slices at the
+start, middle and end of the full batch are replayed by the oracle from their
+own keys (split_batch offsets), task rows and policy streams, every step, across
+the synchronized budget reset.  Size-independent properties cover the whole
+batch: the fused rollout reaches the identical full state, and the in-kernel
+episode statistics equal the sums over the per-step records.
+"""
+import numpy as np
+import pytest
+import torch
+
+from .helpers import benchmark_file, oracle_from_table
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("env_name,config,n,steps", [
+    ("XLand-MiniGrid-R4-13x13", "medium", 1 << 20, 520),
+    ("XLand-MiniGrid-R9-25x25", "high", 1 << 19, 300),
+])
+def test_full_batch_slices_vs_oracle(env_name, config, n, steps):
+    from oracle import oracle as O
+    from paper_2312_12044_b200 import VecEnv, key_from_seed, load_benchmark, make, policy_keys, random_actions
+    _, params = make(env_name)
+    bm = load_benchmark(benchmark_file(config))
+    table = bm.task_table()
+    vec = VecEnv(params, n, bm)
+    stats = vec.enable_stats()
+    root, pol = key_from_seed(0), key_from_seed(1)
+    ts = vec.reset(root)
+    width = 256
+    offs = [0, n // 2 + 77, n - width]
+    oras = []
+    for off in offs:
+        ids = (np.arange(off, off + width) % table.num_tasks).astype(np.int64)
+        ora = oracle_from_table(params, table, ids)
+        k0, k1 = O.split_batch((root.hi, root.lo), width, offset=off)
+        obs0 = ora.reset_with_keys(k0, k1)
+        np.testing.assert_array_equal(ts.observations[off:off + width].cpu().numpy(), obs0)
+        keys = [O.fold_in((pol.hi, pol.lo), off + i) for i in range(width)]
+        pk0 = np.array([k[0] for k in keys], np.uint64)
+        pk1 = np.array([k[1] for k in keys], np.uint64)
+        oras.append((off, ora, O.random_actions(pk0, pk1, 0, steps)))
+    pk = policy_keys(pol, n, device=vec.device)
+    acts = random_actions(pk, 0, steps)
+    rew_sum = torch.zeros((), dtype=torch.float64, device=vec.device)
+    last_sum = torch.zeros((), dtype=torch.float64, device=vec.device)
+    for t in range(steps):
+        ts = vec.step(acts[t])
+        rew_sum += ts.rewards.double().sum()
+        last_sum += (ts.step_types == 2).double().sum()
+        for off, ora, a in oras:
+            o, r, d, s = ora.step(a[t])
+            sl = slice(off, off + width)
+            np.testing.assert_array_equal(ts.step_types[sl].cpu().numpy(), s, err_msg=f"{off} t={t}")
+            np.testing.assert_array_equal(ts.rewards[sl].cpu().numpy(), r.astype(np.float32))
+            np.testing.assert_array_equal(ts.observations[sl].cpu().numpy(), o, err_msg=f"{off} t={t}")
+    vec.check()
+    for off, ora, _ in oras:
+        sl = slice(off, off + width)
+        np.testing.assert_array_equal(vec.grids[sl].cpu().numpy(), ora.grids)
+        np.testing.assert_array_equal(vec.rng[sl].cpu().numpy().view(np.uint64), ora.rng)
+    tot = stats.sum(0)
+    assert float(tot[1]) == float(last_sum)                       # finished trials
+    assert abs(float(tot[0]) - float(rew_sum)) <= 1e-6 * max(1.0, float(rew_sum))
+
+    # the fused rollout from the same start reaches the identical full state
+    roll = VecEnv(params, n, bm)
+    roll.reset(root)
+    roll.rollout(steps, policy_keys=pk, record=())
+    assert torch.equal(roll.grids, vec.grids)
+    assert torch.equal(roll.agent, vec.agent)
+    assert torch.equal(roll.rng, vec.rng)
