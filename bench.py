@@ -362,6 +362,56 @@ def run_ours(args):
                "api": "VecEnv.step with pinned host actions in, full VecTimeStep out (double-buffered)"}
         del vec3
 
+    # ---- the same K steps through VecEnv.steps (xmg_steps: one host call per
+    # block of 64 steps, no per-step host round trip; records written to a
+    # reused (64, n) trajectory buffer)
+    block = None
+    if not args.no_block and (n * 2 * params.view_size ** 2) % 16 == 0:
+        params5, _, vec5 = make_workload(args.workload, dev, n, offset)
+        vec5.reset(key_from_seed(0))
+        rec_bytes = n * (2 * params.view_size ** 2 + 9)
+        bk = int(max(1, min(64, 8e9 // rec_bytes)))  # record buffer <= 8 GB
+        t = 0
+        while t < W + pre:
+            k = min(bk, W + pre - t)
+            vec5.steps(actions[t:t + k], validate=False)
+            t += k
+        buf = vec5.steps(actions[t:t + 1], validate=False)  # allocate a 1-step record, reused below
+        from paper_2312_12044_b200.vecenv import Trajectory
+        v = params5.view_size
+        traj = Trajectory(torch.empty((bk, n, v, v, 2), dtype=torch.uint8, device=dev),
+                          torch.empty((bk, n), dtype=torch.float32, device=dev),
+                          torch.empty((bk, n), dtype=torch.float32, device=dev),
+                          torch.empty((bk, n), dtype=torch.int8, device=dev))
+        del buf
+        vec5.reset(key_from_seed(0))
+        t = 0
+        while t < W + pre:
+            k = min(bk, W + pre - t)
+            vec5.steps(actions[t:t + k], validate=False, out=traj if k == bk else None)
+            t += k
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        while t < total:
+            k = min(bk, total - t)
+            vec5.steps(actions[t:t + k], validate=False, out=traj if k == bk else None)
+            t += k
+        b1.record(stream)
+        torch.cuda.synchronize(dev)
+        bms = b0.elapsed_time(b1)
+        tb = torch.tensor([bms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+        bms = float(tb.item())
+        block = {"value": n * world * K / (bms / 1e3), "unit": "env-steps/s", "ms_per_step": bms / K,
+                 "block_steps": bk,
+                 "note": "VecEnv.steps: the same K steps and actions as the timed window, block_steps per host call "
+                         "(xmg_steps), bit-identical to step() (tests/test_rollout_gpu.py)"}
+        del traj, vec5
+
     # ---- fused rollout: the same K steps (same actions,
     # same phase) as xmg_rollout launches of `chunk` steps each, state on chip
     # within a launch; per env-step only the trajectory record leaves the SM.
@@ -370,7 +420,7 @@ def run_ours(args):
         params4, _, vec4 = make_workload(args.workload, dev, n, offset)
         vec4.reset(key_from_seed(0))
         vec4.enable_stats()
-        chunk = args.fused_chunk
+        chunk = int(max(1, min(args.fused_chunk, 8e9 // (n * (2 * params.view_size ** 2 + 9)))))
         if W + pre:
             vec4.rollout(W + pre, policy_keys=pkeys, t0=0, record=())
         v = params4.view_size
@@ -462,7 +512,7 @@ def run_ours(args):
                        "l2": "inputs larger than L2" if n * params.height * params.width > 126e6
                              else "state resident in L2 (small workload)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "fused_rollout": fused, "image_obs": image,
+            "steps_block": block, "fused_rollout": fused, "image_obs": image,
             "clocks": clocks.summary(),
             "episode_stats": {"return_sum": float(tot[0]), "trials": float(tot[1]), "length_sum": float(tot[2])},
         }
@@ -484,6 +534,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fused", action="store_true")
     ap.add_argument("--no-image", action="store_true")
+    ap.add_argument("--no-block", action="store_true")
     ap.add_argument("--fused-chunk", type=int, default=32)
     args = ap.parse_args()
     if args.warmup < 3:

@@ -163,6 +163,16 @@ int32_t xmg_validate_actions(const void* actions, int32_t action_dtype, int64_t 
 int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* actions, int32_t action_dtype,
                  int64_t n, const xmg_out* out, const uint32_t* abort_flag, uint32_t epoch, void* stream);
 
+/* `steps` consecutive xmg_step calls issued from one host call (no per-step
+ * host round trip: the path for batches too small to hide ~20-30 us of
+ * Python + launch overhead per step).  actions [steps][n] must already be
+ * valid (no device validation: the caller checks the block once); step k
+ * uses epoch epoch0 + k + 1 and writes record k of traj: obs (nullable)
+ * [steps][n][v][v][2] (n*2*v*v a multiple of 16), reward / discount /
+ * step_type [steps][n] (required), stats as in xmg_out. */
+int32_t xmg_steps(const xmg_env_desc* desc, const xmg_state* state, const void* actions, int32_t action_dtype,
+                  int64_t steps, int64_t n, const xmg_out* traj, uint32_t epoch0, void* stream);
+
 /* Profiling hook: while enabled, every xmg_step records CUDA events around
  * its two kernels (this serialises them: standalone per-kernel times, for
  * rooflines only).  xmg_profile_read synchronises, returns the summed

@@ -2504,6 +2504,33 @@ int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* a
   return rc;
 }
 
+int32_t xmg_steps(const xmg_env_desc* desc, const xmg_state* state, const void* actions, int32_t action_dtype,
+                  int64_t steps, int64_t n, const xmg_out* traj, uint32_t epoch0, void* stream) {
+  if (validate_desc(desc, state, n)) return -1;
+  if (!traj || !actions) return fail("null traj/actions");
+  if (!traj->reward || !traj->discount || !traj->step_type) return fail("reward / discount / step_type are required");
+  if (action_dtype < 0 || action_dtype > 2) return fail("unknown action dtype");
+  if (steps < 0) return fail("steps must be >= 0");
+  const int64_t ob = 2LL * desc->view_size * desc->view_size;
+  if ((reinterpret_cast<uintptr_t>(state->grids) & 15) || (reinterpret_cast<uintptr_t>(state->agent) & 15) ||
+      (traj->obs && (((reinterpret_cast<uintptr_t>(traj->obs)) & 15) || ((n * ob) & 15))))
+    return fail("grids / agent / obs buffers must be 16-byte aligned (and n*2*v*v a multiple of 16 with obs)");
+  const int asz = action_dtype == XMG_ACT_U8 ? 1 : action_dtype == XMG_ACT_I32 ? 4 : 8;
+  const int track = use_stream(desc) ? 0 : 1;
+  for (int64_t k = 0; k < steps; ++k) {
+    xmg_out o = *traj;
+    if (o.obs) o.obs += k * n * ob;
+    if (o.reward) o.reward += k * n;
+    if (o.discount) o.discount += k * n;
+    if (o.step_type) o.step_type += k * n;
+    const uint32_t ep = epoch0 + (uint32_t)k + 1u;
+    const void* a = reinterpret_cast<const uint8_t*>(actions) + k * n * asz;
+    if (dispatch_main(desc, state, &o, a, action_dtype, nullptr, ep, n, (cudaStream_t)stream)) return -1;
+    if (launch_rare(desc, state, &o, nullptr, nullptr, ep, n, track, (cudaStream_t)stream)) return -1;
+  }
+  return 0;
+}
+
 int32_t xmg_profile(int32_t enable) {
   std::lock_guard<std::mutex> lk(g_prof.mu);
   g_prof.on = enable != 0;

@@ -378,6 +378,44 @@ class VecEnv:
             self.check()
         return VecTimeStep(*outs)
 
+    # -- many steps per host call
+    def steps(self, actions: torch.Tensor, compute_obs: bool = True, validate: bool = True,
+              out: Trajectory | None = None) -> Trajectory:
+        """``actions.shape[0]`` consecutive ``step`` calls issued by one library
+        call (``xmg_steps``): no per-step host round trip, for batches too
+        small to hide the per-call overhead.  Record k of the returned
+        Trajectory is what ``step`` k would return.  ``validate`` checks the
+        whole block once, before anything is launched (ref vecenv.py:297-301,
+        one host sync)."""
+        n, v, dev = self.num_envs, self.params.view_size, self.device
+        if not isinstance(actions, torch.Tensor):
+            actions = torch.as_tensor(np.asarray(actions))
+        if actions.dim() != 2 or actions.shape[1] != n:
+            raise InvalidAction(f"expected (K, {n}) actions, got shape {tuple(actions.shape)}")
+        k = actions.shape[0]
+        if compute_obs and (n * 2 * v * v) % 16:
+            raise ValueError("steps(): with observations, num_envs * 2 * v * v must be a multiple of 16 "
+                             "(16-byte aligned records); use step() or rollout()")
+        if validate and bool(((actions < 0) | (actions >= 6)).any()):
+            raise InvalidAction("action outside [0, 5]")
+        actions = actions.to(dev)
+        dt = _ACT_DTYPES.get(actions.dtype)
+        if dt is None:
+            actions, dt = actions.to(torch.int64), _lib.ACT_I64
+        actions = actions.contiguous()
+        if out is None:
+            out = Trajectory(torch.empty((k, n, v, v, 2), dtype=torch.uint8, device=dev) if compute_obs else None,
+                             torch.empty((k, n), dtype=torch.float32, device=dev),
+                             torch.empty((k, n), dtype=torch.float32, device=dev),
+                             torch.empty((k, n), dtype=torch.int8, device=dev))
+        o = _lib.Out(_ptr(out.observations), _ptr(out.rewards), _ptr(out.discounts), _ptr(out.step_types),
+                     _ptr(self.stats))
+        _lib.check(_lib.lib().xmg_steps(self._desc_ref, self._state_ref, actions.data_ptr(), dt, k, n, C.byref(o),
+                                        self.epoch & 0xFFFFFFFF, _stream(dev)), "xmg_steps")
+        self.epoch += k
+        self.launches += 2 * k
+        return out
+
     # -- fused rollout (SURVEY.md 8(f)#3)
     def rollout(self, steps: int, policy_keys: torch.Tensor | None = None, actions: torch.Tensor | None = None,
                 t0: int = 0, record: Sequence[str] = ("observations", "rewards", "discounts", "step_types"),

@@ -7,7 +7,7 @@ out=gpurun_out/sweep.jsonl
 for wl in doorkey c3; do
   for p in 10 12 14 16 18 20 22 24; do
     n=$((1 << p))
-    timeout 600 python bench.py --workload $wl --envs $n --steps 512 --warmup 4 --no-e2e --no-cpu --no-fused \
+    timeout 600 python bench.py --workload $wl --envs $n --steps 512 --warmup 4 --no-e2e --no-cpu \
       --no-image 2>> gpurun_out/sweep.err | tail -1 >> $out
     echo "$wl 2^$p rc=$?"
   done
