@@ -19,10 +19,14 @@
 // or a caller-supplied [T][n] u8 tensor.  The result is bit-identical to T
 // calls of xmg_step with the same actions (tests/test_rollout_gpu.py).
 
-constexpr int kRollWarps = 4;
-#ifndef XMG_ROLL_MINB
-#define XMG_ROLL_MINB 4  // resident CTAs per SM the register allocation targets (<= 128 registers)
+#ifndef XMG_ROLL_WARPS
+#define XMG_ROLL_WARPS 4  // warps per CTA (each owns 32 envs and its own scratch)
 #endif
+#ifndef XMG_ROLL_MINB
+#define XMG_ROLL_MINB 4  // resident CTAs per SM the register allocation targets (4 x 4 warps: <= 128 registers)
+#endif
+constexpr int kRollWarps = XMG_ROLL_WARPS;
+constexpr int kRollKeySlots = 16;  // trial keys derived in parallel (resets go in half-warp groups)
 constexpr int kRollLg = 2;  // unused bucket area of WarpScratch (4 << kRollLg bytes)
 
 struct RollGeo {
@@ -33,20 +37,21 @@ struct RollGeo {
 __host__ __device__ inline RollGeo make_roll_geo(int H, int W, int V, int R) {
   RollGeo g;
   g.hw = H * W;
-  g.grids = round16(32 * g.hw + 16);            // the 32 env grids (+ slack for 16-byte reads)
+  g.grids = round16(32 * g.hw);                 // the 32 env grids
   g.rbw = 16 * ((kRowHeader + R + 3) / 4);      // one lane's task row header + rules
   g.rules = R > 0 ? 32 * g.rbw : 0;
   g.ob = 2 * V * V;
-  // double-buffered observation records; between the bulk stores of two
-  // steps the same bytes hold the 32 lanes' trial keys of the resets
-  g.obs = max(2 * round16(32 * g.ob), round16(32 * (int)sizeof(TrialKeys)));
+  // double-buffered observation records (waiting for the previous step's bulk
+  // store to drain costs ~25% with one buffer); between the bulk stores of two
+  // steps the same bytes hold the trial keys of the resets
+  g.obs = max(2 * round16(32 * g.ob), round16(kRollKeySlots * (int)sizeof(TrialKeys)));
   g.hwp = round16(g.hw + 16);
   // WarpScratch of warp_build: wd u64[hwp] | fc u16[hwp] | slot u16[hwp] | bk | grid u8[hwp] | misc 64 u64;
   // the PUT_DOWN candidate list (u32[hw]) reuses wd (never live at once)
   g.scratch = 12 * g.hwp + (4 << kRollLg) + g.hwp + 512;
-  g.desc = round16((int)sizeof(xmg_env_desc));
-  g.warp_bytes = g.grids + g.rules + g.obs + g.scratch + g.desc;
-  g.total = (int64_t)kRollWarps * g.warp_bytes;
+  g.desc = round16((int)sizeof(xmg_env_desc));  // one copy per CTA
+  g.warp_bytes = g.grids + g.rules + g.obs + g.scratch;
+  g.total = (int64_t)kRollWarps * g.warp_bytes + g.desc;
   return g;
 }
 
@@ -74,7 +79,7 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
   uint8_t* scratch = obs_s + geo.obs;
   uint32_t* cand = reinterpret_cast<uint32_t*>(scratch);      // aliases wd
   TrialKeys* keys = reinterpret_cast<TrialKeys*>(obs_s);      // aliases the observation buffers
-  xmg_env_desc* sdesc = reinterpret_cast<xmg_env_desc*>(scratch + geo.scratch);
+  xmg_env_desc* sdesc = reinterpret_cast<xmg_env_desc*>(smem + kRollWarps * geo.warp_bytes);
   ResetOut* rout = reinterpret_cast<ResetOut*>(make_scratch(scratch, geo.hwp, kRollLg).misc + 40);
 
   const int nvalid = (int)min((int64_t)32, n - e0);
@@ -207,13 +212,16 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
     if (lm) {
       if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // obs buffers free
       __syncwarp();
-      if (last) derive_trial_keys(rk.x, rk.y, resample, keys + lane);
+      for (int half = 0; half < 32; half += kRollKeySlots) {
+      uint32_t hm = lm & (kRollKeySlots == 32 ? 0xffffffffu : (((1u << kRollKeySlots) - 1u) << half));
+      if (!hm) continue;
+      if ((hm >> lane) & 1) derive_trial_keys(rk.x, rk.y, resample, keys + (lane - half));
       __syncwarp();
-      for (; lm; lm &= lm - 1) {
-        const int src = __ffs(lm) - 1;
+      for (; hm; hm &= hm - 1) {
+        const int src = __ffs(hm) - 1;
         const int tk = __shfl_sync(0xffffffffu, task, src);
         const uint32_t g_in = xland ? d.task_rows[(int64_t)tk * d.row_words] : 0u;
-        warp_build(sdesc, scratch, geo.hwp, kRollLg, lane, keys + src, tk, g_in, grids + src * HW, rout);
+        warp_build(sdesc, scratch, geo.hwp, kRollLg, lane, keys + (src - half), tk, g_in, grids + src * HW, rout);
         const ResetOut ro = *rout;
         if (lane == src) {
           r = ro.r;
@@ -227,6 +235,7 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
         }
         if (resample) load_row(src, ro.task);
         __syncwarp();
+      }
       }
     }
     // ---- observation of the next playable state: staged, one bulk store per warp
