@@ -2,8 +2,12 @@
 
 Host-side mirror of the reference ``rulegrid`` API for the batched step
 (make / EnvParams / VecEnv / load_benchmark / sample_ruleset / keys) over the
-sm_100a kernels of libxmg.so (C ABI: include/xmg.h).  ``xminigrid``-style
-aliases are provided for code written against the paper's names.
+sm_100a kernels of libxmg.so (C ABI: include/xmg.h).  The paper's
+``xminigrid`` names (make / GymAutoResetWrapper / load_benchmark / batched
+reset and step) are in :mod:`paper_2312_12044_b200.xminigrid`; the fused
+rollout is ``VecEnv.rollout``, observation images are in
+:mod:`paper_2312_12044_b200.render`, the JSON-lines server in
+:mod:`paper_2312_12044_b200.bridge`.
 """
 
 from ._lib import NativeLibraryError, build

@@ -50,6 +50,12 @@ class EnvParams:
         if self.scenario not in SCENARIO_NAMES:
             raise ValueError(f"unknown scenario {self.scenario!r}")
 
+    def replace(self, **changes) -> "EnvParams":
+        """Immutable update, ``env_params.replace(ruleset=...)`` as in the
+        paper's JAX API (dataclasses.replace)."""
+        from dataclasses import replace
+        return replace(self, **changes)
+
     @property
     def step_budget(self) -> int:
         return self.max_steps if self.max_steps is not None else 3 * self.height * self.width
