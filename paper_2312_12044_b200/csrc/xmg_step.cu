@@ -182,20 +182,30 @@ struct View {
 };
 
 // Bounding box of the view window for pose (r, c, d), extended by `ext`
-// cells ahead (ref:vecenv.py:77-92 / ref:observation.py:28-43), clipped.
-__device__ __forceinline__ void window_span(int r, int c, int d, int ext, int H, int W, int V, int& lo, int& hi) {
+// cells ahead and `back` cells behind (ref:vecenv.py:77-92 /
+// ref:observation.py:28-43), clipped.
+__device__ __forceinline__ void window_span(int r, int c, int d, int ext, int back, int H, int W, int V, int& lo,
+                                            int& hi) {
   const int h = V / 2;
   int r0, r1, c0, c1;
   switch (d) {
-    case 0: r0 = r - (V - 1) - ext; r1 = r; c0 = c - h; c1 = c + h; break;
-    case 1: r0 = r - h; r1 = r + h; c0 = c; c1 = c + (V - 1) + ext; break;
-    case 2: r0 = r; r1 = r + (V - 1) + ext; c0 = c - h; c1 = c + h; break;
-    default: r0 = r - h; r1 = r + h; c0 = c - (V - 1) - ext; c1 = c; break;
+    case 0: r0 = r - (V - 1) - ext; r1 = r + back; c0 = c - h; c1 = c + h; break;
+    case 1: r0 = r - h; r1 = r + h; c0 = c - back; c1 = c + (V - 1) + ext; break;
+    case 2: r0 = r - back; r1 = r + (V - 1) + ext; c0 = c - h; c1 = c + h; break;
+    default: r0 = r - h; r1 = r + h; c0 = c - (V - 1) - ext; c1 = c + back; break;
   }
   r0 = max(r0, 0); c0 = max(c0, 0); r1 = min(r1, H - 1); c1 = min(c1, W - 1);
   lo = r0 * W + c0;
   hi = r1 * W + c1 + 1;
 }
+
+// The staged window of step_main: it always covers every cell the step reads
+// (the view of the post-action pose, one cell further ahead for MOVE and one
+// behind for PICK_UP, whose agent-relative rules see all four neighbours),
+// so reads need no range check; writes go through to the grid in HBM.
+struct WView : View {
+  __device__ __forceinline__ uint8_t rd(int f) const { return stage[f - sbase]; }
+};
 
 // Stage grid bytes [lo, hi) of this thread's env with 16-byte cp.async
 // chunks (aligned on the global address; the grid buffer is padded).
@@ -986,7 +996,7 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
 
   uint8_t* rb_base = smem + kThreads * geo.stg;
   uint8_t* obs_stage = rb_base + warp * 32 * geo.rb;  // aliases the warp's rule rows
-  View vw;
+  WView vw;
   vw.g = s.grids + (valid ? e : 0) * (int64_t)HW;
   vw.stage = smem + tid * geo.stg;
   vw.sbase = vw.slo = vw.shi = 0;
@@ -1034,7 +1044,7 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
     const int nd = act == 1 ? ((dir + 3) & 3) : (act == 2 ? ((dir + 1) & 3) : dir);
     if (!FULL) {
       int lo, hi;
-      window_span(r, c, nd, act == 0 ? 1 : 0, H, W, V, lo, hi);
+      window_span(r, c, nd, act == 0 ? 1 : 0, act == 3 ? 1 : 0, H, W, V, lo, hi);
       stage_issue<MAXCH>(vw, lo, hi, HW);
     }
     const bool rules_needed = R > 0 && (act == 0 || act == 3);
@@ -1049,7 +1059,8 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
     const int tr = r + dir_dr(dir), tc = c + dir_dc(dir);
     const bool inside = tr >= 0 && tr < H && tc >= 0 && tc < W;
     const int tflat = tr * W + tc;
-    const int tcode = inside ? vw.rd(tflat) : 0, tt = tcode >> 4;
+    // (turns stage the new facing's window, which need not hold the old target)
+    const int tcode = (inside && act != 1 && act != 2) ? vw.rd(tflat) : 0, tt = tcode >> 4;
     // select-based: lanes with different actions stay converged
     const bool mv = act == 0 && inside && ((kWalkable >> tt) & 1);
     const bool pk = act == 3 && inside && pocket == 0 && ((kPickable >> tt) & 1);
