@@ -347,7 +347,7 @@ __device__ __forceinline__ void obs_see(const uint8_t* stage, int sbase, uint8_t
   const bool odd = (reinterpret_cast<uintptr_t>(dst) & 2) != 0;
   if constexpr (VV != 0) {
     constexpr int NC = VV * VV;
-    uint32_t v[NC];
+    uint32_t cd[NC + 1];  // entity codes, view cell order (+ a zero pad)
 #pragma unroll
     for (int i = 0; i < VV; ++i) {
       const bool vi = (mi >> i) & 1;
@@ -356,14 +356,27 @@ __device__ __forceinline__ void obs_see(const uint8_t* stage, int sbase, uint8_t
       for (int j = 0; j < VV; ++j) {
         uint32_t code = 0;
         if (vi && ((mj >> j) & 1)) code = pi[j * dj];
-        v[i * VV + j] = ((code * 0x1001u) >> 4) & 0x0F0Fu;
+        cd[i * VV + j] = code;
       }
     }
-    *reinterpret_cast<uint16_t*>(dst + (odd ? 0 : 2 * (NC - 1))) = (uint16_t)(odd ? v[0] : v[NC - 1]);
+    cd[NC] = 0;
+    // two cells -> one (tile, color, tile, color) word: pack the codes, split
+    // nibbles, interleave (3 byte_perms + 3 ALU ops per pair)
+    auto pair = [](uint32_t a, uint32_t b) {
+      const uint32_t x = __byte_perm(a, b, 0x0040);
+      return __byte_perm((x >> 4) & 0x0F0Fu, x & 0x0F0Fu, 0x5140);
+    };
+    uint32_t ev[(NC + 1) / 2];  // even-aligned words: cells (2k, 2k+1)
+#pragma unroll
+    for (int k = 0; k < (NC + 1) / 2; ++k) ev[k] = pair(cd[2 * k], cd[2 * k + 1]);
+    // an odd-offset record leads with cell 0 as a u16, then words of cells
+    // (2k+1, 2k+2) = the even words shifted by one cell; an even one ends
+    // with cell NC-1 as a u16
+    *reinterpret_cast<uint16_t*>(dst + (odd ? 0 : 2 * (NC - 1))) =
+        (uint16_t)(odd ? ev[0] : ev[(NC - 1) / 2]);
     uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + (odd ? 2 : 0));
 #pragma unroll
-    for (int k = 0; k < (NC - 1) / 2; ++k)
-      d32[k] = odd ? (v[2 * k + 1] | (v[2 * k + 2] << 16)) : (v[2 * k] | (v[2 * k + 1] << 16));
+    for (int k = 0; k < (NC - 1) / 2; ++k) d32[k] = odd ? __funnelshift_r(ev[k], ev[k + 1], 16) : ev[k];
   } else {
     uint16_t* o = reinterpret_cast<uint16_t*>(dst);
     for (int i = 0; i < V; ++i)
