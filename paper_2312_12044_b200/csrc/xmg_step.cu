@@ -1,31 +1,28 @@
 // xmg_step.cu — B200 (sm_100a) batched XLand-MiniGrid environment step.
 //
-// Implements the C ABI declared in include/xmg.h.  The hot path is ONE fused
-// kernel (`step_kernel`) that replaces the reference's NumPy VecEnv.step
-// (/root/reference/pkg/src/rulegrid/vecenv.py:295-364, cited as ref:<file>:<line>):
+// Implements the C ABI declared in include/xmg.h; the reference is the NumPy
+// VecEnv.step of /root/reference/pkg/src/rulegrid/vecenv.py:295-364 (cited as
+// ref:<file>:<line>):
 //   action (:306-342) -> rules (:368-433) -> goal (:435-477) -> reward /
 //   discount / step type (:351-357) -> auto-reset of finished trials
 //   (:359-361 -> :224-291) -> egocentric observation (:481-500).
 //
-// Mapping:
-//  * one thread per env, 128 envs per CTA, no CTA-wide barrier after the
-//    kernel prologue;
-//  * per env one 16-byte state word (pose, pocket, step count, goal, task)
-//    read with a single coalesced 128-bit load;
-//  * the grid bytes the step needs (the view window of the post-action pose,
-//    extended one cell ahead for MOVE so the target cell is inside) are
-//    copied global->shared with cp.async (LDGSTS) in 16-byte aligned chunks,
-//    together with a speculative copy of the env's rule row (L2-resident task
-//    table); the rest of the grid is never read on the common path;
-//  * rare work is warp-cooperative: PUT_DOWN events (the only events that
-//    gate grid-wide predicates) are resolved by the whole warp with ballot
-//    scans, and every env whose trial ends is rebuilt by its whole warp
-//    (Philox draws spread over the lanes; the reference's stable argsort
-//    replaced by a bucket counting sort on the uniform draw words);
-//  * observations are assembled in shared memory in the reference layout
-//    (n, v, v, 2) and leave each warp as one TMA bulk store (cp.async.bulk).
-// Nothing here is a dense contraction, so no tensor cores are used; the
-// kernel is bounded by HBM bytes per env-step (roofline).
+// Kernels:
+//  * step_main — one thread per env, 128 envs per CTA: one 16-byte state word
+//    per env, the grid bytes of the view window staged global->shared with
+//    16-byte cp.async, the action, MOVE / PICK_UP rules and goals per lane
+//    (select-based), counters and reward, the observation assembled in shared
+//    memory and stored with one TMA bulk copy per warp; PUT_DOWN events and
+//    finished trials are appended to work queues;
+//  * step_rare — one warp per queued env: PUT_DOWN rule passes (speculative
+//    per-slot evaluation) and trial rebuilds (Philox draws spread over lanes,
+//    the reference's stable argsort replaced by a warp radix-select), launched
+//    so that the next step's step_main overlaps it (programmatic dependent
+//    launch, per-chunk release);
+//  * rollout_kernel (xmg_rollout.cuh) — T steps fused, state on chip;
+//  * sprite_kernel / image_kernel (xmg_render.cuh) — 224x224 observation images.
+// Nothing here is a dense contraction, so no tensor cores are used; the step
+// is bounded by HBM bytes per env-step (roofline).
 
 #include <cuda_runtime.h>
 
@@ -235,7 +232,7 @@ __device__ __forceinline__ void stage_issue(View& vw, int lo, int hi, int HW) {
 // they are resolved per lane from the staged window.  Every grid-wide
 // predicate (TILE_NEAR* rules, TILE_* goals) is gated on PUT_DOWN only
 // (ref:rules.py:60-72, ref:goals.py:268-283): PUT_DOWN events are queued and
-// resolved by step_rare (warp_put_event).
+// resolved by step_rare (warp_put_env).
 // The agent's four neighbour cells in NEAR_OFFSETS order (up, left, right,
 // down; ref:rules.py:76), 0x100 when off the grid, plus their flat indices.
 struct Nbrs {
@@ -876,12 +873,10 @@ __host__ __device__ inline int count_index(uint32_t parity, int kind, int q) {
 }
 constexpr uint32_t kQPut = 1u << 31, kQReset = 1u << 30, kQEnv = (1u << 30) - 1;
 
-// capacity of one sub-queue: every env of the CTAs (128 envs, step_main) or
-// warp chunks (32 envs, step_stream) feeding it
+// capacity of one sub-queue: every env of the step_main CTAs (128 envs each) feeding it
 __host__ __device__ inline int64_t queue_cap(int64_t n) {
-  const int64_t blocks = (n + kThreads - 1) / kThreads, chunks = (n + 31) / 32;
-  const int64_t a = (blocks + kQueues - 1) / kQueues * kThreads, b = (chunks + kQueues - 1) / kQueues * 32;
-  return a > b ? a : b;
+  const int64_t blocks = (n + kThreads - 1) / kThreads;
+  return (blocks + kQueues - 1) / kQueues * kThreads;
 }
 
 // Entry slots of sub-queue (parity, kind, q): double-buffered like the counts,
@@ -1209,439 +1204,6 @@ __device__ __noinline__ void warp_obs(const uint8_t* G, uint8_t* gobs, int lane,
                                       int V, bool see) {
   for (int cell = lane; cell < V * V; cell += 32)
     reinterpret_cast<uint16_t*>(gobs)[cell] = obs_cell(G, r, c, d, H, W, V, cell, see);
-}
-
-// ------------------------------------------------------- bit-parallel grids
-// Cell p of an env's grid is bit (p & 31) of word (p >> 5); lane k of a warp
-// holds word k of a bitmap (lanes >= K hold 0).  One ballot builds a word,
-// neighbour relations are multiword shifts done with shuffles.
-__device__ __forceinline__ uint32_t shl_cells(uint32_t x, int s, int lane) {  // bit p <- bit p - s
-  const int q = s >> 5, r = s & 31;
-  uint32_t hi = __shfl_up_sync(0xffffffffu, x, q);
-  uint32_t lo = __shfl_up_sync(0xffffffffu, x, q + 1);
-  if (lane < q) hi = 0;
-  if (lane < q + 1) lo = 0;
-  return r ? ((hi << r) | (lo >> (32 - r))) : hi;
-}
-
-__device__ __forceinline__ uint32_t shr_cells(uint32_t x, int s, int lane) {  // bit p <- bit p + s
-  const int q = s >> 5, r = s & 31;
-  uint32_t lo = __shfl_down_sync(0xffffffffu, x, q);
-  uint32_t hi = __shfl_down_sync(0xffffffffu, x, q + 1);
-  if (lane + q > 31) lo = 0;
-  if (lane + q + 1 > 31) hi = 0;
-  return r ? ((lo >> r) | (hi << (32 - r))) : lo;
-}
-
-template <int KMAX>
-struct Cells {
-  int code[KMAX];  // code[k] = G[32k + lane], 0x100 beyond the grid
-};
-
-template <int KMAX>
-__device__ __forceinline__ void cells_load(Cells<KMAX>& cl, const uint8_t* G, int HW, int lane) {
-#pragma unroll
-  for (int k = 0; k < KMAX; ++k) {
-    const int p = 32 * k + lane;
-    cl.code[k] = p < HW ? (int)G[p] : 0x100;
-  }
-}
-
-template <int KMAX>
-__device__ __forceinline__ void cells_set(Cells<KMAX>& cl, int p, int v, int lane) {
-#pragma unroll
-  for (int k = 0; k < KMAX; ++k)
-    if (k == (p >> 5) && lane == (p & 31)) cl.code[k] = v;
-}
-
-// First cell p (row-major) holding `a` with `b` at the neighbour given by
-// `dir` (0 up, 1 right, 2 down, 3 left, -1: the first of NEAR_OFFSETS up,
-// left, right, down) -- ref:rules.py:192-213, ref:goals.py:380-394.  Returns
-// p (or -1) and the neighbour cell on every lane.
-__device__ __noinline__ int2 tile_match(uint32_t am, uint32_t bm, int lane, int dir, int W, uint32_t col0,
-                                        uint32_t colL);
-
-template <int KMAX>
-__device__ __forceinline__ int bit_tile_scan(const Cells<KMAX>& cl, int lane, int a, int b, int dir, int W,
-                                             uint32_t col0, uint32_t colL, int& nb) {
-  uint32_t am = 0, bm = 0;
-#pragma unroll
-  for (int k = 0; k < KMAX; ++k) {
-    const uint32_t x = __ballot_sync(0xffffffffu, cl.code[k] == a);
-    const uint32_t y = __ballot_sync(0xffffffffu, cl.code[k] == b);
-    if (lane == k) {
-      am = x;
-      bm = y;
-    }
-  }
-  nb = -1;
-  if (!__any_sync(0xffffffffu, am != 0)) return -1;
-  const int2 pq = tile_match(am, bm, lane, dir, W, col0, colL);
-  nb = pq.y;
-  return pq.x;
-}
-
-// The matching half of bit_tile_scan: (p, neighbour) or (-1, -1).
-__device__ __noinline__ int2 tile_match(uint32_t am, uint32_t bm, int lane, int dir, int W, uint32_t col0,
-                                        uint32_t colL) {
-  int nb = -1;
-  const uint32_t up = am & shl_cells(bm, W, lane);             // b at p - W
-  const uint32_t left = am & shl_cells(bm, 1, lane) & ~col0;   // b at p - 1, same row
-  const uint32_t right = am & shr_cells(bm, 1, lane) & ~colL;  // b at p + 1, same row
-  const uint32_t down = am & shr_cells(bm, W, lane);           // b at p + W
-  const uint32_t any = dir < 0 ? (up | left | right | down) : dir == 0 ? up : dir == 1 ? right : dir == 2 ? down : left;
-  const uint32_t wm = __ballot_sync(0xffffffffu, any != 0);
-  if (!wm) return make_int2(-1, -1);
-  const int k = __ffs(wm) - 1;
-  const int bit = __ffs(__shfl_sync(0xffffffffu, any, k)) - 1;
-  const int p = 32 * k + bit;
-  if (dir < 0) {
-    const bool u = (__shfl_sync(0xffffffffu, up, k) >> bit) & 1;
-    const bool l = (__shfl_sync(0xffffffffu, left, k) >> bit) & 1;
-    const bool rt = (__shfl_sync(0xffffffffu, right, k) >> bit) & 1;
-    nb = u ? p - W : l ? p - 1 : rt ? p + 1 : p + W;
-  } else {
-    nb = dir == 0 ? p - W : dir == 1 ? p + 1 : dir == 2 ? p + W : p - 1;
-  }
-  return make_int2(p, nb);
-}
-
-// One PUT_DOWN event of one env, resolved by the whole warp: the rule pass
-// (ref:rules.py:162-213, event PUT_DOWN) then the goal (ref:goals.py:347-394)
-// on the shared-memory grid copy G (+ its bitmap form in registers).
-// Rewritten cells go to G and through to the grid in global memory.
-// Returns goal | dirty << 1 on every lane.
-template <int KMAX>
-__device__ __forceinline__ int warp_put_event(uint8_t* G, Cells<KMAX>& cl, uint8_t* genv, int lane, int H, int W, int ar, int ac,
-                              const uint32_t* rules, int nr, uint32_t goal, uint32_t col0, uint32_t colL) {
-  bool dirty = false;
-  for (int s = 0; s < nr; ++s) {
-    const uint32_t rw = rules[s];
-    const int kind = rw & 0xff, a = (rw >> 8) & 0xff, b = (rw >> 16) & 0xff, out = rw >> 24;
-    if (kind == 0 || kind > 11 || !((cRuleGate[kind] >> 2) & 1)) continue;
-    int p = -1, q = -1;
-    if (kind == 2 || kind >= 8) {  // agent-near family: every lane evaluates the same cells
-      for (int k = 0; k < (kind == 2 ? 4 : 1); ++k) {
-        const int r = ar + (kind == 2 ? near_dr(k) : dir_dr(kind - 8));
-        const int c = ac + (kind == 2 ? near_dc(k) : dir_dc(kind - 8));
-        if (r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a) { p = r * W + c; break; }
-      }
-    } else {  // TILE_NEAR (3) / TILE_NEAR_{UP,RIGHT,DOWN,LEFT} (4..7)
-      p = bit_tile_scan<KMAX>(cl, lane, a, b, kind == 3 ? -1 : kind - 4, W, col0, colL, q);
-    }
-    if (p >= 0) {
-      __syncwarp();
-      if (lane == 0) {
-        G[p] = (uint8_t)out;
-        genv[p] = (uint8_t)out;
-        if (q >= 0) {
-          G[q] = kFloorCode;
-          genv[q] = kFloorCode;
-        }
-      }
-      cells_set<KMAX>(cl, p, out, lane);
-      if (q >= 0) cells_set<KMAX>(cl, q, kFloorCode, lane);
-      dirty = true;
-      __syncwarp();
-    }
-  }
-  bool hit = false;
-  const int kind = goal & 0xff, a1 = (goal >> 8) & 0xff, a2 = (goal >> 16) & 0xff, a3 = goal >> 24;
-  if (kind != 0 && kind <= 14 && ((cGoalGate[kind] >> 2) & 1)) {
-    switch (kind) {
-      case 2: hit = G[ar * W + ac] == a1; break;
-      case 5: hit = ar == a1 && ac == a2; break;
-      case 6: hit = a2 < H && a3 < W && G[a2 * W + a3] == a1; break;
-      case 3:
-        for (int k = 0; k < 4; ++k) {
-          const int r = ar + near_dr(k), c = ac + near_dc(k);
-          hit |= r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a1;
-        }
-        break;
-      case 11: case 12: case 13: case 14: {
-        const int r = ar + dir_dr(kind - 11), c = ac + dir_dc(kind - 11);
-        hit = r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a1;
-        break;
-      }
-      default: {  // TILE_NEAR (4), TILE_NEAR_{UP,RIGHT,DOWN,LEFT} (7..10)
-        int q;
-        hit = bit_tile_scan<KMAX>(cl, lane, a1, a2, kind == 4 ? -1 : kind - 7, W, col0, colL, q) >= 0;
-      }
-    }
-  }
-  return (int)hit | ((int)dirty << 1);
-}
-
-
-// ------------------------------------------------------- step_stream
-// Persistent streaming step for grids of <= 256 cells.  A warp owns chunks of
-// 32 consecutive envs; their grids (32*H*W bytes), 16-byte state words and
-// actions are contiguous in HBM, so lane 0 moves each chunk into the warp's
-// shared memory with three TMA bulk copies (cp.async.bulk + mbarrier),
-// double-buffered: chunk k+2 is in flight while chunk k is computed.  With
-// the whole grid staged, PUT_DOWN events are resolved in place by the warp
-// (bit-parallel scans, warp_put_event); only finished trials are deferred to
-// step_rare.  No CTA-wide barrier after the prologue.
-constexpr int kStreamWarps = 4;
-
-struct StreamGeo {
-  int chunk_grid, stage, ob, rbw, warp_bytes;
-  int64_t total;
-};
-
-__host__ __device__ inline StreamGeo make_stream_geo(int HW, int V, int R) {
-  StreamGeo g;
-  g.chunk_grid = 32 * HW;                      // multiple of 16
-  g.stage = g.chunk_grid + 32 * 16 + 32 * 8;   // grids | state words | actions (<= 8 B each)
-  g.ob = 2 * V * V;
-  g.rbw = 16 * ((kRowHeader + R + 3) / 4);     // per-lane rule row
-  g.warp_bytes = 2 * g.stage + round16(32 * g.ob) + 32 * g.rbw + 16;  // + 2 mbarriers
-  g.total = (int64_t)kStreamWarps * g.warp_bytes;
-  return g;
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst), b = (uint32_t)__cvta_generic_to_shared(bar);
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
-}
-
-template <int KMAX>
-__global__ void __launch_bounds__(kStreamWarps * 32) step_stream(const xmg_env_desc d, const xmg_state s,
-                                                                const xmg_out o, const void* actions, int act_dtype,
-                                                                const uint32_t* abort_flag, uint32_t epoch,
-                                                                int64_t n) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  if (blockIdx.x == 0)
-    for (int i = threadIdx.x; i < 2 * kQueues; i += blockDim.x) s.work[count_index(epoch + 1, 0, 0) + i] = 0;
-  if (batch_rejected(abort_flag, epoch)) return;
-
-  const int H = d.height, W = d.width, HW = H * W, V = d.view_size, R = d.rule_width;
-  const StreamGeo geo = make_stream_geo(HW, V, R);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t gw = (int64_t)blockIdx.x * kStreamWarps + warp, tw = (int64_t)gridDim.x * kStreamWarps;
-  const int64_t nchunks = (n + 31) / 32;
-  const int asz = act_dtype == XMG_ACT_U8 ? 1 : act_dtype == XMG_ACT_I32 ? 4 : 8;
-  const bool act_tma = (reinterpret_cast<uintptr_t>(actions) & 15) == 0;  // else per-lane loads
-  uint8_t* wb = smem + warp * geo.warp_bytes;
-  uint8_t* obs_stage = wb + 2 * geo.stage;
-  uint32_t* rbuf = reinterpret_cast<uint32_t*>(obs_stage + round16(32 * geo.ob) + lane * geo.rbw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(obs_stage + round16(32 * geo.ob) + 32 * geo.rbw);
-  // this lane's word of the first / last column bitmaps (PUT_DOWN scans)
-  uint32_t col0 = 0, colL = 0;
-  for (int p = (32 * lane + W - 1) / W * W; p < 32 * lane + 32 && p < HW; p += W) col0 |= 1u << (p - 32 * lane);
-  for (int p = (32 * lane) / W * W + W - 1; p < 32 * lane + 32 && p < HW; p += W) colL |= 1u << (p - 32 * lane);
-
-  auto issue = [&](int64_t c, int st) {  // lane 0: TMA bulk loads of full chunk c into stage st
-    uint8_t* sb = wb + st * geo.stage;
-    const uint32_t abytes = 32u * asz;
-    mbar_expect(bars + st, (uint32_t)geo.chunk_grid + 512u + (act_tma ? abytes : 0u));
-    bulk_g2s(sb, s.grids + c * (int64_t)geo.chunk_grid, (uint32_t)geo.chunk_grid, bars + st);
-    bulk_g2s(sb + geo.chunk_grid, s.agent + 2 * 32 * c, 512u, bars + st);
-    if (act_tma)
-      bulk_g2s(sb + geo.chunk_grid + 512, reinterpret_cast<const uint8_t*>(actions) + 32 * c * asz, abytes,
-               bars + st);
-  };
-  const int64_t nfull = n / 32;  // chunks fully inside [0, n)
-  if (lane == 0) {
-    mbar_init(bars);
-    mbar_init(bars + 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (gw < nfull) issue(gw, 0);
-    if (gw + tw < nfull) issue(gw + tw, 1);
-  }
-  __syncwarp();
-
-  int k = 0;
-  for (int64_t c = gw; c < nchunks; c += tw, ++k) {
-    const int st = k & 1;
-    uint8_t* sb = wb + st * geo.stage;
-    const int64_t e = 32 * c + lane;
-    const bool valid = e < n;
-    if (c < nfull) {
-      mbar_wait(bars + st, (uint32_t)((k >> 1) & 1));
-    } else {  // the tail chunk: each lane fetches its own env
-      if (valid) {
-        const uint8_t* g = s.grids + e * (int64_t)HW;
-        for (int i = 0; i < HW; ++i) sb[lane * HW + i] = g[i];
-        reinterpret_cast<ulonglong2*>(sb + geo.chunk_grid)[lane] = reinterpret_cast<const ulonglong2*>(s.agent)[e];
-        for (int i = 0; i < asz; ++i)
-          sb[geo.chunk_grid + 512 + lane * asz + i] = reinterpret_cast<const uint8_t*>(actions)[e * asz + i];
-      }
-      __syncwarp();
-    }
-    // ---- this lane's env: state word, action, staged grid
-    const ulonglong2 ag = valid ? reinterpret_cast<const ulonglong2*>(sb + geo.chunk_grid)[lane]
-                                : make_ulonglong2(0, 0);
-    int act = 1;
-    if (valid) {
-      if (act_tma || c >= nfull) {
-        const uint8_t* ap = sb + geo.chunk_grid + 512 + lane * asz;
-        act = asz == 1 ? (int)ap[0] : asz == 4 ? *reinterpret_cast<const int32_t*>(ap)
-                                               : (int)*reinterpret_cast<const int64_t*>(ap);
-      } else {
-        act = load_action(actions, act_dtype, e);
-      }
-    }
-    View vw;
-    vw.g = s.grids + (valid ? e : 0) * (int64_t)HW;
-    vw.stage = sb + lane * HW;
-    vw.sbase = 0;
-    vw.slo = 0;
-    vw.shi = HW;
-    int r = (int)(ag.x & 0xff), c0 = (int)((ag.x >> 8) & 0xff), dir = (int)((ag.x >> 16) & 3);
-    int pocket = (int)((ag.x >> 24) & 0xff);
-    uint32_t sc = (uint32_t)(ag.x >> 32);
-    const uint32_t goal_word = (uint32_t)ag.y;
-    const int task = (int)(ag.y >> 32);
-    // the rule row of actions that can raise a MOVE / PICK_UP / PUT_DOWN event
-    if (valid && R > 0 && (act == 0 || act == 3 || act == 4)) {
-      const uint32_t* src = d.task_rows + (int64_t)task * d.row_words;
-      for (int q = 0; q < (kRowHeader + R + 3) >> 2; ++q) cp_async16(rbuf + 4 * q, src + 4 * q);
-      cp_async_wait_all();
-    }
-    int ev = -1;
-    bool goal = false;
-    if (valid) {
-      // ---- action, ref:vecenv.py:306-342 / ref:env.py:148-191
-      const int tr = r + dir_dr(dir), tc = c0 + dir_dc(dir);
-      const bool inside = tr >= 0 && tr < H && tc >= 0 && tc < W;
-      const int tflat = tr * W + tc;
-      const int tcode = inside ? vw.stage[tflat] : 0, tt = tcode >> 4;
-      switch (act) {
-        case 0:
-          if (inside && ((kWalkable >> tt) & 1)) { r = tr; c0 = tc; ev = 0; }
-          break;
-        case 1: dir = (dir + 3) & 3; break;
-        case 2: dir = (dir + 1) & 3; break;
-        case 3:
-          if (inside && pocket == 0 && ((kPickable >> tt) & 1)) {
-            pocket = tcode; vw.wr(tflat, kFloorCode); ev = 1;
-          }
-          break;
-        case 4:
-          if (inside && pocket != 0 && tt == kFloor) {
-            vw.wr(tflat, (uint8_t)pocket); pocket = 0; ev = 2;
-          }
-          break;
-        default:
-          if (inside) {
-            const int col = tcode & 15;
-            if (tt == kClosed || (tt == kLocked && pocket == kKey * 16 + col)) {
-              vw.wr(tflat, (uint8_t)(kOpen * 16 + col)); ev = 3;
-            }
-          }
-      }
-      // ---- MOVE / PICK_UP: agent-relative rules and goal (ref:vecenv.py:344-349)
-      if (ev == 0 || ev == 1) {
-        Nbrs nb = load_nbrs(vw, H, W, r, c0);
-        const int nr = R > 0 ? (int)(rbuf[1] & 0xff) : 0;
-        if (nr) {
-          if (R <= 32) {
-            const uint32_t slots = rbuf[2 + ev];
-            if (slots) pocket = agent_rules(vw, nb, rbuf + kRowHeader, slots, pocket);
-          } else {
-            for (int s0 = 0; s0 < nr; ++s0) {
-              const int kind = rbuf[kRowHeader + s0] & 0xff;
-              if (kind >= 1 && kind <= 11 && ((cRuleGate[kind] >> ev) & 1))
-                pocket = agent_rules(vw, nb, rbuf + kRowHeader + s0, 1u, pocket);
-            }
-          }
-        }
-        goal = agent_goal(nb, vw.stage[r * W + c0], goal_word, ev, r, c0, pocket);
-      }
-    }
-    // ---- PUT_DOWN: grid-wide rules and goal, one env at a time by the warp
-    uint32_t pm = __ballot_sync(0xffffffffu, ev == 2);
-    if (pm) {
-      __syncwarp();
-      while (pm) {
-        const int t = __ffs(pm) - 1;
-        pm &= pm - 1;
-        uint8_t* G = sb + t * HW;
-        const uint64_t agx = __shfl_sync(0xffffffffu, (unsigned long long)pack_agent(r, c0, dir, pocket, sc), t);
-        const uint32_t gw_t = __shfl_sync(0xffffffffu, goal_word, t);
-        const uint32_t* rt = reinterpret_cast<const uint32_t*>(obs_stage + round16(32 * geo.ob) + t * geo.rbw);
-        const int nr = R > 0 ? (int)(rt[1] & 0xff) : 0;
-        Cells<KMAX> cl;
-        cells_load<KMAX>(cl, G, HW, lane);
-        const int res = warp_put_event<KMAX>(G, cl, s.grids + (32 * c + t) * (int64_t)HW, lane, H, W,
-                                             (int)(agx & 0xff), (int)((agx >> 8) & 0xff), rt + kRowHeader, nr,
-                                             gw_t, col0, colL);
-        if (lane == t) goal = res & 1;
-      }
-    }
-    // ---- counters and reward, ref:vecenv.py:351-357
-    float rew = 0.f;
-    bool last = false;
-    if (valid) {
-      sc += 1;
-      last = goal || sc >= (uint32_t)d.budget;
-      if (goal) rew = goal_reward(sc, d.budget);
-      o.reward[e] = rew;
-      o.discount[e] = last ? 0.f : 1.f;
-      o.step_type[e] = last ? 2 : 1;
-      s.agent[2 * e] = pack_agent(r, c0, dir, pocket, sc);
-    }
-    // ---- finished trials go to step_rare's reset queue
-    const uint32_t qm = __ballot_sync(0xffffffffu, last);
-    if (qm) {
-      const int kq = (int)(c % kQueues);
-      const int leader = __ffs(qm) - 1;
-      uint32_t base = 0;
-      if (lane == leader) base = atomicAdd(s.work + count_index(epoch, 1, kq), (uint32_t)__popc(qm));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      if (last)
-        s.work[queue_base(n, epoch, 1, kq) + base + __popc(qm & ((1u << lane) - 1))] =
-            (uint32_t)e;
-    }
-    if (o.stats != nullptr) warp_stats(o.stats, (int)(c / 4), rew, last ? 1.0 : 0.0, last ? (double)sc : 0.0);
-    // ---- observation: staged in smem, one TMA bulk store per warp
-    if (o.obs != nullptr) {
-      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // previous store drained
-      __syncwarp();
-      if (valid) {
-        uint8_t* dst = obs_stage + lane * geo.ob;
-        if (d.see_through_walls) {
-          if (V == 5) obs_see<5>(vw.stage, 0, dst, r, c0, dir, H, W, V);
-          else obs_see<0>(vw.stage, 0, dst, r, c0, dir, H, W, V);
-        } else {
-          obs_occluded(vw, dst, r, c0, dir, H, W, V);
-        }
-      }
-      const int nvalid = (int)min((int64_t)32, n - 32 * c);
-      const uint32_t bytes = (uint32_t)(nvalid * geo.ob), bulk = bytes & ~15u;
-      uint8_t* gdst = o.obs + 32 * c * geo.ob;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0 && bulk) {
-        const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(obs_stage);
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(saddr), "r"(bulk)
-                     : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-      for (uint32_t q = bulk + lane; q < bytes; q += 32) gdst[q] = obs_stage[q];
-    }
-    // ---- refill this stage with chunk c + 2 tw
-    __syncwarp();
-    if (lane == 0 && c + 2 * tw < nfull) issue(c + 2 * tw, st);
-  }
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // ------------------------------------------------------- warp-level PUT_DOWN
@@ -2335,33 +1897,6 @@ int validate_desc(const xmg_env_desc* d, const xmg_state* s, int64_t n) {
   return 0;
 }
 
-template <int KMAX>
-int launch_stream(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
-                  const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st) {
-  const StreamGeo geo = make_stream_geo(d->height * d->width, d->view_size, d->rule_width);
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  static int sms = 148;
-  std::call_once(once, [] {
-    attr_err = allow_smem(step_stream<KMAX>, kMaxDynSmem - 1024);
-    int dev = 0;
-    if (attr_err == cudaSuccess) attr_err = cudaGetDevice(&dev);
-    if (attr_err == cudaSuccess) attr_err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  });
-  if (attr_err != cudaSuccess) return fail(std::string("step_stream attributes: ") + cudaGetErrorString(attr_err));
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_stream<KMAX>, kStreamWarps * 32,
-                                                    (size_t)geo.total) != cudaSuccess || per_sm < 1)
-    return fail("step_stream does not fit on an SM");
-  const int64_t nchunks = (n + 31) / 32;
-  int64_t blocks = (int64_t)per_sm * sms;
-  const int64_t need = (nchunks + kStreamWarps - 1) / kStreamWarps;
-  if (blocks > need) blocks = need;
-  step_stream<KMAX><<<(unsigned)blocks, kStreamWarps * 32, (size_t)geo.total, st>>>(*d, *s, *o, actions, dtype, flag,
-                                                                                  epoch, n);
-  return check_launch("step_stream");
-}
-
 // whole-grid staging: 16-byte chunks of a grid at any alignment
 inline int full_chunks(int hw) { return (hw + 30) / 16; }
 
@@ -2374,22 +1909,8 @@ bool use_full(const xmg_env_desc* d) {
   return mode == 1 && full_chunks(d->height * d->width) <= 12;
 }
 
-bool use_stream(const xmg_env_desc* d) {
-  static int mode = -1;  // XMG_MAIN=stream|window (default: window)
-  if (mode < 0) {
-    const char* m = getenv("XMG_MAIN");
-    mode = (m && !strcmp(m, "stream")) ? 1 : 0;
-  }
-  return mode == 1 && d->height * d->width <= 256 &&
-         make_stream_geo(d->height * d->width, d->view_size, d->rule_width).total <= kMaxDynSmem - 1024;
-}
-
 int dispatch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
                   const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st) {
-  if (use_stream(d)) {
-    if (d->height * d->width <= 128) return launch_stream<4>(d, s, o, actions, dtype, flag, epoch, n, st);
-    return launch_stream<8>(d, s, o, actions, dtype, flag, epoch, n, st);
-  }
   if (use_full(d)) {
     const int fc = full_chunks(d->height * d->width);
     if (fc <= 6) return launch_main<6, true>(d, s, o, actions, dtype, flag, epoch, n, st);
@@ -2522,7 +2043,7 @@ int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* a
   if (dispatch_main(desc, state, out, actions, action_dtype, abort_flag, epoch, n, (cudaStream_t)stream)) return -1;
   if (prof) cudaEventRecord(ev[1], (cudaStream_t)stream);
   // step_main (window mode) records the tiles step_rare must release
-  const int track = use_stream(desc) ? 0 : 1;
+  const int track = 1;
   const int rc = launch_rare(desc, state, out, nullptr, abort_flag, epoch, n, track, (cudaStream_t)stream);
   if (prof) cudaEventRecord(ev[2], (cudaStream_t)stream);
   return rc;
@@ -2540,7 +2061,7 @@ int32_t xmg_steps(const xmg_env_desc* desc, const xmg_state* state, const void* 
       (traj->obs && (((reinterpret_cast<uintptr_t>(traj->obs)) & 15) || ((n * ob) & 15))))
     return fail("grids / agent / obs buffers must be 16-byte aligned (and n*2*v*v a multiple of 16 with obs)");
   const int asz = action_dtype == XMG_ACT_U8 ? 1 : action_dtype == XMG_ACT_I32 ? 4 : 8;
-  const int track = use_stream(desc) ? 0 : 1;
+  const int track = 1;
   for (int64_t k = 0; k < steps; ++k) {
     xmg_out o = *traj;
     if (o.obs) o.obs += k * n * ob;

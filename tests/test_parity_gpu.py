@@ -191,3 +191,45 @@ def test_shards_reproduce_the_global_batch():
                 assert torch.equal(s.observations, w.observations[sl])
                 assert torch.equal(s.rewards, w.rewards[sl])
                 assert torch.equal(p.grids, whole.grids[sl])
+
+
+@pytest.mark.parametrize("knobs", [{"XMG_STAGE": "full"}, {"XMG_PDL": "0"}, {"XMG_RARE_CTAS": "2"}])
+def test_tuning_knobs_keep_parity(knobs):
+    """The library's tuning switches (whole-grid staging, no programmatic
+    overlap, a small step_rare grid) change scheduling only: a fresh process
+    with each switch reproduces the oracle bit for bit (switches are read once
+    per process)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, sys
+sys.path.insert(0, "tests")
+from helpers import benchmark_file, oracle_from_table
+from paper_2312_12044_b200 import VecEnv, key_from_seed, load_benchmark, make, policy_keys, random_actions
+for env_name, cfg, n, steps in (("XLand-MiniGrid-R4-13x13", "medium", 2048, 520), ("MiniGrid-DoorKey-8x8", None, 1024, 200)):
+    _, params = make(env_name)
+    if cfg:
+        bm = load_benchmark(benchmark_file(cfg)); vec = VecEnv(params, n, bm)
+        ora = oracle_from_table(params, bm.task_table(), vec._ids_host)
+    else:
+        from paper_2312_12044_b200.ruleset import TaskTable
+        vec = VecEnv(params, n)
+        ora = oracle_from_table(params, TaskTable(np.zeros((1, 4), np.uint32), 0, 0, 0), np.zeros(n, np.int64))
+    root = key_from_seed(0)
+    assert np.array_equal(vec.reset(root).observations.cpu().numpy(), ora.reset(root))
+    acts = random_actions(policy_keys(key_from_seed(1), n, device="cuda"), 0, steps)
+    ah = acts.cpu().numpy()
+    for t in range(steps):
+        ts = vec.step(acts[t]); o, r, d, s = ora.step(ah[t])
+        assert np.array_equal(ts.observations.cpu().numpy(), o), t
+        assert np.array_equal(ts.rewards.cpu().numpy(), r.astype(np.float32)), t
+        assert np.array_equal(ts.step_types.cpu().numpy(), s), t
+    assert np.array_equal(vec.grids.cpu().numpy(), ora.grids)
+    vec.check()
+print("ok")
+'''
+    from .conftest import ROOT
+    env = dict(os.environ, **knobs)
+    res = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0 and "ok" in res.stdout, res.stderr[-3000:]
