@@ -75,7 +75,8 @@ typedef struct xmg_env_desc {
     int32_t resample_tasks;      /* 0: a trial keeps its env's task (reference semantics,
                                   * vecenv.py:224-233); 1 (extension): every reset draws
                                   * task = rows[word0(split(ek, 2)) % M] (benchio.py:57-58) */
-    const uint8_t* base_cells;   /* [H*W] grid before doors/objects for this scenario */
+    const uint8_t* base_cells;   /* [H*W] grid before doors/objects for this scenario
+                                  * (allocation padded to a multiple of 16 bytes) */
     const int16_t* seg_off;      /* [num_segments+1] offsets into seg_cells */
     const int16_t* seg_cells;    /* flat cell indices of each door segment */
     const uint32_t* task_rows;   /* [num_tasks][row_words] */

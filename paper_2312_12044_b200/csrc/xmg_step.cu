@@ -642,7 +642,7 @@ __device__ __forceinline__ int select_rank(const uint64_t* wd, int lane, int F, 
 // spawn_base) (ref:scenarios.py:281-288), via warp_select: the element of
 // rank nobj - 1 bounds the object cells, which are then ordered exactly
 // among themselves.
-__device__ void rank_place(const WarpScratch& ws, int lane, int F, int W, int mode, int x, const uint8_t* objs,
+__device__ void rank_place(const WarpScratch& ws, int lane, int F, int W, int mode, int x, int obj_lane,
                            int nobj, int spawn_base, uint64_t spawn_word) {
   const int K = (F + 127) >> 7;
   uint32_t valid = 0;
@@ -653,10 +653,12 @@ __device__ void rank_place(const WarpScratch& ws, int lane, int F, int W, int mo
       if (f < F && col_ok(mode, ws.fc[f], W, x)) valid |= 1u << (4 * k + i);
     }
   const int total = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(valid));
+  XMG_TRB(7);
   const int no = nobj < total ? nobj : total;
   uint32_t* list = reinterpret_cast<uint32_t*>(ws.slot);  // the object cells' element indices
   if (no > 0) {
     const int fb = select_rank(ws.wd, lane, F, valid, total, no - 1);
+    XMG_TRB(8);
     const uint64_t wb = ws.wd[fb];
     int cnt = 0;
     for (int k = 0; k < K; ++k)
@@ -673,18 +675,23 @@ __device__ void rank_place(const WarpScratch& ws, int lane, int F, int W, int mo
         cnt += __popc(m);
       }
     __syncwarp();
-    for (int l = lane; l < no; l += 32) {  // exact rank among the no smallest
-      const int f = (int)list[l];
+    XMG_TRB(9);
+    // exact rank among the no (<= 32) smallest; object `rank` comes from
+    // lane `rank` (objects were read into lanes before the draws)
+    int f = 0, rank = 0;
+    if (lane < no) {
+      f = (int)list[lane];
       const uint64_t w = ws.wd[f];
-      int rank = 0;
       for (int m = 0; m < no; ++m) {
         const int g = (int)list[m];
         const uint64_t wg = ws.wd[g];
         rank += (wg < w) | ((wg == w) & (g < f));
       }
-      ws.grid[ws.fc[f]] = objs[rank];
     }
+    const int obj = __shfl_sync(0xffffffffu, obj_lane, rank & 31);
+    if (lane < no) ws.grid[ws.fc[f]] = (uint8_t)obj;
   }
+  XMG_TRB(10);
   const int tail = total - spawn_base;
   if (tail > 0) {
     const int fs = select_rank(ws.wd, lane, F, valid, total, spawn_base + (int)(spawn_word % (uint64_t)tail));
@@ -734,6 +741,7 @@ __device__ __noinline__ void derive_trial_keys(uint64_t ek_hi, uint64_t ek_lo, b
 __device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, int hwp, int lg, int lane,
                                         const TrialKeys* keyp, int task_in, uint32_t goal_in, uint8_t* gdst,
                                         ResetOut* outp) {
+  XMG_TRB(0);
   const TrialKeys key = *keyp;
   const xmg_env_desc& d = *dp;  // CTA copy in shared memory
   const WarpScratch ws = make_scratch(wbase, hwp, lg);
@@ -749,8 +757,21 @@ __device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
     res.goal = d.task_rows[(int64_t)res.task * d.row_words];
   }
   const uint32_t* row = d.task_rows + (int64_t)res.task * d.row_words;
-  // base cells of this scenario
-  for (int i = lane; i < HW; i += 32) ws.grid[i] = d.base_cells[i];
+  // the objects this trial places, one per lane, read now so the load is in
+  // flight during the draws (ref:vecenv.py:261-270; FourRooms: the goal,
+  // ref:scenarios.py:361-370; EmptyRandom: none)
+  int nobj = 0, obj_lane = 0;
+  if (sc == XMG_SCENARIO_XLAND) {
+    nobj = (int)((row[1] >> 8) & 0xff);
+    if (lane < nobj) obj_lane = reinterpret_cast<const uint8_t*>(row + kRowHeader + d.rule_width)[lane];
+  } else if (sc == XMG_SCENARIO_FOUR_ROOMS) {
+    nobj = 1;
+    obj_lane = kGreenGoal;
+  }
+  // base cells of this scenario (16-byte read-only loads; the buffer and
+  // ws.grid are padded to a multiple of 16 bytes)
+  for (int i = lane; i < (HW + 15) >> 4; i += 32)
+    reinterpret_cast<uint4*>(ws.grid)[i] = __ldg(reinterpret_cast<const uint4*>(d.base_cells) + i);
   if (sc == XMG_SCENARIO_EMPTY) {  // ref:scenarios.py:320-327
     __syncwarp();
     for (int i = lane; i < HW; i += 32) gdst[i] = ws.grid[i];
@@ -784,9 +805,12 @@ __device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
     if (lane == 0) ws.grid[door_row * W + wall_col] = (uint8_t)(kLocked * 16 + color);
   }
   __syncwarp();
+  XMG_TRB(1);
   const int F = build_free_list(ws, HW, lane);
+  XMG_TRB(2);
   const int nseg = (sc == XMG_SCENARIO_XLAND || sc == XMG_SCENARIO_FOUR_ROOMS) ? d.num_segments : 0;
   draw_all(ws, lane, F, k1h, k1l, nseg, k0h, k0l, k2h, k2l);
+  XMG_TRB(3);
   // doors: ref:layouts.py:532-544 (segments never hold free cells)
   if (lane < nseg) {
     const int off = d.seg_off[lane], len = d.seg_off[lane + 1] - off;
@@ -795,27 +819,11 @@ __device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
   }
   const uint64_t a0 = ws.misc[24], a1 = ws.misc[25];
   res.d = (int)(a1 & 3);  // a1 % 4
-  uint8_t objs_local[4];
   if (sc == XMG_SCENARIO_XLAND || sc == XMG_SCENARIO_FOUR_ROOMS || sc == XMG_SCENARIO_EMPTY_RANDOM) {
-    int nobj;
-    const uint8_t* objs;
-    if (sc == XMG_SCENARIO_XLAND) {  // ref:vecenv.py:261-279
-      nobj = (row[1] >> 8) & 0xff;
-      objs = reinterpret_cast<const uint8_t*>(row + kRowHeader + d.rule_width);
-    } else if (sc == XMG_SCENARIO_FOUR_ROOMS) {  // ref:scenarios.py:361-370
-      objs_local[0] = kGreenGoal;
-      objs = objs_local;
-      nobj = 1;
-      res.goal = 2u | ((uint32_t)kGreenGoal << 8);
-    } else {  // EMPTY_RANDOM, ref:scenarios.py:330-338
-      objs = objs_local;
-      nobj = 0;
-      res.goal = 2u | ((uint32_t)kGreenGoal << 8);
-    }
-    rank_place(ws, lane, F, W, 0, 0, objs, nobj, nobj, a0);
+    if (sc != XMG_SCENARIO_XLAND) res.goal = 2u | ((uint32_t)kGreenGoal << 8);  // ref:scenarios.py:330-370
+    rank_place(ws, lane, F, W, 0, 0, obj_lane, nobj, nobj, a0);
   } else {  // two-room ports: shuffle all free cells, keep the left room
-    objs_local[0] = (uint8_t)(kKey * 16 + color);
-    rank_place(ws, lane, F, W, 1, wall_col, objs_local, 1, 1, a0);
+    rank_place(ws, lane, F, W, 1, wall_col, kKey * 16 + color, 1, 1, a0);
     if (sc == XMG_SCENARIO_DOOR_KEY) {
       res.goal = 2u | ((uint32_t)kGreenGoal << 8);
     } else if (sc == XMG_SCENARIO_UNLOCK) {  // ref:scenarios.py:393-397
@@ -841,12 +849,14 @@ __device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
       __syncwarp();
     }
   }
+  XMG_TRB(4);
   const int spawn_cell = reinterpret_cast<const int*>(ws.misc + 32)[0];
   res.r = spawn_cell / W;
   res.c = spawn_cell - res.r * W;
   for (int i = lane; i < HW; i += 32) gdst[i] = ws.grid[i];
   if (lane == 0) *outp = res;
   __syncwarp();
+  XMG_TRB(5);
 }
 
 // ------------------------------------------------------- the step: two kernels
@@ -1246,21 +1256,34 @@ __device__ __forceinline__ int warp_cands(const uint8_t* G, int HW, uint32_t* ca
   return nc;
 }
 
-// first cell (row-major) holding `a` with `b` at the neighbour of `dir`, by one lane
-__device__ __forceinline__ int lane_find(const uint8_t* G, const uint32_t* cand, int nc, int H, int W, int a, int b,
-                                         int dir, int& q) {
-  if (is_cand(a)) {
-    for (int i = 0; i < nc; ++i) {
-      const uint32_t en = cand[i];
-      if ((int)(en & 0xff) != a) continue;
-      q = nb_match(G, H, W, (int)(en >> 8), b, dir);
-      if (q >= 0) return (int)(en >> 8);
+// First cell (row-major) holding `a` with `b` at the neighbour of `dir`
+// (ref:rules.py:192-213), by the whole warp: a ballot per 32 candidates (or
+// cells, when `a` is floor / wall and so not in the candidate list).  Returns
+// the cell and its neighbour `q` on every lane, or -1.
+__device__ __forceinline__ int warp_tile_find(const uint8_t* G, const uint32_t* cand, int nc, int H, int W, int a,
+                                              int b, int dir, int lane, int& q) {
+  const bool in_list = is_cand(a);
+  const int total = in_list ? nc : H * W;
+  for (int base = 0; base < total; base += 32) {
+    const int i = base + lane;
+    int pos = -1, nb = -1;
+    if (i < total) {
+      int code;
+      if (in_list) {
+        const uint32_t en = cand[i];
+        pos = (int)(en >> 8);
+        code = (int)(en & 0xff);
+      } else {
+        pos = i;
+        code = G[i];
+      }
+      if (code == a) nb = nb_match(G, H, W, pos, b, dir);
     }
-  } else {
-    for (int p = 0; p < H * W; ++p) {
-      if (G[p] != a) continue;
-      q = nb_match(G, H, W, p, b, dir);
-      if (q >= 0) return p;
+    const uint32_t hit = __ballot_sync(0xffffffffu, nb >= 0);
+    if (hit) {
+      const int w = __ffs(hit) - 1;
+      q = __shfl_sync(0xffffffffu, nb, w);
+      return __shfl_sync(0xffffffffu, pos, w);
     }
   }
   q = -1;
@@ -1275,12 +1298,18 @@ __device__ __noinline__ int warp_put_env(uint8_t* G, uint8_t* genv, uint32_t* ca
   const int HW = H * W;
   int nc = warp_cands(G, HW, cand, lane);
   bool dirty = false;
+  // Slots in stored order, restarting after every slot that fires (it changed
+  // the grid).  AGENT_NEAR-family slots are cheap: lane s evaluates slot s0 + s
+  // speculatively on the current grid.  TILE_NEAR-family slots are evaluated
+  // only when they come first in order, by the whole warp (a ballot over the
+  // candidate list: the lowest hit is the first in row-major order).
   for (int s0 = 0; s0 < nr;) {
     const int sl = s0 + lane;
     int p = -1, q = -1, out = 0;
+    bool tile = false;
     if (sl < nr) {
       const uint32_t rw = rules[sl];
-      const int kind = rw & 0xff, a = (rw >> 8) & 0xff, b = (rw >> 16) & 0xff;
+      const int kind = rw & 0xff, a = (rw >> 8) & 0xff;
       out = (int)(rw >> 24);
       if (kind == 2 || (kind >= 8 && kind <= 11)) {  // AGENT_NEAR family
         for (int k = 0; k < 4; ++k) {
@@ -1289,19 +1318,37 @@ __device__ __noinline__ int warp_put_env(uint8_t* G, uint8_t* genv, uint32_t* ca
           if (r >= 0 && r < H && c >= 0 && c < W && G[r * W + c] == a) { p = r * W + c; break; }
           if (kind != 2) break;
         }
-      } else if (kind >= 3 && kind <= 7) {  // TILE_NEAR family
-        p = lane_find(G, cand, nc, H, W, a, b, kind == 3 ? -1 : kind - 4, q);
+      } else if (kind >= 3 && kind <= 7) {  // TILE_NEAR family: resolved below, in order
+        tile = true;
       }
     }
     const uint32_t fired = __ballot_sync(0xffffffffu, p >= 0);
-    if (fired == 0) {
+    uint32_t pend = fired | __ballot_sync(0xffffffffu, tile);
+    int w = -1;
+    while (pend) {
+      const int t = __ffs(pend) - 1;
+      if ((fired >> t) & 1) {
+        p = __shfl_sync(0xffffffffu, p, t);
+        q = __shfl_sync(0xffffffffu, q, t);
+        out = __shfl_sync(0xffffffffu, out, t);
+        w = t;
+        break;
+      }
+      const uint32_t rw = rules[s0 + t];
+      const int kind = rw & 0xff, a = (rw >> 8) & 0xff, b = (rw >> 16) & 0xff;
+      const int pt = warp_tile_find(G, cand, nc, H, W, a, b, kind == 3 ? -1 : kind - 4, lane, q);
+      if (pt >= 0) {
+        p = pt;
+        out = (int)(rw >> 24);
+        w = t;
+        break;
+      }
+      pend &= pend - 1;
+    }
+    if (w < 0) {
       s0 += 32;
       continue;
     }
-    const int w = __ffs(fired) - 1;
-    p = __shfl_sync(0xffffffffu, p, w);
-    q = __shfl_sync(0xffffffffu, q, w);
-    out = __shfl_sync(0xffffffffu, out, w);
     const int old = G[p];
     __syncwarp();
     if (lane == 0) {
@@ -1429,6 +1476,7 @@ __device__ __forceinline__ void warp_reset_env(const xmg_env_desc& d, const xmg_
   }
   if (o.obs != nullptr) warp_obs(ws.grid, o.obs + e * ob, lane, ro.r, ro.c, ro.d, H, W, V, d.see_through_walls != 0);
   __syncwarp();
+  XMG_TRB(6);
 }
 
 // Resets of a group of up to 32 envs (one per lane, `mine`): each lane

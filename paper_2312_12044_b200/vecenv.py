@@ -226,7 +226,10 @@ class VecEnv:
         self._ids_host = ids
 
         # -- device buffers
-        self._base = torch.from_numpy(base.copy()).to(dev)
+        # padded to 16 bytes: the reset kernels read it with 16-byte loads
+        base_p = np.zeros((self._hw + 15) // 16 * 16, np.uint8)
+        base_p[: self._hw] = base.reshape(-1)
+        self._base = torch.from_numpy(base_p).to(dev)
         self._seg_off = torch.from_numpy(seg_off.astype(np.int16)).to(dev)
         self._seg_cells = torch.from_numpy(seg_cells.astype(np.int16)).to(dev)
         self._table = torch.from_numpy(table.rows.view(np.int32).copy()).to(dev)
