@@ -1535,10 +1535,32 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRar
   const bool reset_mode = reset_keys != nullptr;
   const int q = gw % kQueues, j = gw / kQueues, per_q = tw / kQueues;
   int64_t cnt_put = 0, cnt_reset = 0;
+  // the sub-queue's warps split into PUT_DOWN warps [0, put_w) and reset
+  // warps [put_w, per_q), in proportion to the work (a trial build costs
+  // about four PUT_DOWN events), so a warp's chain is PUT_DOWN envs or builds,
+  // not both
+  int put_w = per_q, jp = j, jr = -1, rs_w = 0;
   if (!reset_mode) {
     cnt_put = s.work[count_index(epoch, 0, q)];
     cnt_reset = s.work[count_index(epoch, 1, q)];
-    const bool idle = j >= cnt_put && j >= cnt_reset;
+    if (cnt_reset > 0 && per_q < 2) {  // a single warp per sub-queue does both
+      rs_w = per_q;
+      jr = j;
+    } else if (cnt_reset > 0) {
+      if (cnt_put == 0) {
+        rs_w = per_q;
+      } else {
+        const double wr = 4.0 * (double)cnt_reset, wp = (double)cnt_put;
+        rs_w = (int)(per_q * wr / (wr + wp) + 0.5);
+        rs_w = rs_w < 1 ? 1 : rs_w > per_q - 1 ? per_q - 1 : rs_w;
+      }
+      put_w = per_q - rs_w;
+      if (j >= put_w) {
+        jp = -1;
+        jr = j - put_w;
+      }
+    }
+    const bool idle = (jp < 0 || jp >= cnt_put) && (jr < 0 || jr >= cnt_reset);
     // the counts are read (and used): the next step's step_main may launch
     // (it clears them), and waits per tile on `pending` for the envs below
     if (track) griddep_launch();
@@ -1574,15 +1596,15 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRar
   // ---- PUT_DOWN events: entries j, j + per_q, ... of sub-queue q, kPutBatch
   // at a time prefetched into shared memory (one env per lane), then
   // resolved one by one by the whole warp
-  if (j < cnt_put) {
+  if (jp >= 0 && jp < cnt_put) {
     const uint32_t* qp = s.work + queue_base(n, epoch, 0, q);
     uint8_t* pg = tail;                                                  // kPutBatch grids
     uint32_t* pr = reinterpret_cast<uint32_t*>(tail + kPutBatch * geo.pgb);  // kPutBatch rule rows
     ulonglong2* pa = reinterpret_cast<ulonglong2*>(tail + kPutBatch * (geo.pgb + geo.rbw));  // state words
     uint32_t* pc = reinterpret_cast<uint32_t*>(tail + kPutBatch * (geo.pgb + geo.rbw + 16));  // candidates
     const bool resample = d.resample_tasks && d.scenario == XMG_SCENARIO_XLAND;
-    for (int64_t i0 = j; i0 < cnt_put; i0 += (int64_t)kPutBatch * per_q) {
-      const int64_t it = i0 + (int64_t)lane * per_q;
+    for (int64_t i0 = jp; i0 < cnt_put; i0 += (int64_t)kPutBatch * put_w) {
+      const int64_t it = i0 + (int64_t)lane * put_w;
       const bool mine = lane < kPutBatch && it < cnt_put;
       int64_t e_l = 0;
       int off_l = 0;
@@ -1669,10 +1691,10 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRar
   XMG_TR(gw, 3, (unsigned long long)cnt_put | ((unsigned long long)cnt_reset << 32));
 #endif
   // ---- trial resets, 32 at a time (entries i0 + lane * per_q)
-  if (j < cnt_reset) {
+  if (jr >= 0 && jr < cnt_reset) {
     const uint32_t* qp = s.work + queue_base(n, epoch, 1, q);
-    for (int64_t i0 = j; i0 < cnt_reset; i0 += 32 * (int64_t)per_q) {
-      const int64_t i = i0 + (int64_t)lane * per_q;
+    for (int64_t i0 = jr; i0 < cnt_reset; i0 += 32 * (int64_t)rs_w) {
+      const int64_t i = i0 + (int64_t)lane * rs_w;
       const bool mine = i < cnt_reset;
       const int64_t e = mine ? (int64_t)qp[i] : 0;
       warp_reset_group(d, sdesc, s, o, wbase, geo, keys, lane, mine, e, nullptr, gw);
