@@ -169,3 +169,34 @@ def test_steps_block_equals_single_steps(env_name, config, n, k):
     with pytest.raises(InvalidAction):
         b.steps(bad)
     assert torch.equal(before, b.grids)
+
+
+def test_resample_on_reset_uses_sample_ruleset():
+    """Resample mode (an extension without a reference
+    oracle) is pinned to the reference's sampling primitive: a trial that ends
+    with episode key ek continues with task Benchmark.sample_ruleset(split(ek,
+    2)) = row randint(split(ek, 2), M) (ref benchio.py:57-58), and its new
+    trial equals a plain reset_with_keys(ek) of an env bound to that task."""
+    from paper_2312_12044_b200 import Key, VecEnv, key_from_seed, load_benchmark, make, policy_keys, random_actions
+    from paper_2312_12044_b200.core import randint, split
+    _, params = make("XLand-MiniGrid-R4-13x13")
+    bm = load_benchmark(benchmark_file("medium"))
+    n, budget = 512, params.step_budget
+    vec = VecEnv(params, n, bm, resample_tasks=True)
+    vec.reset(key_from_seed(3))
+    acts = random_actions(policy_keys(key_from_seed(4), n, device=vec.device), 0, budget)
+    for t in range(budget - 1):
+        vec.step(acts[t])
+    ek = vec.rng.cpu().numpy().view(np.uint64).copy()
+    ts = vec.step(acts[budget - 1])
+    last = ts.step_types.cpu().numpy() == 2
+    assert last.sum() > n // 2  # the synchronized budget reset
+    want = np.array([randint(split(Key(int(a), int(b)), 3)[2], bm.num_rulesets()) for a, b in ek], np.int64)
+    got = vec.task.cpu().numpy()
+    np.testing.assert_array_equal(got[last], want[last])
+    ref = VecEnv(params, n, bm, task_ids=want)
+    rts = ref.reset_with_keys(ek[:, 0], ek[:, 1])
+    np.testing.assert_array_equal(vec.grids.cpu().numpy()[last], ref.grids.cpu().numpy()[last])
+    np.testing.assert_array_equal(vec.agent.cpu().numpy()[last], ref.agent.cpu().numpy()[last])
+    np.testing.assert_array_equal(vec.rng.cpu().numpy()[last], ref.rng.cpu().numpy()[last])
+    np.testing.assert_array_equal(ts.observations.cpu().numpy()[last], rts.observations.cpu().numpy()[last])
