@@ -102,3 +102,22 @@ def test_constructor_and_reset_errors():
     vec.reset(key_from_seed(1))
     st = vec.env_state(2)
     assert st.step_count == 0 and not st.goal_reached and st.grid.height == 9
+
+
+def test_compute_obs_false_skips_only_observations():
+    """ref vecenv.py:295 step(actions, compute_obs=False): no observation
+    record, identical rewards / discounts / step types and state."""
+    from paper_2312_12044_b200 import VecEnv, key_from_seed, load_benchmark, make, policy_keys, random_actions
+    from .helpers import benchmark_file
+    _, params = make("XLand-MiniGrid-R4-13x13")
+    bm = load_benchmark(benchmark_file("medium"))
+    a, b = VecEnv(params, 1024, bm), VecEnv(params, 1024, bm)
+    assert a.reset(key_from_seed(2), compute_obs=False).observations is None
+    b.reset(key_from_seed(2))
+    acts = random_actions(policy_keys(key_from_seed(3), 1024, device="cuda"), 0, 520)
+    for t in range(520):
+        ta, tb = a.step(acts[t], compute_obs=False), b.step(acts[t])
+        assert ta.observations is None
+        assert torch.equal(ta.rewards, tb.rewards) and torch.equal(ta.step_types, tb.step_types)
+        assert torch.equal(ta.discounts, tb.discounts)
+    assert torch.equal(a.grids, b.grids) and torch.equal(a.agent, b.agent) and torch.equal(a.rng, b.rng)
