@@ -30,7 +30,9 @@
  *   word 0 = goal, word 1 = rule_count | obj_count<<8,
  *   word 2 = bitmask of rule slots gated on MOVE, word 3 = on PICK_UP
  *   (AGENT_NEAR family / + AGENT_HOLD, ref rules.py:60-72; all ones if R > 32),
- *   words 4..4+R-1 = active rules (kind, in_a, in_b, out) left-packed,
+ *   words 4..4+R-1 = active rules (kind, in_a, in_b, out) left-packed
+ *   (AGENT_NEAR-family rules, whose in_b is 0, carry instead the neighbour
+ *   slots they try: bit k = NEAR_OFFSETS[k], up / left / right / down),
  *   then ceil(O/4) words of active object codes, left-packed; rows are
  *   padded to a multiple of 4 words (16-byte aligned 128-bit loads).
  */

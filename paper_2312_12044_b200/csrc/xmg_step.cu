@@ -183,14 +183,12 @@ struct View {
 // ref:observation.py:28-43), clipped.
 __device__ __forceinline__ void window_span(int r, int c, int d, int ext, int back, int H, int W, int V, int& lo,
                                             int& hi) {
-  const int h = V / 2;
-  int r0, r1, c0, c1;
-  switch (d) {
-    case 0: r0 = r - (V - 1) - ext; r1 = r + back; c0 = c - h; c1 = c + h; break;
-    case 1: r0 = r - h; r1 = r + h; c0 = c - back; c1 = c + (V - 1) + ext; break;
-    case 2: r0 = r - back; r1 = r + (V - 1) + ext; c0 = c - h; c1 = c + h; break;
-    default: r0 = r - h; r1 = r + h; c0 = c - (V - 1) - ext; c1 = c + back; break;
-  }
+  const int h = V / 2, far = V - 1 + ext;
+  // select-based (lanes facing different ways stay converged)
+  int r0 = d == 0 ? r - far : d == 2 ? r - back : r - h;
+  int r1 = d == 0 ? r + back : d == 2 ? r + far : r + h;
+  int c0 = d == 1 ? c - back : d == 3 ? c - far : c - h;
+  int c1 = d == 1 ? c + far : d == 3 ? c + back : c + h;
   r0 = max(r0, 0); c0 = max(c0, 0); r1 = min(r1, H - 1); c1 = min(c1, W - 1);
   lo = r0 * W + c0;
   hi = r1 * W + c1 + 1;
@@ -281,7 +279,7 @@ __device__ XMG_RARE int agent_rules(VW vw, Nbrs& nb, const uint32_t* rules, uint
     // AGENT_NEAR_{UP,RIGHT,DOWN,LEFT}: the one slot of that direction
     const uint32_t m = (uint32_t)(nb.code[0] == a) | ((uint32_t)(nb.code[1] == a) << 1) |
                        ((uint32_t)(nb.code[2] == a) << 2) | ((uint32_t)(nb.code[3] == a) << 3);
-    const uint32_t allow = kind == 2 ? 0xFu : (kind >= 8 && kind <= 11) ? (0x2841u >> (4 * (kind - 8))) & 0xFu : 0u;
+    const uint32_t allow = (rw >> 16) & 0xFu;  // the table's neighbour-slot mask (0 for AGENT_HOLD)
     const uint32_t hit = m & allow;
     if (hit) {
       const int k = __ffs(hit) - 1;

@@ -181,6 +181,14 @@ def pack_raw_rows(raw: np.ndarray, max_rules: int, max_objects: int) -> TaskTabl
                 .astype(np.uint32)
         else:
             words[:, 2] = words[:, 3] = 0xFFFFFFFF
+        # AGENT_NEAR-family rules take no second input (in_b is 0, ref
+        # rules.py:140-143): the table stores there the neighbour slots the
+        # kind tries (NEAR_OFFSETS up, left, right, down = bits 0..3), so the
+        # step kernel needs no per-kind decoding
+        rules = rules.copy()
+        allow = np.where(kinds == 2, 0xF, np.where((kinds >= 8) & (kinds <= 11),
+                                                   (0x2841 >> (4 * np.clip(kinds - 8, 0, 3))) & 0xF, 0))
+        rules[..., 2] = np.where(agent_near, allow, rules[..., 2]).astype(np.uint8)
         words[:, HEADER_WORDS:HEADER_WORDS + R] = np.ascontiguousarray(rules).view(np.uint32)[..., 0]
     if O:
         ob = np.zeros((m, 4 * ow), np.uint8)

@@ -121,7 +121,8 @@ def test_task_table_left_packs_like_the_reference():
     assert row[1] & 0xFF == 3 and (row[1] >> 8) & 0xFF == 3
     assert row[2] == 0b010 and row[3] == 0b110  # MOVE: AGENT_NEAR slot 1; PICK: + AGENT_HOLD slot 2
     rules = row[HEADER_WORDS:HEADER_WORDS + 3].view(np.uint8).reshape(3, 4)
-    assert rules.tolist() == [[3, 85, 102, 150], [2, 86, 0, 57], [1, 151, 0, 57]]
+    # AGENT_NEAR carries its neighbour-slot mask (all four) in the unused in_b byte
+    assert rules.tolist() == [[3, 85, 102, 150], [2, 86, 15, 57], [1, 151, 0, 57]]
     objs = row[HEADER_WORDS + t.rule_width:].view(np.uint8)[:3]
     assert objs.tolist() == [85, 102, 86]
     assert t.row_words % 4 == 0
