@@ -221,6 +221,17 @@ int32_t xmg_sprites(int32_t px, uint8_t* atlas /*[15][14][px][px][3]*/, void* st
 int32_t xmg_image_obs(const uint8_t* obs /*[n][v][v][2]*/, int64_t n, int32_t view, const uint8_t* atlas,
                       uint8_t* out /*[n][224][224][3]*/, void* stream);
 
+/* Faster image path for views 1..37 (tiles >= 6 px): an "aligned atlas" with
+ * every sprite row stored once per 16-byte phase the view's columns start
+ * at, so an image is written in aligned 16-byte chunks.
+ * xmg_image_atlas_bytes(view): its size (-1 if the view is outside the path);
+ * xmg_image_atlas: builds it (16-byte aligned buffer) from xmg_sprites(224 /
+ * view); xmg_image_obs_aligned: as xmg_image_obs, byte-identical output. */
+int64_t xmg_image_atlas_bytes(int32_t view);
+int32_t xmg_image_atlas(int32_t view, const uint8_t* atlas, uint8_t* aligned, void* stream);
+int32_t xmg_image_obs_aligned(const uint8_t* obs /*[n][v][v][2]*/, int64_t n, int32_t view, const uint8_t* aligned,
+                              uint8_t* out /*[n][224][224][3]*/, void* stream);
+
 /* Size in u32 words of xmg_state.work for n envs. */
 int64_t xmg_work_words(int64_t n);
 

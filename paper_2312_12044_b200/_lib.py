@@ -32,7 +32,8 @@ ACT_U8, ACT_I32, ACT_I64 = 0, 1, 2
 EXPORTS = ("xmg_abi_version", "xmg_last_error", "xmg_philox", "xmg_split_batch", "xmg_random_actions",
            "xmg_key_from_seed", "xmg_fold_in", "xmg_philox_host", "xmg_reset", "xmg_validate_actions",
            "xmg_step", "xmg_step_smem_bytes", "xmg_work_words", "xmg_profile", "xmg_profile_read", "xmg_rollout",
-           "xmg_rollout_smem_bytes", "xmg_sprites", "xmg_image_obs", "xmg_steps")
+           "xmg_rollout_smem_bytes", "xmg_sprites", "xmg_image_obs", "xmg_steps", "xmg_image_atlas_bytes",
+           "xmg_image_atlas", "xmg_image_obs_aligned")
 
 
 class NativeLibraryError(RuntimeError):
@@ -96,6 +97,9 @@ def _bind(L):
         "xmg_sprites": ([i32, vp, vp], i32),
         "xmg_steps": ([C.POINTER(EnvDesc), C.POINTER(State), vp, i32, i64, i64, C.POINTER(Out), C.c_uint32, vp], i32),
         "xmg_image_obs": ([vp, i64, i32, vp, vp, vp], i32),
+        "xmg_image_atlas_bytes": ([i32], i64),
+        "xmg_image_atlas": ([i32, vp, vp, vp], i32),
+        "xmg_image_obs_aligned": ([vp, i64, i32, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

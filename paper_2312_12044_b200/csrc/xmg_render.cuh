@@ -176,3 +176,151 @@ __global__ void __launch_bounds__(kImageWords) image_kernel(const uint8_t* __res
     }
   }
 }
+
+// ---------------------------------------------------------------- aligned path
+// For views with px >= 6 (v <= 37) the image is written in 16-byte chunks
+// straight from a phase-shifted copy of the atlas: column c's sprite rows
+// start at image-row byte D_c = 3 * (off + c * px); their phase D_c mod 16 is
+// one of at most 16 values, and the "aligned atlas" holds every sprite row
+// once per phase in use, shifted right by that phase inside a row pitch of
+// P = round16(3 * px + 15) bytes.  A 16-byte output chunk then shows at most
+// two columns (3 * px >= 18 > 16), each one aligned 16-byte load, merged with
+// byte_perm; one coalesced 16-byte store.
+struct ImgGeo {
+  int px, off, span, pitch, nphase;
+  int phase_of[37];  // column -> phase index (first-appearance order of D_c mod 16)
+  int phase_val[16];
+};
+
+__host__ __device__ inline ImgGeo make_img_geo(int v) {
+  ImgGeo g;
+  g.px = kImageSide / v;
+  g.off = (kImageSide - v * g.px) / 2;
+  g.span = v * g.px;
+  g.pitch = round16(3 * g.px + 15);
+  g.nphase = 0;
+  for (int c = 0; c < v && c < 37; ++c) {
+    const int ph = (3 * (g.off + c * g.px)) & 15;
+    int k = 0;
+    while (k < g.nphase && g.phase_val[k] != ph) ++k;
+    if (k == g.nphase) g.phase_val[g.nphase++] = ph;
+    g.phase_of[c] = k;
+  }
+  return g;
+}
+
+inline int64_t aligned_atlas_bytes(int v) {
+  const ImgGeo g = make_img_geo(v);
+  return (int64_t)g.nphase * 210 * g.px * g.pitch;
+}
+
+// aligned[p][s][sy][pitch] = sprite s row sy shifted right by phase_val[p]
+__global__ void aligned_atlas_kernel(int v, const uint8_t* __restrict__ atlas, uint8_t* __restrict__ out) {
+  const ImgGeo g = make_img_geo(v);
+  const int64_t per_row = g.pitch, rows = (int64_t)g.nphase * 210 * g.px;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * per_row) return;
+  const int64_t row = i / per_row;
+  const int b = (int)(i - row * per_row);
+  const int p = (int)(row / (210 * g.px));
+  const int64_t sr = row - (int64_t)p * 210 * g.px;  // sprite * px + sy
+  const int src = b - g.phase_val[p];
+  out[i] = (src >= 0 && src < 3 * g.px) ? atlas[sr * 3 * g.px + src] : 0;
+}
+
+constexpr int kImgChunks = kImageRow / 16;   // 42 chunks of 16 bytes per row
+constexpr int kImgRowsPar = 4;               // rows in flight per CTA
+constexpr int kImgThreads = kImgChunks * kImgRowsPar;  // 168
+constexpr int kMarginColA = 255;
+
+#ifndef XMG_IMG_MINB
+#define XMG_IMG_MINB 1
+#endif
+#ifndef XMG_IMG_UNROLL
+#define XMG_IMG_UNROLL 4
+#endif
+__global__ void __launch_bounds__(kImgThreads, XMG_IMG_MINB) image_kernel_aligned(const uint8_t* __restrict__ obs, int64_t n,
+                                                                    int v, const uint8_t* __restrict__ aligned,
+                                                                    uint8_t* __restrict__ out) {
+  __shared__ uint16_t spr[37 * 37];      // sprite index (tile * 14 + color) of cell (r, c)
+  __shared__ uint16_t rowinfo[kImageSide];  // image row -> cell row << 8 | sprite row, 0xFFFF in the margin
+  const ImgGeo g = make_img_geo(v);
+  const int t = threadIdx.x, q = t % kImgChunks, rp = t / kImgChunks;
+  for (int Y = t; Y < kImageSide; Y += blockDim.x) {
+    const int yy = Y - g.off;
+    rowinfo[Y] = (yy < 0 || yy >= g.span) ? (uint16_t)0xFFFF : (uint16_t)(((yy / g.px) << 8) | (yy % g.px));
+  }
+  // this thread's chunk: its first / last byte's column (or the margin)
+  auto col_of = [&](int b) {
+    const int x = b / 3 - g.off;
+    return (x < 0 || x >= g.span) ? kMarginColA : x / g.px;
+  };
+  const int ca = col_of(16 * q), cb = col_of(16 * q + 15);
+  const bool two = cb != ca;
+  // first byte of cb inside the chunk
+  const int tb = !two ? 16 : (cb == kMarginColA ? 3 * (g.off + g.span) : 3 * (g.off + cb * g.px)) - 16 * q;
+  // per-word merge: k = bytes of word w taken from A
+  uint32_t selw[4];
+  int takeA[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const int k = min(max(tb - 4 * w, 0), 4);
+    takeA[w] = k;
+    uint32_t sel = 0;
+    for (int j = 0; j < 4; ++j) sel |= (uint32_t)(j < k ? j : 4 + j) << (4 * j);
+    selw[w] = sel;
+  }
+  // 32-bit atlas offsets: chunk offset inside the column's aligned row plus
+  // its phase block; a sprite adds spr * sstride, a sprite row sy * pitch
+  const uint32_t sstride = (uint32_t)(g.px * g.pitch);
+  uint32_t baseA = 0, baseB = 0;
+  if (ca != kMarginColA) {
+    const int D = 3 * (g.off + ca * g.px);
+    baseA = (uint32_t)(g.phase_of[ca] * 210) * sstride + (uint32_t)(16 * q - (D - g.phase_val[g.phase_of[ca]]));
+  }
+  if (two && cb != kMarginColA) {
+    const int D = 3 * (g.off + cb * g.px);
+    baseB = (uint32_t)(g.phase_of[cb] * 210) * sstride + (uint32_t)(16 * q - (D - g.phase_val[g.phase_of[cb]]));
+  }
+  const bool loadA = ca != kMarginColA, loadB = two && cb != kMarginColA;
+  const uint32_t pitch = (uint32_t)g.pitch;
+  const uint4 shade = make_uint4(kShade, kShade, kShade, kShade);
+  for (int64_t e = blockIdx.x; e < n; e += gridDim.x) {
+    __syncthreads();  // previous image's sprite ids consumed
+    for (int k = t; k < v * v; k += blockDim.x) {
+      const int tt = obs[(e * v * v + k) * 2], cc = obs[(e * v * v + k) * 2 + 1];
+      spr[k] = (tt <= 14 && cc <= 13) ? (uint16_t)(tt * 14 + cc) : 0;  // invalid codes: END_OF_MAP
+    }
+    __syncthreads();
+    uint8_t* img = out + e * (int64_t)kImageBytes + 16 * q;
+    // kU rows per iteration: their loads are independent and go out together
+    constexpr int kU = XMG_IMG_UNROLL;
+    for (int Y0 = rp; Y0 < kImageSide; Y0 += kU * kImgRowsPar) {
+      uint4 A[kU], B[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int Y = Y0 + u * kImgRowsPar;
+        A[u] = B[u] = shade;
+        const uint32_t info = Y < kImageSide ? rowinfo[Y] : 0xFFFFu;
+        if (info != 0xFFFFu) {
+          const int i = (int)(info >> 8);
+          const uint32_t rowoff = (info & 0xFFu) * pitch;
+          if (loadA) A[u] = __ldg(reinterpret_cast<const uint4*>(aligned + baseA + spr[i * v + ca] * sstride + rowoff));
+          if (loadB) B[u] = __ldg(reinterpret_cast<const uint4*>(aligned + baseB + spr[i * v + cb] * sstride + rowoff));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int Y = Y0 + u * kImgRowsPar;
+        if (Y >= kImageSide) break;
+        const uint4 b = two ? B[u] : A[u];
+        const uint32_t a4[4] = {A[u].x, A[u].y, A[u].z, A[u].w}, b4[4] = {b.x, b.y, b.z, b.w};
+        uint32_t r4[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          r4[w] = takeA[w] == 4 ? a4[w] : takeA[w] == 0 ? b4[w] : __byte_perm(a4[w], b4[w], selw[w]);
+        *reinterpret_cast<uint4*>(img + (int64_t)Y * kImageRow) = make_uint4(r4[0], r4[1], r4[2], r4[3]);
+      }
+    }
+  }
+}

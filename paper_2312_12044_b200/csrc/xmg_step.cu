@@ -2217,6 +2217,37 @@ int32_t xmg_image_obs(const uint8_t* obs, int64_t n, int32_t view, const uint8_t
   return check_launch("image_kernel");
 }
 
+int64_t xmg_image_atlas_bytes(int32_t view) {
+  if (view < 1 || view > 37 || kImageSide / view < 6) return -1;
+  return aligned_atlas_bytes(view);
+}
+
+int32_t xmg_image_atlas(int32_t view, const uint8_t* atlas, uint8_t* aligned, void* stream) {
+  if (xmg_image_atlas_bytes(view) < 0) return fail("aligned image atlas needs view in [1, 37]");
+  if (!atlas || !aligned) return fail("null buffer");
+  if (reinterpret_cast<uintptr_t>(aligned) & 15) return fail("aligned atlas must be 16-byte aligned");
+  const int64_t total = aligned_atlas_bytes(view);
+  aligned_atlas_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(view, atlas, aligned);
+  return check_launch("aligned_atlas_kernel");
+}
+
+int32_t xmg_image_obs_aligned(const uint8_t* obs, int64_t n, int32_t view, const uint8_t* aligned, uint8_t* out,
+                              void* stream) {
+  if (xmg_image_atlas_bytes(view) < 0) return fail("aligned image path needs view in [1, 37]");
+  if (!obs || !aligned || !out) return fail("null buffer");
+  if (reinterpret_cast<uintptr_t>(out) & 15) return fail("image buffer must be 16-byte aligned");
+  if (n <= 0) return 0;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t blocks = std::min<int64_t>(n, (int64_t)sms * 12);
+  image_kernel_aligned<<<(unsigned)blocks, kImgThreads, 0, (cudaStream_t)stream>>>(obs, n, view, aligned, out);
+  return check_launch("image_kernel_aligned");
+}
+
 int64_t xmg_rollout_smem_bytes(const xmg_env_desc* desc) {
   if (!desc) return -1;
   return make_roll_geo(desc->height, desc->width, desc->view_size, desc->rule_width).total;

@@ -49,6 +49,28 @@ def sprite_atlas(px: int, device=None) -> torch.Tensor:
     return atlas
 
 
+_ALIGNED: dict[tuple[int, str], torch.Tensor] = {}
+
+
+def aligned_atlas(view: int, device=None) -> torch.Tensor | None:
+    """The phase-shifted atlas of the fast image path (xmg_image_atlas) for a
+    view of at most 37 cells, built once per (view, device); None otherwise."""
+    size = int(_lib.lib().xmg_image_atlas_bytes(view))
+    if size < 0:
+        return None
+    dev = _device(device)
+    key = (view, str(dev))
+    with _atlas_lock:
+        al = _ALIGNED.get(key)
+    if al is None:
+        base = sprite_atlas(IMAGE_SIDE // view, dev)
+        al = torch.empty(size, dtype=torch.uint8, device=dev)
+        _lib.check(_lib.lib().xmg_image_atlas(view, base.data_ptr(), al.data_ptr(), _stream(dev)), "xmg_image_atlas")
+        with _atlas_lock:
+            _ALIGNED[key] = al
+    return al
+
+
 def sprite(tile: int, color: int, px: int, device=None) -> torch.Tensor:
     """(px, px, 3) uint8 sprite of one entity code (ref render.py:158-169)."""
     if not (0 <= int(tile) <= 14 and 0 <= int(color) <= 13):
@@ -72,6 +94,11 @@ def image_observations(obs: torch.Tensor, out: torch.Tensor | None = None, check
         raise ValueError("observation holds a code outside the tile / color enums")
     if out is None:
         out = torch.empty((n, IMAGE_SIDE, IMAGE_SIDE, 3), dtype=torch.uint8, device=obs.device)
+    aligned = aligned_atlas(v, obs.device)
+    if aligned is not None:  # views up to 37 cells: aligned 16-byte chunks
+        _lib.check(_lib.lib().xmg_image_obs_aligned(obs.data_ptr(), n, v, aligned.data_ptr(), out.data_ptr(),
+                                                    _stream(obs.device)), "xmg_image_obs_aligned")
+        return out
     atlas = sprite_atlas(px, obs.device)
     _lib.check(_lib.lib().xmg_image_obs(obs.data_ptr(), n, v, atlas.data_ptr(), out.data_ptr(), _stream(obs.device)),
                "xmg_image_obs")

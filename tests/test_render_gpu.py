@@ -102,3 +102,29 @@ def test_decode_round_trip_and_errors():
     bad[0, 2, 2, 1] = 14
     with pytest.raises(ValueError):
         image_observations(bad)
+
+
+def test_aligned_and_generic_image_paths_agree():
+    """The aligned 16-byte path (views <= 37) and the word-gather path give the
+    same bytes for every odd view both cover, and agree with the oracle."""
+    from paper_2312_12044_b200 import _lib
+    from paper_2312_12044_b200.render import aligned_atlas, sprite_atlas
+    L = _lib.lib()
+    g = torch.Generator(device="cuda").manual_seed(1)
+    for v in (3, 5, 7, 9, 11, 13, 17, 21, 25, 31, 37):
+        n = 64
+        obs = torch.stack([torch.randint(0, 15, (n, v, v), device="cuda", generator=g),
+                           torch.randint(0, 14, (n, v, v), device="cuda", generator=g)], -1).to(torch.uint8)
+        a = torch.empty((n, 224, 224, 3), dtype=torch.uint8, device="cuda")
+        b = torch.empty_like(a)
+        al = aligned_atlas(v, "cuda")
+        assert al is not None
+        assert L.xmg_image_obs_aligned(obs.data_ptr(), n, v, al.data_ptr(), a.data_ptr(), None) == 0
+        base = sprite_atlas(224 // v, "cuda")
+        assert L.xmg_image_obs(obs.data_ptr(), n, v, base.data_ptr(), b.data_ptr(), None) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), v
+        if v in (3, 5, 13, 37):
+            want = O.image_observations(obs[:8].cpu().numpy())
+            assert np.array_equal(a[:8].cpu().numpy(), want), v
+    assert aligned_atlas(39, "cuda") is None  # 5-px tiles: the word-gather path
