@@ -128,6 +128,11 @@ class ClockSampler:
         return out
 
 
+def _allreduce(dist, t, op):
+    dist.all_reduce(t, op=op)
+    return t
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -218,10 +223,21 @@ def run_ours(args):
 
     from paper_2312_12044_b200 import key_from_seed, policy_keys, random_actions
     rank, world, local = dist_env()
+    # one rank per GPU over NCCL; ranks sharing a GPU (more ranks than
+    # devices: only a code-path check, the numbers mean nothing) use gloo with
+    # CPU-side collectives, since NCCL refuses two ranks on one device
+    ndev = max(torch.cuda.device_count(), 1)
+    shared = world > ndev
+    dev = torch.device("cuda", (local % ndev) if world > 1 else 0)
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local if world > 1 else 0)
+        torch.cuda.set_device(dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def coll(t: torch.Tensor) -> torch.Tensor:  # tensor placement the backend reduces
+        return t.cpu() if shared else t
     torch.cuda.set_device(dev)
     env_id, config, n, desc = WORKLOADS[args.workload]
     if args.envs:
@@ -261,14 +277,14 @@ def run_ours(args):
     vec.check()
     t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        t_max = _allreduce(dist, coll(t_max), dist.ReduceOp.MAX)
     ms_max = float(t_max.item())
     value = n * world * K / (ms_max / 1e3)
 
     # ---- episode statistics: the single collective (NCCL all-reduce, ~24 B)
     tot = vec.episode_stats()
     if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        tot = _allreduce(dist, coll(tot), dist.ReduceOp.SUM)
     tot = tot.cpu().numpy()
 
     # ---- the dominant kernel alone (roofline): the library's profiling hook
@@ -366,7 +382,7 @@ def run_ours(args):
         ems = e0.elapsed_time(e1)
         te = torch.tensor([ems], dtype=torch.float64, device=dev)
         if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            te = _allreduce(dist, coll(te), dist.ReduceOp.MAX)
         e2e = {"value": n * world * ke / (float(te.item()) / 1e3), "unit": "env-steps/s",
                "h2d_bytes_per_step": n, "d2h_bytes_per_step": n * (2 * v * v + 4 + 4 + 1), "steps": ke,
                "api": "VecEnv.step with pinned host actions in, full VecTimeStep out (double-buffered pinned "
@@ -415,7 +431,7 @@ def run_ours(args):
         bms = b0.elapsed_time(b1)
         tb = torch.tensor([bms], dtype=torch.float64, device=dev)
         if world > 1:
-            dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+            tb = _allreduce(dist, coll(tb), dist.ReduceOp.MAX)
         bms = float(tb.item())
         block = {"value": n * world * K / (bms / 1e3), "unit": "env-steps/s", "ms_per_step": bms / K,
                  "block_steps": bk,
@@ -464,7 +480,7 @@ def run_ours(args):
             fms = f0.elapsed_time(f1)
             tf = torch.tensor([fms], dtype=torch.float64, device=dev)
             if world > 1:
-                dist.all_reduce(tf, op=dist.ReduceOp.MAX)
+                tf = _allreduce(dist, coll(tf), dist.ReduceOp.MAX)
             fms = float(tf.item())
             bpe_f = (2 * v * v + 9) if rec else 0
             ach = bpe_f * n * K / (fms / 1e3) / 1e9
@@ -518,7 +534,9 @@ def run_ours(args):
             "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u8", "data": "synthetic",
             "config": {"workload": desc, "env": env_id, "rulesets": f"data/{config}-65536.xmgb" if config else None,
-                       "envs_per_gpu": n, "global_envs": n * world, "parallelism": f"env-shard x{world}",
+                       "envs_per_gpu": n, "global_envs": n * world,
+                       "parallelism": f"env-shard x{world}" + (" (ranks sharing a GPU: code-path check only)"
+                                                                 if shared else ""),
                        "timed_window": f"steps [{W + pre}, {total}) incl. budget reset burst at t={budget}",
                        "l2": "inputs larger than L2" if n * params.height * params.width > 126e6
                              else "state resident in L2 (small workload)"},
