@@ -27,7 +27,6 @@
 #endif
 constexpr int kRollWarps = XMG_ROLL_WARPS;
 constexpr int kRollKeySlots = 16;  // trial keys derived in parallel (resets go in half-warp groups)
-constexpr int kRollLg = 2;  // unused bucket area of WarpScratch (4 << kRollLg bytes)
 
 struct RollGeo {
   int hw, grids, rbw, rules, ob, obs, hwp, scratch, desc, warp_bytes;
@@ -48,7 +47,7 @@ __host__ __device__ inline RollGeo make_roll_geo(int H, int W, int V, int R) {
   g.hwp = round16(g.hw + 16);
   // WarpScratch of warp_build: wd u64[hwp] | fc u16[hwp] | slot u16[hwp] | bk | grid u8[hwp] | misc 64 u64;
   // the PUT_DOWN candidate list (u32[hw]) reuses wd (never live at once)
-  g.scratch = 12 * g.hwp + (4 << kRollLg) + g.hwp + 512;
+  g.scratch = warp_scratch_bytes(g.hwp);
   g.desc = round16((int)sizeof(xmg_env_desc));  // one copy per CTA
   g.warp_bytes = g.grids + g.rules + g.obs + g.scratch;
   g.total = (int64_t)kRollWarps * g.warp_bytes + g.desc;
@@ -83,7 +82,7 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
   uint32_t* cand = reinterpret_cast<uint32_t*>(scratch);      // aliases wd
   TrialKeys* keys = reinterpret_cast<TrialKeys*>(obs_s);      // aliases the observation buffers
   xmg_env_desc* sdesc = reinterpret_cast<xmg_env_desc*>(smem + kRollWarps * geo.warp_bytes);
-  ResetOut* rout = reinterpret_cast<ResetOut*>(make_scratch(scratch, geo.hwp, kRollLg).misc + 40);
+  ResetOut* rout = reinterpret_cast<ResetOut*>(make_scratch(scratch, geo.hwp).misc + 40);
 
   const int nvalid = (int)min((int64_t)32, n - e0);
   const int64_t e = e0 + lane;
@@ -224,7 +223,7 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
         const int src = __ffs(hm) - 1;
         const int tk = __shfl_sync(0xffffffffu, task, src);
         const uint32_t g_in = xland ? d.task_rows[(int64_t)tk * d.row_words] : 0u;
-        warp_build(sdesc, scratch, geo.hwp, kRollLg, lane, keys + (src - half), tk, g_in, grids + src * HW, rout);
+        warp_build(sdesc, scratch, geo.hwp, lane, keys + (src - half), tk, g_in, grids + src * HW, rout);
         const ResetOut ro = *rout;
         if (lane == src) {
           r = ro.r;

@@ -262,10 +262,6 @@ __device__ __forceinline__ Nbrs load_nbrs(const VW& vw, int H, int W, int ar, in
 // (ref:rules.py:80-89, ref:goals.py:287-296)
 __device__ __forceinline__ int dir_slot(int d) { return d == 0 ? 0 : d == 1 ? 2 : d == 2 ? 3 : 1; }
 
-__device__ __forceinline__ int nbr_code(const Nbrs& nb, int k) {
-  return k == 0 ? nb.code[0] : k == 1 ? nb.code[1] : k == 2 ? nb.code[2] : nb.code[3];
-}
-
 // Rules gated on MOVE / PICK_UP (only the slots in `slots`, stored order).
 // Select-based, so lanes holding different rule kinds stay converged.
 template <class VW>
@@ -461,25 +457,30 @@ struct ResetOut {
   int task;
 };
 
+// One warp's trial-build scratch (shared memory), hwp = round16(H*W + 16):
+//   wd   u64[hwp]  draw words by free-cell index
+//   fc   u16[hwp]  free cells (flat), row-major
+//   slot u16[hwp]  the object cells' element indices (rank_place)
+//   grid u8[hwp]   the trial grid under construction
+//   misc u64[64]   door words [0, 24), agent words [24, 28), spawn [32], ResetOut at [40..)
+constexpr int kScratchPad = 16;  // keeps `grid` 16-byte aligned
 struct WarpScratch {
-  uint64_t* wd;    // draw words by free-cell index
-  uint16_t* fc;    // free cells (flat), row-major
-  uint16_t* slot;  // free-cell indices in bucket order
-  uint32_t* bk;    // bucket offsets
-  uint8_t* grid;   // trial grid under construction / PUT_DOWN working copy
-  uint64_t* misc;  // 64 words: door words [0,24), agent words [24,28), results [32..)
-  int lg;
+  uint64_t* wd;
+  uint16_t* fc;
+  uint16_t* slot;
+  uint8_t* grid;
+  uint64_t* misc;
 };
 
-__device__ __forceinline__ WarpScratch make_scratch(uint8_t* wbase, int hwp, int lg) {
+__host__ __device__ inline int warp_scratch_bytes(int hwp) { return 12 * hwp + kScratchPad + hwp + 512; }
+
+__device__ __forceinline__ WarpScratch make_scratch(uint8_t* wbase, int hwp) {
   WarpScratch ws;
   ws.wd = reinterpret_cast<uint64_t*>(wbase);
   ws.fc = reinterpret_cast<uint16_t*>(wbase + 8 * hwp);
   ws.slot = reinterpret_cast<uint16_t*>(wbase + 10 * hwp);
-  ws.bk = reinterpret_cast<uint32_t*>(wbase + 12 * hwp);
-  ws.grid = wbase + 12 * hwp + 4 * (1 << lg);
+  ws.grid = wbase + 12 * hwp + kScratchPad;
   ws.misc = reinterpret_cast<uint64_t*>(ws.grid + hwp);
-  ws.lg = lg;
   return ws;
 }
 
@@ -736,13 +737,13 @@ __device__ __noinline__ void derive_trial_keys(uint64_t ek_hi, uint64_t ek_lo, b
 // (batched: ref:vecenv.py:242-291).  Called by all 32 lanes with the same
 // arguments; writes the new grid to `gdst` (and leaves it in ws.grid) and
 // returns the new pose / goal / task on every lane.
-__device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, int hwp, int lg, int lane,
+__device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, int hwp, int lane,
                                         const TrialKeys* keyp, int task_in, uint32_t goal_in, uint8_t* gdst,
                                         ResetOut* outp) {
   XMG_TRB(0);
   const TrialKeys key = *keyp;
   const xmg_env_desc& d = *dp;  // CTA copy in shared memory
-  const WarpScratch ws = make_scratch(wbase, hwp, lg);
+  const WarpScratch ws = make_scratch(wbase, hwp);
   const int H = d.height, W = d.width, HW = H * W;
   const int sc = d.scenario;
   ResetOut res;
@@ -902,7 +903,6 @@ __host__ __device__ inline int64_t pending_base(int64_t n) { return kWorkHeader 
 __host__ __device__ inline int64_t dirty_base(int64_t n) { return pending_base(n) + num_chunks(n); }
 __host__ __device__ inline int64_t work_words(int64_t n) { return pending_base(n) + 2 * num_chunks(n); }
 
-__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ ulonglong2 ld_cg_u64x2(const ulonglong2* p) {  // fresh from L2, not CSE'd
   ulonglong2 v;
@@ -1425,27 +1425,21 @@ constexpr int kKeySlots = 16;  // trial keys derived in parallel per warp (reset
 static_assert(kPutBatch <= kKeySlots, "a PUT_DOWN batch derives its finished trials' keys at once");
 
 struct RareGeo {
-  int hwp, lg, ws, rbw, keys, pgb, put;
+  int hwp, ws, rbw, keys, pgb, put;
   int64_t total;
 };
 
-__host__ __device__ inline int log2_buckets(int hw) {  // >= 5, 2^lg >= hw
-  int lg = 5;
-  while ((1 << lg) < hw) ++lg;
-  return lg;
-}
 
 __host__ __device__ inline RareGeo make_rare_geo(int H, int W, int R) {
   RareGeo g;
   g.hwp = round16(H * W + 16);
-  g.lg = 2;  // the bucket area of WarpScratch is unused since the radix-select (keep 16 bytes)
   g.rbw = round16(4 * (kRowHeader + R));
   g.keys = kKeySlots * (int)sizeof(TrialKeys);
   g.pgb = round16(H * W + 32);                      // one prefetched grid (16-byte chunks, unaligned start)
   g.put = kPutBatch * (g.pgb + g.rbw + 16) + 4 * g.hwp;  // grids | rule rows | state words | candidates
   // per warp: wd: u64[hwp] | fc: u16[hwp] | slot: u16[hwp] | bk: u32[2^lg] | grid: u8[hwp] | misc: 64 u64
   //           | rules | 32 trial keys | env description
-  g.ws = 8 * g.hwp + 2 * g.hwp + 2 * g.hwp + 4 * (1 << g.lg) + g.hwp + 512 + g.rbw + g.keys +
+  g.ws = warp_scratch_bytes(g.hwp) + g.rbw + g.keys +
          round16((int)sizeof(xmg_env_desc)) + g.put;
   g.total = (int64_t)kRareWarps * g.ws;
   return g;
@@ -1457,9 +1451,9 @@ __device__ __forceinline__ void warp_reset_env(const xmg_env_desc& d, const xmg_
                                                int64_t e, const TrialKeys* key, int task, bool reset_mode,
                                                ResetOut* rs) {
   const int H = d.height, W = d.width, HW = H * W, V = d.view_size, ob = 2 * V * V;
-  const WarpScratch ws = make_scratch(wbase, geo.hwp, geo.lg);
+  const WarpScratch ws = make_scratch(wbase, geo.hwp);
   const uint32_t g_in = d.scenario == XMG_SCENARIO_XLAND ? d.task_rows[(int64_t)task * d.row_words] : 0u;
-  warp_build(sd, wbase, geo.hwp, geo.lg, lane, key, task, g_in, s.grids + e * (int64_t)HW, rs);
+  warp_build(sd, wbase, geo.hwp, lane, key, task, g_in, s.grids + e * (int64_t)HW, rs);
   const ResetOut ro = *rs;
   if (lane == 0) {
     reinterpret_cast<ulonglong2*>(s.rng)[e] = make_ulonglong2(ro.st_hi, ro.st_lo);
@@ -1505,13 +1499,13 @@ __device__ __forceinline__ void warp_reset_group(const xmg_env_desc& d, const xm
       const int64_t es = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)e, src);
       const int ts = __shfl_sync(0xffffffffu, task, src);
       warp_reset_env(d, sd, s, o, wbase, geo, lane, es, keys + (src - half), ts, reset_keys != nullptr,
-                     reinterpret_cast<ResetOut*>(make_scratch(wbase, geo.hwp, geo.lg).misc + 40));
+                     reinterpret_cast<ResetOut*>(make_scratch(wbase, geo.hwp).misc + 40));
     }
   }
 }
 
 // step_rare drains the two queues step_main filled, one env per warp:
-//  * PUT_DOWN queue: the grid-wide rule pass, goal, reward (warp_put_event);
+//  * PUT_DOWN queue: the grid-wide rule pass, goal, reward (warp_put_env);
 //  * reset queue: the trial rebuild (warp_build), 32 envs' keys at a time.
 // Sub-queue q of each kind is served by the warps gw with gw % kQueues == q,
 // striding over its entries; warps without entries exit at once.
@@ -1571,7 +1565,7 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRar
   const int H = d.height, W = d.width, HW = H * W, V = d.view_size, ob = 2 * V * V, R = d.rule_width;
   const RareGeo geo = make_rare_geo(H, W, R);
   uint8_t* wbase = smem + warp * geo.ws;
-  const WarpScratch ws = make_scratch(wbase, geo.hwp, geo.lg);
+  const WarpScratch ws = make_scratch(wbase, geo.hwp);
   uint8_t* tail = wbase + geo.ws - geo.put;  // PUT_DOWN prefetch area
   uint32_t* rules_s = reinterpret_cast<uint32_t*>(tail - geo.rbw - geo.keys - round16((int)sizeof(xmg_env_desc)));
   TrialKeys* keys = reinterpret_cast<TrialKeys*>(tail - geo.keys - round16((int)sizeof(xmg_env_desc)));

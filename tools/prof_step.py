@@ -1,8 +1,9 @@
-"""Drive a workload to a given step for profiling (ncu -k regex:step_kernel).
+"""Drive a workload to a given step for profiling (ncu -k regex:step_).
 
-python tools/prof_step.py <workload> <pre_steps> <steps>
-step_kernel launches: 1 (reset) + pre_steps + steps, so
-`ncu -k regex:step_kernel -s <1+pre_steps> -c <steps>` captures the tail.
+python tools/prof_step.py <workload> <pre_steps> <steps> [n]
+Each step launches step_main and step_rare (validation off), after one reset
+launch of step_rare, so `ncu -k regex:step_ -s <1 + 2*pre_steps> -c <2*k>`
+captures k steps of the tail.
 """
 import os
 import sys
