@@ -130,6 +130,9 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
 
   SView vw;
   vw.stage = grids + lane * HW;
+#ifdef XMG_CHECKS
+  vw.hw = HW;
+#endif
   double st_ret = 0.0, st_trials = 0.0, st_len = 0.0;
   uint32_t acts4 = 0;
 

@@ -160,6 +160,21 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
+// ------------------------------------------------------- debug checks
+// XMG_CHECKS builds (tests/test_parity_gpu.py::test_checked_build_parity)
+// trap on any index outside the buffer it addresses: the stand-in for
+// compute-sanitizer, which this pool does not run.
+#ifdef XMG_CHECKS
+#define XMG_ASSERT(c) \
+  do {                \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define XMG_ASSERT(c) \
+  do {                \
+  } while (0)
+#endif
+
 // ------------------------------------------------------- per-thread view
 // The bytes of one env's grid staged in shared memory: stage[k] mirrors grid
 // flat index sbase + k for flat indices in [slo, shi); everything else falls
@@ -170,9 +185,11 @@ struct View {
   int sbase, slo, shi;
 
   __device__ __forceinline__ uint8_t rd(int f) const {
+    XMG_ASSERT(f >= 0);
     return (f >= slo && f < shi) ? stage[f - sbase] : g[f];
   }
   __device__ __forceinline__ void wr(int f, uint8_t v) const {
+    XMG_ASSERT(f >= 0);
     g[f] = v;
     if (f >= slo && f < shi) stage[f - sbase] = v;
   }
@@ -199,7 +216,14 @@ __device__ __forceinline__ void window_span(int r, int c, int d, int ext, int ba
 // behind for PICK_UP, whose agent-relative rules see all four neighbours),
 // so reads need no range check; writes go through to the grid in HBM.
 struct WView : View {
-  __device__ __forceinline__ uint8_t rd(int f) const { return stage[f - sbase]; }
+  __device__ __forceinline__ uint8_t rd(int f) const {
+    XMG_ASSERT(f >= slo && f < shi);  // the invariant that makes the unchecked read safe
+    return stage[f - sbase];
+  }
+  __device__ __forceinline__ void wr(int f, uint8_t v) const {
+    XMG_ASSERT(f >= slo && f < shi);
+    View::wr(f, v);
+  }
 };
 
 // Stage grid bytes [lo, hi) of this thread's env with 16-byte cp.async
@@ -241,8 +265,21 @@ struct Nbrs {
 // A grid staged whole in shared memory (the rollout kernel): no range checks.
 struct SView {
   uint8_t* stage;
-  __device__ __forceinline__ uint8_t rd(int f) const { return stage[f]; }
-  __device__ __forceinline__ void wr(int f, uint8_t v) const { stage[f] = v; }
+#ifdef XMG_CHECKS
+  int hw = 1 << 30;
+#endif
+  __device__ __forceinline__ uint8_t rd(int f) const {
+#ifdef XMG_CHECKS
+    XMG_ASSERT(f >= 0 && f < hw);
+#endif
+    return stage[f];
+  }
+  __device__ __forceinline__ void wr(int f, uint8_t v) const {
+#ifdef XMG_CHECKS
+    XMG_ASSERT(f >= 0 && f < hw);
+#endif
+    stage[f] = v;
+  }
 };
 
 template <class VW>
@@ -1142,6 +1179,7 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
       if (lane == leader) base = atomicAdd(s.work + count_index(epoch, kind, k), (uint32_t)__popc(km));
       base = __shfl_sync(0xffffffffu, base, leader);
       if (qflags == want) {
+        XMG_ASSERT(base + __popc(km & ((1u << lane) - 1)) < queue_cap(n));
         s.work[queue_base(n, epoch, kind, k) + base + __popc(km & ((1u << lane) - 1))] = (uint32_t)e;
       }
     }
@@ -1346,6 +1384,7 @@ __device__ __noinline__ int warp_put_env(uint8_t* G, uint8_t* genv, uint32_t* ca
       s0 += 32;
       continue;
     }
+    XMG_ASSERT(p >= 0 && p < HW && q < HW);
     const int old = G[p];
     __syncwarp();
     if (lane == 0) {

@@ -233,3 +233,28 @@ print("ok")
     env = dict(os.environ, **knobs)
     res = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0 and "ok" in res.stdout, res.stderr[-3000:]
+
+
+@pytest.mark.parametrize("env_name,config", [("XLand-MiniGrid-R4-13x13", "medium"),
+                                             ("XLand-MiniGrid-R9-25x25", "high"),
+                                             ("MiniGrid-DoorKey-8x8", None)])
+def test_checked_build_parity(env_name, config):
+    """The XMG_CHECKS build (device asserts on every window / grid / queue
+    index) runs the soak workload -- pipelined steps with a slice vs the
+    oracle every step, then the fused rollout vs the stepped state -- without
+    a trap (compute-sanitizer is not available on this pool)."""
+    import os
+    import subprocess
+    import sys
+    from .conftest import ROOT
+    lib = os.path.join(ROOT, "paper_2312_12044_b200", "libxmg_checked.so")
+    assert os.path.exists(lib), "build() makes libxmg_checked.so"
+    env = dict(os.environ, XMG_LIB=lib)
+    args = [sys.executable, os.path.join(ROOT, "tools", "soak.py"), "1100", "8192", env_name]
+    if config:
+        args.append(config)
+    res = subprocess.run(args, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-3000:]
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize.py"), "1000"], cwd=ROOT, env=env,
+                         capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-3000:]

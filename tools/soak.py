@@ -21,15 +21,20 @@ from paper_2312_12044_b200 import VecEnv, key_from_seed, load_benchmark, make, p
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 16
 env_name = sys.argv[3] if len(sys.argv) > 3 else "XLand-MiniGrid-R4-13x13"
-config = sys.argv[4] if len(sys.argv) > 4 else "medium"
+config = sys.argv[4] if len(sys.argv) > 4 else ("medium" if env_name.startswith("XLand") else None)
 _, params = make(env_name)
-bm = load_benchmark(benchmark_file(config))
-table = bm.task_table()
+if config:
+    bm = load_benchmark(benchmark_file(config))
+    table = bm.task_table()
+else:
+    from paper_2312_12044_b200.ruleset import TaskTable
+    bm = None
+    table = TaskTable(np.zeros((1, 4), np.uint32), 0, 0, 0)
 vec = VecEnv(params, n, bm, reuse_outputs=True)
 root, pol = key_from_seed(123), key_from_seed(456)
 vec.reset(root)
 w, off = 256, n // 3
-ids = (np.arange(off, off + w) % table.num_tasks).astype(np.int64)
+ids = (np.arange(off, off + w) % table.num_tasks).astype(np.int64) if config else np.zeros(w, np.int64)
 ora = oracle_from_table(params, table, ids)
 k0, k1 = O.split_batch((root.hi, root.lo), w, offset=off)
 ora.reset_with_keys(k0, k1)
