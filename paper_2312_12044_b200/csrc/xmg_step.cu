@@ -1459,7 +1459,7 @@ constexpr int kPutBatch = 8;  // PUT_DOWN envs a step_rare warp prefetches toget
 #define XMG_RARE_WARPS 4
 #endif
 constexpr int kRareWarps = XMG_RARE_WARPS;  // warps per step_rare CTA (each warp owns its scratch)
-constexpr int kRareWarpsPerSM = 20;         // resident step_rare warps per SM (see launch_rare_k)
+constexpr int kRareWarpsPerSM = 20;         // resident step_rare warps per SM (see launch_rare)
 constexpr int kKeySlots = 16;  // trial keys derived in parallel per warp (resets go in half-warp groups)
 static_assert(kPutBatch <= kKeySlots, "a PUT_DOWN batch derives its finished trials' keys at once");
 
@@ -1551,7 +1551,6 @@ __device__ __forceinline__ void warp_reset_group(const xmg_env_desc& d, const xm
 // reset_keys != nullptr: reset mode (ref VecEnv.reset_with_keys,
 // vecenv.py:205-222), every env [0, n) rebuilt from keys[e] with a FIRST
 // record.
-template <int KMAX>
 __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRareWarps) step_rare(const xmg_env_desc d, const xmg_state s,
                                                                      const xmg_out o, const uint64_t* reset_keys,
                                                                      const uint32_t* abort_flag, uint32_t epoch,
@@ -1911,18 +1910,16 @@ int launch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, con
   return check_launch("step_main");
 }
 
-int kmax_of(const xmg_env_desc* d) {
-  const int K = (d->height * d->width + 31) / 32;
-  return K <= 4 ? 4 : K <= 8 ? 8 : K <= 20 ? 20 : K <= 32 ? 32 : 0;
-}
+// grids up to 1024 cells: the PUT_DOWN candidate lists and the radix select
+// of the trial builds assume it
+bool grid_fits(const xmg_env_desc* d) { return d->height * d->width <= 1024; }
 
-template <int KMAX>
-int launch_rare_k(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const uint64_t* keys,
-                  const uint32_t* flag, uint32_t epoch, int64_t n, int track, cudaStream_t st) {
+int launch_rare(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const uint64_t* keys,
+                const uint32_t* flag, uint32_t epoch, int64_t n, int track, cudaStream_t st) {
   const RareGeo geo = make_rare_geo(d->height, d->width, d->rule_width);
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] { attr_err = allow_smem(step_rare<KMAX>, kMaxDynSmem - 1024); });
+  std::call_once(once, [] { attr_err = allow_smem(step_rare, kMaxDynSmem - 1024); });
   if (attr_err != cudaSuccess) return fail(std::string("step_rare attributes: ") + cudaGetErrorString(attr_err));
   // one resident wave (warps stride over their sub-queue's entries); a
   // multiple of 32 CTAs so every sub-queue gets equal warps
@@ -1937,7 +1934,7 @@ int launch_rare_k(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, c
   static thread_local int64_t cached_smem = -1;
   static thread_local int cached_per_sm = 0;
   if (cached_smem != geo.total) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per_sm, step_rare<KMAX>, kRareWarps * 32,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per_sm, step_rare, kRareWarps * 32,
                                                       (size_t)geo.total) !=
         cudaSuccess)
       cached_per_sm = 0;
@@ -1961,20 +1958,11 @@ int launch_rare_k(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, c
   const int64_t need = ((n + kRareWarps * 64 - 1) / (kRareWarps * 64) + unit - 1) / unit * unit;  // <= a warp / 64 envs
   if (blocks > need) blocks = need;
   if (blocks < unit) blocks = unit;
-  step_rare<KMAX><<<(unsigned)blocks, kRareWarps * 32, (size_t)geo.total, st>>>(*d, *s, *o, keys, flag, epoch, n,
+  step_rare<<<(unsigned)blocks, kRareWarps * 32, (size_t)geo.total, st>>>(*d, *s, *o, keys, flag, epoch, n,
                                                                                 track);
   return check_launch("step_rare");
 }
 
-int launch_rare(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const uint64_t* keys,
-                const uint32_t* flag, uint32_t epoch, int64_t n, int track, cudaStream_t st) {
-  switch (kmax_of(d)) {
-    case 4: return launch_rare_k<4>(d, s, o, keys, flag, epoch, n, track, st);
-    case 8: return launch_rare_k<8>(d, s, o, keys, flag, epoch, n, track, st);
-    case 20: return launch_rare_k<20>(d, s, o, keys, flag, epoch, n, track, st);
-    default: return launch_rare_k<32>(d, s, o, keys, flag, epoch, n, track, st);
-  }
-}
 
 int validate_desc(const xmg_env_desc* d, const xmg_state* s, int64_t n) {
   if (!d) return fail("null env description");
@@ -1990,7 +1978,7 @@ int validate_desc(const xmg_env_desc* d, const xmg_state* s, int64_t n) {
   if (d->num_tasks < 1) return fail("empty task table");
   if (!d->base_cells || !d->task_rows) return fail("null base_cells / task_rows");
   if (pick_maxch(d) == 0) return fail("view window too wide for this build (v*W + v > 482)");
-  if (kmax_of(d) == 0) return fail("grid too large for this build (H*W <= 1024)");
+  if (!grid_fits(d)) return fail("grid too large for this build (H*W <= 1024)");
   if (make_main_geo(d->view_size, pick_maxch(d), d->rule_width).total > kMaxDynSmem - 1024 ||
       make_rare_geo(d->height, d->width, d->rule_width).total > kMaxDynSmem - 1024)
     return fail("grid too large for the shared-memory scratch of this build (H*W <= ~3000)");
