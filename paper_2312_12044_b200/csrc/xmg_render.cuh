@@ -259,13 +259,12 @@ __global__ void __launch_bounds__(kImgThreads, XMG_IMG_MINB) image_kernel_aligne
   const bool two = cb != ca;
   // first byte of cb inside the chunk
   const int tb = !two ? 16 : (cb == kMarginColA ? 3 * (g.off + g.span) : 3 * (g.off + cb * g.px)) - 16 * q;
-  // per-word merge: k = bytes of word w taken from A
+  // per-word merge selectors: the first k = tb - 4w bytes of word w from A,
+  // the rest from B (0x3210 = all A, 0x7654 = all B)
   uint32_t selw[4];
-  int takeA[4];
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
     const int k = min(max(tb - 4 * w, 0), 4);
-    takeA[w] = k;
     uint32_t sel = 0;
     for (int j = 0; j < 4; ++j) sel |= (uint32_t)(j < k ? j : 4 + j) << (4 * j);
     selw[w] = sel;
@@ -313,13 +312,10 @@ __global__ void __launch_bounds__(kImgThreads, XMG_IMG_MINB) image_kernel_aligne
       for (int u = 0; u < kU; ++u) {
         const int Y = Y0 + u * kImgRowsPar;
         if (Y >= kImageSide) break;
-        const uint4 b = two ? B[u] : A[u];
-        const uint32_t a4[4] = {A[u].x, A[u].y, A[u].z, A[u].w}, b4[4] = {b.x, b.y, b.z, b.w};
-        uint32_t r4[4];
-#pragma unroll
-        for (int w = 0; w < 4; ++w)
-          r4[w] = takeA[w] == 4 ? a4[w] : takeA[w] == 0 ? b4[w] : __byte_perm(a4[w], b4[w], selw[w]);
-        *reinterpret_cast<uint4*>(img + (int64_t)Y * kImageRow) = make_uint4(r4[0], r4[1], r4[2], r4[3]);
+        const uint4 a = A[u], b = B[u];  // B == shade when the chunk shows one column (selectors: all A)
+        *reinterpret_cast<uint4*>(img + (int64_t)Y * kImageRow) =
+            make_uint4(__byte_perm(a.x, b.x, selw[0]), __byte_perm(a.y, b.y, selw[1]),
+                       __byte_perm(a.z, b.z, selw[2]), __byte_perm(a.w, b.w, selw[3]));
       }
     }
   }
