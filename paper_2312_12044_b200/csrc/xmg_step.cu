@@ -376,16 +376,23 @@ __device__ __forceinline__ void obs_see(const uint8_t* stage, int sbase, uint8_t
   if constexpr (VV != 0) {
     constexpr int NC = VV * VV;
     uint32_t cd[NC + 1];  // entity codes, view cell order (+ a zero pad)
+    int jo[VV];           // column offsets, once per view (not per cell)
+#pragma unroll
+    for (int j = 0; j < VV; ++j) jo[j] = j * dj;
+    static_assert(VV * VV <= 32, "the cell mask is one 32-bit word");
+    uint32_t m25 = 0;  // validity of every view cell: bit i*VV + j = mi bit i and mj bit j
+#pragma unroll
+    for (int i = 0; i < VV; ++i) m25 |= (((mi >> i) & 1u) ? mj : 0u) << (i * VV);
+    const uint8_t* pi = p0;
 #pragma unroll
     for (int i = 0; i < VV; ++i) {
-      const bool vi = (mi >> i) & 1;
-      const uint8_t* pi = p0 + i * di;
 #pragma unroll
       for (int j = 0; j < VV; ++j) {
         uint32_t code = 0;
-        if (vi && ((mj >> j) & 1)) code = pi[j * dj];
+        if ((m25 >> (i * VV + j)) & 1u) code = pi[jo[j]];
         cd[i * VV + j] = code;
       }
+      pi += di;
     }
     cd[NC] = 0;
     // two cells -> one (tile, color, tile, color) word: pack the codes, split
