@@ -258,3 +258,40 @@ def test_checked_build_parity(env_name, config):
     res = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize.py"), "1000"], cwd=ROOT, env=env,
                          capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stderr[-3000:]
+
+
+@pytest.mark.parametrize("env_name,config,v,see", [
+    ("XLand-MiniGrid-R9-25x25", "high", 9, True),
+    ("XLand-MiniGrid-R6-19x19", "medium", 11, True),
+    ("MiniGrid-DoorKey-16x16", None, 3, True),
+    ("XLand-MiniGrid-R2-17x17", "small", 7, False),
+    ("MiniGrid-EmptyRandom-16x16", None, 13, True),
+])
+def test_view_sizes_and_layouts_vs_oracle(env_name, config, v, see):
+    """Non-default views (3..13 cells: other window chunk counts / generic
+    observation path), R6 fixed doors, occlusion at v=7, 16x16 ports."""
+    from dataclasses import replace
+    from paper_2312_12044_b200 import VecEnv, key_from_seed, load_benchmark, make, policy_keys, random_actions
+    from paper_2312_12044_b200.ruleset import TaskTable
+    _, params = make(env_name)
+    params = replace(params, view_size=v, see_through_walls=see)
+    n, steps = 1024, min(params.step_budget + 5, 800)
+    if config:
+        bm = load_benchmark(benchmark_file(config))
+        vec = VecEnv(params, n, bm)
+        ora = oracle_from_table(params, bm.task_table(), vec._ids_host)
+    else:
+        vec = VecEnv(params, n)
+        ora = oracle_from_table(params, TaskTable(np.zeros((1, 4), np.uint32), 0, 0, 0), np.zeros(n, np.int64))
+    root = key_from_seed(5)
+    np.testing.assert_array_equal(vec.reset(root).observations.cpu().numpy(), ora.reset(root))
+    acts = random_actions(policy_keys(key_from_seed(6), n, device=vec.device), 0, steps)
+    ah = acts.cpu().numpy()
+    for t in range(steps):
+        ts = vec.step(acts[t])
+        o, r, d, s = ora.step(ah[t])
+        np.testing.assert_array_equal(ts.observations.cpu().numpy(), o, err_msg=f"obs t={t}")
+        np.testing.assert_array_equal(ts.rewards.cpu().numpy(), r.astype(np.float32))
+        np.testing.assert_array_equal(ts.step_types.cpu().numpy(), s)
+    np.testing.assert_array_equal(vec.grids.cpu().numpy(), ora.grids)
+    vec.check()
