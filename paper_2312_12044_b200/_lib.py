@@ -17,7 +17,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB_PATH = os.environ.get("XMG_LIB") or os.path.join(PKG, "libxmg.so")
 SOURCES = [os.path.join(PKG, "csrc", "xmg_step.cu")]
-DEPENDS = [os.path.join(PKG, "csrc", "xmg_rollout.cuh"), os.path.join(PKG, "csrc", "xmg_render.cuh")]
+DEPENDS = [os.path.join(PKG, "csrc", f) for f in ("xmg_common.cuh", "xmg_build.cuh", "xmg_main.cuh", "xmg_rare.cuh",
+                                                  "xmg_rollout.cuh", "xmg_render.cuh")]
 HEADER = os.path.join(ROOT, "include", "xmg.h")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xptxas", "-v", "-shared", "-Xcompiler", "-fPIC"]

@@ -1,0 +1,329 @@
+// xmg_main.cuh — the streaming step kernel step_main and the work-queue
+// layout it shares with step_rare (included by xmg_step.cu inside its
+// anonymous namespace).
+
+// ------------------------------------------------------- the step: two kernels
+// step_main (one thread per env, streaming) applies the action, the
+// agent-relative rules / goals of MOVE and PICK_UP, the counters, reward and
+// observation of every env, and defers the two rare cases into a work queue:
+//   * PUT_DOWN events (grid-wide TILE_NEAR rules / goals, ref:rules.py:60-72),
+//   * finished trials (auto-reset, ref:vecenv.py:359-361).
+// step_rare (one warp per queued env) drains the queue: the PUT_DOWN rule
+// pass + goal + reward, the trial rebuild, and the observation of every env
+// it touched.  Both run back to back on the caller's stream.
+//
+// Work queues (state.work, xmg_work_words(n) u32): a PUT_DOWN queue and a
+// reset queue, each split in kQueues sub-queues fed by the CTAs with
+// blockIdx % kQueues == k (spreads the atomics).  Counts are double-buffered
+// by step parity: step t appends to counts[t & 1] while its CTA 0 clears
+// counts[(t + 1) & 1] (consumed by the previous step), so no kernel ever
+// waits for another.  Layout: counts [2 parities][2 kinds][kQueues], then the
+// PUT entries (kQueues x queue_cap) and the reset entries (kQueues x queue_cap).
+constexpr int kQueues = 128;
+constexpr int kWorkHeader = 4 * kQueues;
+__host__ __device__ inline int count_index(uint32_t parity, int kind, int q) {
+  return (int)((parity & 1) * 2 * kQueues + kind * kQueues + q);
+}
+constexpr uint32_t kQPut = 1u << 31, kQReset = 1u << 30, kQEnv = (1u << 30) - 1;
+
+// capacity of one sub-queue: every env of the step_main CTAs (128 envs each) feeding it
+__host__ __device__ inline int64_t queue_cap(int64_t n) {
+  const int64_t blocks = (n + kThreads - 1) / kThreads;
+  return (blocks + kQueues - 1) / kQueues * kThreads;
+}
+
+// Entry slots of sub-queue (parity, kind, q): double-buffered like the counts,
+// so step t + 1's step_main appends while step t's step_rare still drains.
+__host__ __device__ inline int64_t queue_base(int64_t n, uint32_t parity, int kind, int q) {
+  return kWorkHeader + ((int64_t)(parity & 1) * 2 * kQueues + kind * kQueues + q) * queue_cap(n);
+}
+
+// Chunk bookkeeping after the queues (chunk = the 32 envs of one step_main warp):
+//   pending[nchunks]  queued envs of the chunk step_rare has not finished yet
+//   dirty[nchunks]    epoch of the last step that queued envs of the chunk
+// Only the chunk's own warp reads and writes its dirty word, so the tag needs
+// no clearing.
+__host__ __device__ inline int64_t num_chunks(int64_t n) { return (n + kThreads - 1) / kThreads * kWarps; }
+__host__ __device__ inline int64_t pending_base(int64_t n) { return kWorkHeader + 4 * kQueues * queue_cap(n); }
+__host__ __device__ inline int64_t dirty_base(int64_t n) { return pending_base(n) + num_chunks(n); }
+__host__ __device__ inline int64_t work_words(int64_t n) { return pending_base(n) + 2 * num_chunks(n); }
+
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ ulonglong2 ld_cg_u64x2(const ulonglong2* p) {  // fresh from L2, not CSE'd
+  ulonglong2 v;
+  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ int load_action(const void* a, int dtype, int64_t e) {
+  switch (dtype) {
+    case XMG_ACT_U8: return reinterpret_cast<const uint8_t*>(a)[e];
+    case XMG_ACT_I32: return reinterpret_cast<const int32_t*>(a)[e];
+    default: return (int)reinterpret_cast<const int64_t*>(a)[e];
+  }
+}
+
+__device__ __forceinline__ uint64_t pack_agent(int r, int c, int d, int pocket, uint32_t sc) {
+  return (uint64_t)(uint32_t)r | ((uint64_t)(uint32_t)c << 8) | ((uint64_t)(uint32_t)d << 16) |
+         ((uint64_t)(uint32_t)pocket << 24) | ((uint64_t)sc << 32);
+}
+
+// float32(1.0 - 0.9 * (sc / budget)) in IEEE double without contraction
+// (ref:env.py:204, ref:vecenv.py:355)
+__device__ __forceinline__ float goal_reward(uint32_t sc, int budget) {
+  const double frac = __ddiv_rn((double)sc, (double)budget);
+  return __double2float_rn(__dsub_rn(1.0, __dmul_rn(0.9, frac)));
+}
+
+// Per-CTA episode statistics slot (ref RolloutStats, harness.py:314-354).
+__device__ __forceinline__ void warp_stats(double* stats, int slot, double rs, double trl, double ln) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    rs += __shfl_down_sync(0xffffffffu, rs, off);
+    trl += __shfl_down_sync(0xffffffffu, trl, off);
+    ln += __shfl_down_sync(0xffffffffu, ln, off);
+  }
+  if ((threadIdx.x & 31) == 0 && trl + rs > 0.0) {
+    atomicAdd(stats + 3 * slot, rs);
+    atomicAdd(stats + 3 * slot + 1, trl);
+    atomicAdd(stats + 3 * slot + 2, ln);
+  }
+}
+
+struct MainGeo {
+  int ob, stg, rb;
+  int64_t total;
+};
+
+__host__ __device__ inline MainGeo make_main_geo(int V, int maxch, int R) {
+  MainGeo g;
+  g.ob = 2 * V * V;
+  g.stg = 16 * maxch + 16;
+  // per-lane rule row; after the rule pass the warp's 32 rule rows hold its
+  // 32 observation records (the staging area of the bulk store)
+  g.rb = max(16 * ((kRowHeader + R + 3) / 4), round16(g.ob));
+  g.total = (int64_t)kThreads * (g.stg + g.rb);
+  return g;
+}
+
+// abort iff *flag == epoch: xmg_validate_actions tags a rejected batch with
+// the epoch of its step (atomicMax), so the flag never needs clearing.
+__device__ __forceinline__ bool batch_rejected(const uint32_t* flag, uint32_t epoch) {
+  return flag != nullptr && *reinterpret_cast<volatile const uint32_t*>(flag) == epoch;
+}
+
+// FULL: small grids are staged whole, issued before the state word arrives
+// (one DRAM round trip per env instead of two: state word -> view window).
+template <int MAXCH, bool FULL>
+__global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_desc d, const xmg_state s,
+                                                                const xmg_out o, const void* actions, int act_dtype,
+                                                                const uint32_t* abort_flag, uint32_t epoch,
+                                                                int64_t n) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // Launched as a programmatic dependent of the previous kernel (the previous
+  // step's step_rare, or this step's validation), so it runs concurrently with
+  // the previous step_rare: with a validation it waits for the verdict, and
+  // per 32-env chunk it waits only where the previous step queued envs (below).
+  if (abort_flag != nullptr) {  // this epoch's validation verdict (published by its last CTA)
+    if (lane == 0)
+      for (uint32_t spins = 0; ld_acquire(abort_flag + 1) != epoch; ++spins) {
+        if (spins > (1u << 25)) __trap();
+        __nanosleep(64);
+      }
+    __syncwarp();
+  }
+  // the previous step_rare has read these counts (it reads them before it
+  // lets this grid launch); this step appends to the other parity
+  if (blockIdx.x == 0)
+    for (int i = tid; i < 2 * kQueues; i += blockDim.x) s.work[count_index(epoch + 1, 0, 0) + i] = 0;
+  if (batch_rejected(abort_flag, epoch)) return;
+
+  const int H = d.height, W = d.width, HW = H * W, V = d.view_size, R = d.rule_width;
+  const MainGeo geo = make_main_geo(V, MAXCH, R);
+  const int64_t tile = blockIdx.x;
+  const int64_t e0 = tile * kThreads;
+  const int64_t chunk = tile * kWarps + warp;
+  uint32_t* pending = s.work + pending_base(n) + chunk;
+  uint32_t* dirty = s.work + dirty_base(n) + chunk;
+  const int64_t e = e0 + tid;
+  const bool valid = e < n;
+
+  uint8_t* rb_base = smem + kThreads * geo.stg;
+  uint8_t* obs_stage = rb_base + warp * 32 * geo.rb;  // aliases the warp's rule rows
+  WView vw;
+  vw.g = s.grids + (valid ? e : 0) * (int64_t)HW;
+  vw.stage = smem + tid * geo.stg;
+  vw.sbase = vw.slo = vw.shi = 0;
+  uint32_t* rbuf = reinterpret_cast<uint32_t*>(rb_base + tid * geo.rb);
+  if (FULL && valid) stage_issue<MAXCH>(vw, 0, HW, HW);
+
+  // ---- load: the 16-byte state word and the action
+  ulonglong2 ag = make_ulonglong2(0, 0);
+  int act = 1;
+  const uint32_t was_dirty = e0 + warp * 32 < n ? *dirty : 0u;  // issued together with the state loads
+  if (valid) {
+    ag = reinterpret_cast<const ulonglong2*>(s.agent)[e];
+    act = load_action(actions, act_dtype, e);
+  }
+  if (was_dirty == epoch - 1 && e0 + warp * 32 < n) {
+    // the previous step queued envs of this chunk: wait until its step_rare has
+    // released them all, then reload the state word it may have rewritten
+    if (lane == 0) {
+      // bounded: a lost release is a bug, trap (launch error) rather than hang
+      for (uint32_t spins = 0; ld_acquire(pending) != 0; ++spins) {
+        if (spins > (1u << 25)) __trap();
+        __nanosleep(128);
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncwarp();
+    if (valid) ag = ld_cg_u64x2(reinterpret_cast<const ulonglong2*>(s.agent) + e);
+    if (FULL && valid) {  // the early grid copy may predate step_rare's writes
+      cp_async_wait_all();
+      stage_issue<MAXCH>(vw, 0, HW, HW);
+    }
+  }
+  int r = (int)(ag.x & 0xff), c = (int)((ag.x >> 8) & 0xff), dir = (int)((ag.x >> 16) & 3);
+  int pocket = (int)((ag.x >> 24) & 0xff);
+  uint32_t sc = (uint32_t)(ag.x >> 32);
+  const uint32_t goal_word = (uint32_t)ag.y;
+  const int task = (int)(ag.y >> 32);
+
+  uint32_t qflags = 0;
+  float rew = 0.f;
+  bool last = false;
+  if (valid) {
+    // ---- stage the post-action window (MOVE: both candidate poses) and,
+    // for actions that can raise an event, the env's rule row
+    const int nd = act == 1 ? ((dir + 3) & 3) : (act == 2 ? ((dir + 1) & 3) : dir);
+    if (!FULL) {
+      int lo, hi;
+      window_span(r, c, nd, act == 0 ? 1 : 0, act == 3 ? 1 : 0, H, W, V, lo, hi);
+      stage_issue<MAXCH>(vw, lo, hi, HW);
+    }
+    const bool rules_needed = R > 0 && (act == 0 || act == 3);
+    if (rules_needed) {
+      const uint32_t* src = d.task_rows + (int64_t)task * d.row_words;
+      const int nq = (kRowHeader + R + 3) >> 2;
+      for (int q = 0; q < nq; ++q) cp_async16(rbuf + 4 * q, src + 4 * q);
+    }
+    cp_async_wait_all();
+
+    // ---- action, ref:vecenv.py:306-342 / ref:env.py:148-191
+    const int tr = r + dir_dr(dir), tc = c + dir_dc(dir);
+    const bool inside = tr >= 0 && tr < H && tc >= 0 && tc < W;
+    const int tflat = tr * W + tc;
+    // (turns stage the new facing's window, which need not hold the old target)
+    const int tcode = (inside && act != 1 && act != 2) ? vw.rd(tflat) : 0, tt = tcode >> 4;
+    // select-based: lanes with different actions stay converged
+    const bool mv = act == 0 && inside && ((kWalkable >> tt) & 1);
+    const bool pk = act == 3 && inside && pocket == 0 && ((kPickable >> tt) & 1);
+    const bool pt = act == 4 && inside && pocket != 0 && tt == kFloor;
+    const bool tg = act == 5 && inside && (tt == kClosed || (tt == kLocked && pocket == kKey * 16 + (tcode & 15)));
+    const int ev = mv ? 0 : pk ? 1 : pt ? 2 : tg ? 3 : -1;
+    const int wval = pk ? kFloorCode : pt ? pocket : kOpen * 16 + (tcode & 15);
+    r = mv ? tr : r;
+    c = mv ? tc : c;
+    dir = nd;  // nd == dir unless turning
+    pocket = pk ? tcode : pt ? 0 : pocket;
+    if (pk || pt || tg) vw.wr(tflat, (uint8_t)wval);
+    // ---- MOVE / PICK_UP: agent-relative rules (only the slots their event
+    // gates, in stored order) and goal; TOGGLE gates no rule and no goal.
+    bool goal = false;
+    if (ev == 0 || ev == 1) {
+      Nbrs nb = load_nbrs(vw, H, W, r, c);
+      const int nr = R > 0 ? (int)(rbuf[1] & 0xff) : 0;
+      if (nr) {
+        if (R <= 32) {
+          const uint32_t slots = rbuf[2 + ev];
+          if (slots) pocket = agent_rules(vw, nb, rbuf + kRowHeader, slots, pocket);
+        } else {  // wide tables: gate every slot here
+          for (int s0 = 0; s0 < nr; ++s0) {
+            const int kind = rbuf[kRowHeader + s0] & 0xff;
+            if (kind >= 1 && kind <= 11 && ((cRuleGate[kind] >> ev) & 1))
+              pocket = agent_rules(vw, nb, rbuf + kRowHeader + s0, 1u, pocket);
+          }
+        }
+      }
+      goal = agent_goal(nb, vw.rd(r * W + c), goal_word, ev, r, c, pocket);
+    }
+    // ---- counters and reward, ref:vecenv.py:351-357
+    sc += 1;
+    if (ev == 2) {
+      qflags = kQPut;  // rules, goal and reward resolved by step_rare
+    } else {
+      last = goal || sc >= (uint32_t)d.budget;
+      if (goal) rew = goal_reward(sc, d.budget);
+      o.reward[e] = rew;
+      o.discount[e] = last ? 0.f : 1.f;
+      o.step_type[e] = last ? 2 : 1;
+      if (last) qflags = kQReset;
+    }
+    s.agent[2 * e] = pack_agent(r, c, dir, pocket, sc);
+  }
+
+  // ---- defer the rare work: warp-aggregated append to this CTA's sub-queue
+  const uint32_t qm = __ballot_sync(0xffffffffu, qflags != 0);
+  if (qm) {
+    const int k = (int)(tile % kQueues);
+    if (lane == 0) {
+      atomicAdd(pending, (uint32_t)__popc(qm));
+      *dirty = epoch;
+    }
+    // PUT_DOWN and reset entries go to their own queues
+#pragma unroll
+    for (int kind = 0; kind < 2; ++kind) {
+      const uint32_t want = kind ? kQReset : kQPut;
+      const uint32_t km = __ballot_sync(0xffffffffu, qflags == want);
+      if (!km) continue;
+      const int leader = __ffs(km) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(s.work + count_index(epoch, kind, k), (uint32_t)__popc(km));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (qflags == want) {
+        XMG_ASSERT(base + __popc(km & ((1u << lane) - 1)) < queue_cap(n));
+        s.work[queue_base(n, epoch, kind, k) + base + __popc(km & ((1u << lane) - 1))] = (uint32_t)e;
+      }
+    }
+  }
+
+  // ---- episode statistics of the trials decided here
+  if (o.stats != nullptr) warp_stats(o.stats, (int)tile, rew, last ? 1.0 : 0.0, last ? (double)sc : 0.0);
+
+
+  // ---- observation: assembled in smem, one TMA bulk store per warp
+  // (envs queued for step_rare get theirs rewritten there)
+  if (o.obs != nullptr) {
+    __syncwarp();  // every lane is done with its rule row
+    if (valid) {
+      uint8_t* dst = obs_stage + lane * geo.ob;
+      if (d.see_through_walls) {
+        if (V == 5) obs_see<5>(vw.stage, vw.sbase, dst, r, c, dir, H, W, V);
+        else obs_see<0>(vw.stage, vw.sbase, dst, r, c, dir, H, W, V);
+      } else {
+        obs_occluded(vw, dst, r, c, dir, H, W, V);
+      }
+    }
+    const int64_t w0 = e0 + warp * 32;
+    const int nvalid = (int)max((int64_t)0, min((int64_t)32, n - w0));
+    const uint32_t bytes = (uint32_t)(nvalid * geo.ob);
+    const uint32_t bulk = bytes & ~15u;
+    uint8_t* gdst = o.obs + w0 * geo.ob;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0 && bulk) {
+      const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(obs_stage);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                   ::"l"(gdst), "r"(saddr), "r"(bulk) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    for (uint32_t k = bulk + lane; k < bytes; k += 32) gdst[k] = obs_stage[k];
+    if (lane == 0 && bulk) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
