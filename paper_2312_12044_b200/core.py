@@ -60,39 +60,13 @@ class InvalidProportion(ValueError):
 
 
 # ------------------------------------------------------------------ codes
-class Tile(IntEnum):
-    END_OF_MAP = 0
-    UNSEEN = 1
-    EMPTY = 2
-    FLOOR = 3
-    WALL = 4
-    BALL = 5
-    SQUARE = 6
-    PYRAMID = 7
-    GOAL = 8
-    KEY = 9
-    DOOR_LOCKED = 10
-    DOOR_CLOSED = 11
-    DOOR_OPEN = 12
-    HEX = 13
-    STAR = 14
-
-
-class Color(IntEnum):
-    END_OF_MAP = 0
-    UNSEEN = 1
-    EMPTY = 2
-    RED = 3
-    GREEN = 4
-    BLUE = 5
-    PURPLE = 6
-    YELLOW = 7
-    GREY = 8
-    BLACK = 9
-    ORANGE = 10
-    WHITE = 11
-    BROWN = 12
-    PINK = 13
+# tile and color ids in code order (ref core.py:17-49); code = tile * 16 + color
+Tile = IntEnum("Tile", [(name, i) for i, name in enumerate(
+    "END_OF_MAP UNSEEN EMPTY FLOOR WALL BALL SQUARE PYRAMID GOAL KEY DOOR_LOCKED DOOR_CLOSED DOOR_OPEN HEX STAR"
+    .split())])
+Color = IntEnum("Color", [(name, i) for i, name in enumerate(
+    "END_OF_MAP UNSEEN EMPTY RED GREEN BLUE PURPLE YELLOW GREY BLACK ORANGE WHITE BROWN PINK".split())])
+Tile.__module__ = Color.__module__ = __name__
 
 
 PICKABLE_TILES = frozenset({Tile.BALL, Tile.SQUARE, Tile.PYRAMID, Tile.KEY, Tile.HEX, Tile.STAR})
@@ -106,11 +80,15 @@ GENERATION_COLORS = (Color.RED, Color.GREEN, Color.BLUE, Color.PURPLE, Color.YEL
                      Color.GREY, Color.ORANGE, Color.WHITE, Color.BROWN, Color.PINK)
 
 
+def _check_part(value: int, top: int, what: str) -> None:
+    if not 0 <= value <= top:
+        raise InvalidCode(f"{what} {value} outside [0, {top}]")
+
+
 def pack_entity(tile: int, color: int) -> int:
-    if not 0 <= tile <= MAX_TILE:
-        raise InvalidCode(f"tile id {tile} outside [0, {MAX_TILE}]")
-    if not 0 <= color <= MAX_COLOR:
-        raise InvalidCode(f"color id {color} outside [0, {MAX_COLOR}]")
+    """tile * 16 + color, both parts range-checked (ref core.py:73-79)."""
+    _check_part(tile, MAX_TILE, "tile id")
+    _check_part(color, MAX_COLOR, "color id")
     return tile * 16 + color
 
 
@@ -125,11 +103,10 @@ class Entity:
 
 
 def unpack_entity(code: int) -> Entity:
+    """Inverse of pack_entity; rejects codes no (tile, color) maps to (ref core.py:82-89)."""
     tile, color = divmod(code, 16)
-    if not 0 <= tile <= MAX_TILE:
-        raise InvalidCode(f"code {code}: tile part {tile} outside [0, {MAX_TILE}]")
-    if color > MAX_COLOR:
-        raise InvalidCode(f"code {code}: color part {color} outside [0, {MAX_COLOR}]")
+    _check_part(tile, MAX_TILE, f"code {code}: tile part")
+    _check_part(color, MAX_COLOR, f"code {code}: color part")
     return Entity(Tile(tile), Color(color))
 
 
