@@ -133,6 +133,17 @@ def _allreduce(dist, t, op):
     return t
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -200,7 +211,7 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": desc, "env": env_id, "rulesets": config, "envs_per_gpu": n_gpu},
         "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference arm = CPU oracle port of rulegrid.VecEnv (oracle/xmg_oracle.c, OpenMP over host "
                 "threads); the Python reference cannot travel to the GPU box",
@@ -524,9 +535,11 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         r = cpu_reference(args.workload, min(n, 1 << 14), 1 << 20, os.cpu_count() or 1, budget_s=12.0)
+        r1 = cpu_reference(args.workload, 1 << 12, 1 << 20, 1, budget_s=3.0)  # one core, for scale
         cpu = {"value": r["value"], "unit": "env-steps/s", "cores": os.cpu_count() or 1, "kind": "port",
                "sample": f"{r['envs']} envs x {r['steps']} steps of the same workload on the host "
-                         f"({r['seconds']:.1f} s, OpenMP over all host threads)"}
+                         f"({r['seconds']:.1f} s, OpenMP over all host threads)",
+               "cpu_model": cpu_model(), "one_core_value": r1["value"]}
 
     if rank == 0:
         line = {

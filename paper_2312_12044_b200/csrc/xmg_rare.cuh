@@ -236,7 +236,10 @@ __device__ __forceinline__ void release_envs(uint32_t* pending, bool mine, int64
   if (mine) atomicSub(pending + e / 32, 1u);
 }
 
-constexpr int kPutBatch = 8;  // PUT_DOWN envs a step_rare warp prefetches together
+#ifndef XMG_PUT_BATCH
+#define XMG_PUT_BATCH 8
+#endif
+constexpr int kPutBatch = XMG_PUT_BATCH;  // PUT_DOWN envs a step_rare warp prefetches together
 #ifndef XMG_RARE_WARPS
 #define XMG_RARE_WARPS 4
 #endif
