@@ -183,44 +183,6 @@ __device__ __forceinline__ int warp_select_fast(const uint64_t* wd, int lane, in
   return __shfl_sync(0xffffffffu, f, src);
 }
 
-// Two ranks of the same candidate set at once (the object bound and the
-// spawn cell of a trial build): one digit mask per bit serves both, and the
-// two reductions are independent, so their latencies overlap.
-template <int KR>
-__device__ __forceinline__ void warp_select_fast2(const uint64_t* wd, int lane, int F, uint32_t cand, int cnt,
-                                                  int t1, int t2, int& f1, int& f2) {
-  uint32_t hi[4 * KR];
-#pragma unroll
-  for (int j = 0; j < 4 * KR; ++j) {
-    const int f = 128 * (j >> 2) + 4 * lane + (j & 3);
-    hi[j] = f < F ? (uint32_t)(wd[f] >> 32) : 0u;
-  }
-  uint32_t c1 = cand, c2 = cand;
-  int tt1 = t1, tt2 = t2, cc1 = cnt, cc2 = cnt;
-  for (int b = 31; b >= 0 && (cc1 > 1 || cc2 > 1); --b) {
-    uint32_t z = 0;
-#pragma unroll
-    for (int j = 0; j < 4 * KR; ++j) z |= ((~hi[j] >> b) & 1u) << j;
-    const uint32_t z1 = z & c1, z2 = z & c2;
-    const int zeros1 = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(z1));
-    const int zeros2 = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(z2));
-    if (cc1 > 1) {
-      if (tt1 < zeros1) { c1 = z1; cc1 = zeros1; } else { c1 &= ~z1; tt1 -= zeros1; cc1 -= zeros1; }
-    }
-    if (cc2 > 1) {
-      if (tt2 < zeros2) { c2 = z2; cc2 = zeros2; } else { c2 &= ~z2; tt2 -= zeros2; cc2 -= zeros2; }
-    }
-  }
-  auto pick = [&](uint32_t c) {
-    const uint32_t who = __ballot_sync(0xffffffffu, c != 0);
-    const int src = __ffs(who) - 1;
-    const int bit = __ffs(c) - 1;
-    return __shfl_sync(0xffffffffu, 128 * (bit >> 2) + 4 * lane + (bit & 3), src);
-  };
-  f1 = cc1 > 1 ? warp_select(wd, lane, F, cand, cnt, t1) : pick(c1);
-  f2 = cc2 > 1 ? warp_select(wd, lane, F, cand, cnt, t2) : pick(c2);
-}
-
 __device__ __forceinline__ int select_rank(const uint64_t* wd, int lane, int F, uint32_t cand, int cnt, int t) {
   if (F <= 128) return warp_select_fast<1>(wd, lane, F, cand, cnt, t);
   if (F <= 256) return warp_select_fast<2>(wd, lane, F, cand, cnt, t);
@@ -247,20 +209,8 @@ __device__ void rank_place(const WarpScratch& ws, int lane, int F, int W, int mo
   XMG_TRB(7);
   const int no = nobj < total ? nobj : total;
   uint32_t* list = reinterpret_cast<uint32_t*>(ws.slot);  // the object cells' element indices
-  const int tail = total - spawn_base;
-  const int ts = tail > 0 ? spawn_base + (int)(spawn_word % (uint64_t)tail) : -1;  // the spawn cell's rank
-  // both ranks in one radix pass when both are needed and F fits the
-  // register path; otherwise one select each
-  int fb = -1, fs = -1;
-  if (no > 0 && ts >= 0 && F <= 512) {
-    if (F <= 128) warp_select_fast2<1>(ws.wd, lane, F, valid, total, no - 1, ts, fb, fs);
-    else if (F <= 256) warp_select_fast2<2>(ws.wd, lane, F, valid, total, no - 1, ts, fb, fs);
-    else warp_select_fast2<4>(ws.wd, lane, F, valid, total, no - 1, ts, fb, fs);
-  } else {
-    if (no > 0) fb = select_rank(ws.wd, lane, F, valid, total, no - 1);
-    if (ts >= 0) fs = select_rank(ws.wd, lane, F, valid, total, ts);
-  }
   if (no > 0) {
+    const int fb = select_rank(ws.wd, lane, F, valid, total, no - 1);
     XMG_TRB(8);
     const uint64_t wb = ws.wd[fb];
     int cnt = 0;
@@ -295,7 +245,11 @@ __device__ void rank_place(const WarpScratch& ws, int lane, int F, int W, int mo
     if (lane < no) ws.grid[ws.fc[f]] = (uint8_t)obj;
   }
   XMG_TRB(10);
-  if (fs >= 0 && lane == 0) reinterpret_cast<int*>(ws.misc + 32)[0] = ws.fc[fs];
+  const int tail = total - spawn_base;
+  if (tail > 0) {
+    const int fs = select_rank(ws.wd, lane, F, valid, total, spawn_base + (int)(spawn_word % (uint64_t)tail));
+    if (lane == 0) reinterpret_cast<int*>(ws.misc + 32)[0] = ws.fc[fs];
+  }
   __syncwarp();
 }
 

@@ -434,7 +434,10 @@ __device__ __noinline__ bool cell_visible_p(const uint8_t* stage, int sbase, int
 }
 
 // Occluded view (see_through_walls=False), ref:observation.py:90-110.
-__device__ XMG_RARE void obs_occluded(View vw, uint8_t* dst, int r, int c, int d, int H, int W, int V) {
+#ifndef XMG_OCC_INLINE
+#define XMG_OCC_INLINE XMG_RARE
+#endif
+__device__ XMG_OCC_INLINE void obs_occluded(View vw, uint8_t* dst, int r, int c, int d, int H, int W, int V) {
   const int h = V / 2;
   const int fr = dir_dr(d), fc = dir_dc(d);
   const int rr = fc, rc = -fr;  // right-hand vector (ref:observation.py:25)
