@@ -130,20 +130,6 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
   // step's step_rare, or this step's validation), so it runs concurrently with
   // the previous step_rare: with a validation it waits for the verdict, and
   // per 32-env chunk it waits only where the previous step queued envs (below).
-  if (abort_flag != nullptr) {  // this epoch's validation verdict (published by its last CTA)
-    if (lane == 0)
-      for (uint32_t spins = 0; ld_acquire(abort_flag + 1) != epoch; ++spins) {
-        if (spins > (1u << 25)) __trap();
-        __nanosleep(64);
-      }
-    __syncwarp();
-  }
-  // the previous step_rare has read these counts (it reads them before it
-  // lets this grid launch); this step appends to the other parity
-  if (blockIdx.x == 0)
-    for (int i = tid; i < 2 * kQueues; i += blockDim.x) s.work[count_index(epoch + 1, 0, 0) + i] = 0;
-  if (batch_rejected(abort_flag, epoch)) return;
-
   const int H = d.height, W = d.width, HW = H * W, V = d.view_size, R = d.rule_width;
   const MainGeo geo = make_main_geo(V, MAXCH, R);
   const int64_t tile = blockIdx.x;
@@ -170,6 +156,25 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
   if (valid) {
     ag = reinterpret_cast<const ulonglong2*>(s.agent)[e];
     act = load_action(actions, act_dtype, e);
+  }
+  // the loads above are in flight while the verdict is awaited (reads only:
+  // a rejected batch writes nothing; state step_rare may still rewrite is
+  // reloaded below)
+  if (abort_flag != nullptr) {  // this epoch's validation verdict (published by its last CTA)
+    if (lane == 0)
+      for (uint32_t spins = 0; ld_acquire(abort_flag + 1) != epoch; ++spins) {
+        if (spins > (1u << 25)) __trap();
+        __nanosleep(64);
+      }
+    __syncwarp();
+  }
+  // the previous step_rare has read these counts (it reads them before it
+  // lets this grid launch); this step appends to the other parity
+  if (blockIdx.x == 0)
+    for (int i = tid; i < 2 * kQueues; i += blockDim.x) s.work[count_index(epoch + 1, 0, 0) + i] = 0;
+  if (batch_rejected(abort_flag, epoch)) {
+    if (FULL) cp_async_wait_all();  // no copy may still target shared memory at exit
+    return;
   }
   if (was_dirty == epoch - 1 && e0 + warp * 32 < n) {
     // the previous step queued envs of this chunk: wait until its step_rare has
