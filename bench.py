@@ -161,11 +161,10 @@ def make_workload(name: str, device, n: int, offset: int):
     return params, bm, vec
 
 
-def cpu_reference(name: str, n_sample: int, steps: int, threads: int, budget_s: float = 20.0,
-                  min_s: float = 0.0) -> dict:
-    """The oracle port (oracle/xmg_oracle.c, OpenMP) on host cores: the same
-    workload restricted to `n_sample` envs, stepping until `steps` steps or
-    `budget_s` seconds (and for at least `min_s` seconds).  Returns env-steps/s."""
+def cpu_sample(name: str, n_sample: int, threads: int):
+    """The oracle port (oracle/xmg_oracle.c, OpenMP over `threads`) on the
+    workload restricted to its first `n_sample` envs, reset, with the random
+    policy's per-env keys."""
     from helpers import benchmark_file, oracle_from_table
     from oracle import oracle as O
     from paper_2312_12044_b200 import make
@@ -178,11 +177,19 @@ def cpu_reference(name: str, n_sample: int, steps: int, threads: int, budget_s: 
         table = TaskTable(np.zeros((1, 4), np.uint32), 0, 0, 0)
     ids = (np.arange(n_sample) % table.num_tasks).astype(np.int64)
     ora = oracle_from_table(params, table, ids, threads)
-    root = O.key_from_seed(0)
-    ora.reset(root)
+    ora.reset(O.key_from_seed(0))
     keys = [O.fold_in(O.key_from_seed(1), i) for i in range(n_sample)]
     pk0 = np.array([k[0] for k in keys], np.uint64)
     pk1 = np.array([k[1] for k in keys], np.uint64)
+    return ora, pk0, pk1
+
+
+def cpu_reference(name: str, n_sample: int, steps: int, threads: int, budget_s: float = 20.0,
+                  min_s: float = 0.0) -> dict:
+    """The oracle port on host cores: the sample stepping until `steps` steps
+    or `budget_s` seconds (and for at least `min_s` seconds).  Returns
+    env-steps/s."""
+    ora, pk0, pk1 = cpu_sample(name, n_sample, threads)
     done, t0 = 0, time.perf_counter()
     chunk = 16
     while (done < steps or time.perf_counter() - t0 < min_s) and time.perf_counter() - t0 < budget_s:
@@ -194,22 +201,51 @@ def cpu_reference(name: str, n_sample: int, steps: int, threads: int, budget_s: 
 
 
 def run_reference(args):
+    """The reference arm: the oracle port on all host threads, W untimed then
+    K timed steps, each step one bounded sample of the workload (n_sample
+    envs advanced m env-steps, m sized so the K steps take ~12 s)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     env_id, config, n_gpu, desc = WORKLOADS[args.workload]
     threads = os.cpu_count() or 1
     n_sample = min(n_gpu, 1 << 16)
-    # a bounded sample: at least the K requested steps, continued up to ~12 s
-    # of host work so the rate is stable (the whole run stays well within minutes)
-    r = cpu_reference(args.workload, n_sample, max(args.steps, 1), threads, budget_s=30.0, min_s=12.0)
-    value = r["value"]
-    sample = f"{r['envs']} envs x {r['steps']} steps of the {desc} workload ({r['seconds']:.1f} s)"
+    ora, pk0, pk1 = cpu_sample(args.workload, n_sample, threads)
+    # calibrate (after a first untimed pass: thread start-up, first touch):
+    # seconds per env-step pass over the sample, from >= 0.5 s of passes
+    ora.rollout_random(pk0, pk1, 0, 16, compute_obs=True)
+    done, t0 = 16, time.perf_counter()
+    while time.perf_counter() - t0 < 0.5:
+        ora.rollout_random(pk0, pk1, done, 16, compute_obs=True)
+        done += 16
+    per = (time.perf_counter() - t0) / (done - 16)
+    # longer passes run faster per env-step (each env's state stays in cache
+    # across the pass): re-measure at the pass length the steps will use
+    # (capped at ~1 s)
+    m = max(16, min(int(12.0 / max(args.steps, 1) / max(per, 1e-9)), int(1.0 / max(per, 1e-9))))
+    t0 = time.perf_counter()
+    ora.rollout_random(pk0, pk1, done, m, compute_obs=True)
+    per = (time.perf_counter() - t0) / m
+    done += m
+    k_steps, w_steps = max(args.steps, 1), max(args.warmup, 0)
+    m = max(1, int(round(12.0 / k_steps / max(per, 1e-9))))
+    for _ in range(w_steps):
+        ora.rollout_random(pk0, pk1, done, m, compute_obs=True)
+        done += m
+    t0 = time.perf_counter()
+    for _ in range(k_steps):
+        ora.rollout_random(pk0, pk1, done, m, compute_obs=True)
+        done += m
+    el = time.perf_counter() - t0
+    value = n_sample * m * k_steps / el
+    sample = (f"each step: {n_sample} envs x {m} env-steps of the {desc} workload "
+              f"({k_steps} steps in {el:.1f} s after {w_steps} warm-up steps)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": args.gpus,
-        "steps": r["steps"], "warmup": 0, "ms_per_step": 1e3 * r["envs"] / value, "higher_is_better": True,
+        "steps": k_steps, "warmup": w_steps, "ms_per_step": 1e3 * el / k_steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": desc, "env": env_id, "rulesets": config, "envs_per_gpu": n_gpu},
+        "config": {"workload": desc, "env": env_id, "rulesets": config, "envs_per_gpu": n_gpu,
+                   "sample_envs": n_sample, "env_steps_per_step": m},
         "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": threads, "kind": "port",
                          "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
