@@ -436,9 +436,9 @@ def run_ours(args):
                       "slots, D2H on a copy stream overlapping the next step)"}
         del vec3
 
-    # ---- the same K steps through VecEnv.steps (xmg_steps: one host call per
-    # block of 64 steps, no per-step host round trip; records written to a
-    # reused (64, n) trajectory buffer)
+    # ---- the same K steps through VecEnv.steps (one host call and one fused
+    # kernel per block of 64 steps, no per-step host round trip; records
+    # written to a reused (64, n) trajectory buffer)
     block = None
     if not args.no_block and (n * 2 * params.view_size ** 2) % 16 == 0:
         params5, _, vec5 = make_workload(args.workload, dev, n, offset)
@@ -483,7 +483,8 @@ def run_ours(args):
         block = {"value": n * world * K / (bms / 1e3), "unit": "env-steps/s", "ms_per_step": bms / K,
                  "block_steps": bk,
                  "note": "VecEnv.steps: the same K steps and actions as the timed window, block_steps per host call "
-                         "(xmg_steps), bit-identical to step() (tests/test_rollout_gpu.py)"}
+                         "(the fused kernel, xmg_rollout with the given actions), bit-identical to step() "
+                         "(tests/test_rollout_gpu.py)"}
         del traj, vec5
 
     # ---- fused rollout: the same K steps (same actions,

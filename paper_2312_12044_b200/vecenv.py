@@ -383,34 +383,39 @@ class VecEnv:
 
     # -- many steps per host call
     def steps(self, actions: torch.Tensor, compute_obs: bool = True, validate: bool = True,
-              out: Trajectory | None = None) -> Trajectory:
+              out: Trajectory | None = None, fused: bool = True) -> Trajectory:
         """``actions.shape[0]`` consecutive ``step`` calls issued by one library
-        call (``xmg_steps``): no per-step host round trip, for batches too
-        small to hide the per-call overhead.  Record k of the returned
+        call: no per-step host round trip.  Record k of the returned
         Trajectory is what ``step`` k would return.  ``validate`` checks the
         whole block once, before anything is launched (ref vecenv.py:297-301,
-        one host sync)."""
+        one host sync).  ``fused`` (default) runs the block in the fused
+        kernel (``xmg_rollout`` with the given actions: state on chip for the
+        whole block, one launch); ``fused=False`` issues the per-call kernels
+        K times (``xmg_steps``).  Both are bit-identical to ``step``."""
         n, v, dev = self.num_envs, self.params.view_size, self.device
         if not isinstance(actions, torch.Tensor):
             actions = torch.as_tensor(np.asarray(actions))
         if actions.dim() != 2 or actions.shape[1] != n:
             raise InvalidAction(f"expected (K, {n}) actions, got shape {tuple(actions.shape)}")
         k = actions.shape[0]
-        if compute_obs and (n * 2 * v * v) % 16:
-            raise ValueError("steps(): with observations, num_envs * 2 * v * v must be a multiple of 16 "
-                             "(16-byte aligned records); use step() or rollout()")
+        if not fused and compute_obs and (n * 2 * v * v) % 16:
+            raise ValueError("steps(fused=False): with observations, num_envs * 2 * v * v must be a multiple of 16 "
+                             "(16-byte aligned records); use step() or the fused path")
         if validate and bool(((actions < 0) | (actions >= 6)).any()):
             raise InvalidAction("action outside [0, 5]")
-        actions = actions.to(dev)
-        dt = _ACT_DTYPES.get(actions.dtype)
-        if dt is None:
-            actions, dt = actions.to(torch.int64), _lib.ACT_I64
-        actions = actions.contiguous()
         if out is None:
             out = Trajectory(torch.empty((k, n, v, v, 2), dtype=torch.uint8, device=dev) if compute_obs else None,
                              torch.empty((k, n), dtype=torch.float32, device=dev),
                              torch.empty((k, n), dtype=torch.float32, device=dev),
                              torch.empty((k, n), dtype=torch.int8, device=dev))
+        if fused:
+            # in range (checked above, or the caller's promise): u8 is exact
+            return self._launch_rollout(k, None, actions.to(dev, torch.uint8).contiguous(), 0, out)
+        actions = actions.to(dev)
+        dt = _ACT_DTYPES.get(actions.dtype)
+        if dt is None:
+            actions, dt = actions.to(torch.int64), _lib.ACT_I64
+        actions = actions.contiguous()
         o = _lib.Out(_ptr(out.observations), _ptr(out.rewards), _ptr(out.discounts), _ptr(out.step_types),
                      _ptr(self.stats))
         _lib.check(_lib.lib().xmg_steps(self._desc_ref, self._state_ref, actions.data_ptr(), dt, k, n, C.byref(o),
@@ -457,10 +462,14 @@ class VecEnv:
                 torch.empty((steps, n), dtype=torch.float32, device=dev) if "rewards" in record else None,
                 torch.empty((steps, n), dtype=torch.float32, device=dev) if "discounts" in record else None,
                 torch.empty((steps, n), dtype=torch.int8, device=dev) if "step_types" in record else None)
+        return self._launch_rollout(steps, policy_keys, actions, t0, out)
+
+    def _launch_rollout(self, steps: int, policy_keys, actions, t0: int, out: Trajectory) -> Trajectory:
         o = _lib.Out(_ptr(out.observations), _ptr(out.rewards), _ptr(out.discounts), _ptr(out.step_types),
                      _ptr(self.stats))
         _lib.check(_lib.lib().xmg_rollout(C.byref(self._desc), C.byref(self._state), _ptr(policy_keys),
-                                          _ptr(actions), t0, steps, n, C.byref(o), _stream(dev)), "xmg_rollout")
+                                          _ptr(actions), t0, steps, self.num_envs, C.byref(o),
+                                          _stream(self.device)), "xmg_rollout")
         self.launches += 1
         return out
 

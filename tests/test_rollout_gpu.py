@@ -133,14 +133,16 @@ def test_rollout_explicit_actions_and_partial_records():
     assert torch.equal(before, b.grids)
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("env_name,config,n,k", [
     ("XLand-MiniGrid-R4-13x13", "medium", 4096, 530),
     ("MiniGrid-Empty-8x8", None, 1024, 256),      # BASELINE configs[0] shape
     ("XLand-MiniGrid-R1-9x9", "trivial", 1 << 16, 260),
 ])
-def test_steps_block_equals_single_steps(env_name, config, n, k):
-    """VecEnv.steps (xmg_steps: K steps from one host call) == K step() calls,
-    interleaved with single steps and a rollout on the same state."""
+def test_steps_block_equals_single_steps(env_name, config, n, k, fused):
+    """VecEnv.steps (K steps from one host call: the fused kernel, or
+    xmg_steps) == K step() calls, interleaved with single steps and a rollout
+    on the same state."""
     from paper_2312_12044_b200 import InvalidAction, key_from_seed, policy_keys, random_actions
     params, bm, a, b = _pair(env_name, config, n)
     root = key_from_seed(9)
@@ -149,7 +151,7 @@ def test_steps_block_equals_single_steps(env_name, config, n, k):
     sa, sb = a.enable_stats(), b.enable_stats()
     pk = policy_keys(key_from_seed(1), n, device=a.device)
     acts = random_actions(pk, 0, k + 20)
-    tr = b.steps(acts[:k])
+    tr = b.steps(acts[:k], fused=fused)
     for t in range(k):
         ts = a.step(acts[t])
         assert torch.equal(ts.observations, tr.observations[t]), f"obs t={t}"
@@ -160,14 +162,14 @@ def test_steps_block_equals_single_steps(env_name, config, n, k):
         a.step(acts[t])
         b.step(acts[t])
     a.rollout(10, policy_keys=pk, t0=k + 10, record=())
-    b.steps(acts[k + 10:k + 20], compute_obs=False)
+    b.steps(acts[k + 10:k + 20], compute_obs=False, fused=fused)
     _same_state(a, b, "after mixing")
     torch.testing.assert_close(sa.sum(0), sb.sum(0), rtol=1e-12, atol=1e-9)
     bad = acts[:4].clone()
     bad[2, 5] = 7
     before = b.grids.clone()
     with pytest.raises(InvalidAction):
-        b.steps(bad)
+        b.steps(bad, fused=fused)
     assert torch.equal(before, b.grids)
 
 
