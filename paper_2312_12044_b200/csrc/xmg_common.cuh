@@ -121,6 +121,11 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem_src) : "memory");
 }
+__device__ __forceinline__ void cp_async16_hint(void* smem_dst, const void* gmem_src, uint64_t pol) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem_src), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
@@ -194,7 +199,7 @@ struct WView : View {
 // Stage grid bytes [lo, hi) of this thread's env with 16-byte cp.async
 // chunks (aligned on the global address; the grid buffer is padded).
 template <int MAXCH>
-__device__ __forceinline__ void stage_issue(View& vw, int lo, int hi, int HW) {
+__device__ __forceinline__ void stage_issue(View& vw, int lo, int hi, int HW, const uint64_t* pol = nullptr) {
   if constexpr (MAXCH == 0) {
     vw.slo = vw.shi = vw.sbase = 0;
   } else {
@@ -206,7 +211,10 @@ __device__ __forceinline__ void stage_issue(View& vw, int lo, int hi, int HW) {
     vw.shi = min(vw.sbase + 16 * nch, HW);
 #pragma unroll
     for (int k = 0; k < MAXCH; ++k)
-      if (k < nch) cp_async16(vw.stage + 16 * k, reinterpret_cast<const void*>(a0 + 16 * k));
+      if (k < nch) {
+        if (pol) cp_async16_hint(vw.stage + 16 * k, reinterpret_cast<const void*>(a0 + 16 * k), *pol);
+        else cp_async16(vw.stage + 16 * k, reinterpret_cast<const void*>(a0 + 16 * k));
+      }
   }
 }
 
