@@ -130,6 +130,28 @@ __device__ __forceinline__ void warp_stats(double* stats, int slot, double rs, d
   }
 }
 
+// The same slot update for one step of a warp's 32 envs: a reward is only
+// paid on a step that ends the trial, so a warp with no trial ending (the
+// common case, ~94% of warps per step at C3) does two votes and nothing
+// else; trials and lengths are integer warp reductions (popc / redux.sync).
+// Called converged (all 32 lanes).
+__device__ __forceinline__ void warp_stats_step(double* stats, int slot, float rew, bool last, uint32_t sc) {
+  const uint32_t lm = __ballot_sync(0xffffffffu, last);
+  if (!lm) return;
+  const uint32_t len = __reduce_add_sync(0xffffffffu, last ? sc : 0u);
+  double rs = 0.0;
+  if (__any_sync(0xffffffffu, rew != 0.f)) {
+    rs = (double)rew;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) rs += __shfl_down_sync(0xffffffffu, rs, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (rs != 0.0) atomicAdd(stats + 3 * slot, rs);
+    atomicAdd(stats + 3 * slot + 1, (double)__popc(lm));
+    atomicAdd(stats + 3 * slot + 2, (double)len);
+  }
+}
+
 struct MainGeo {
   int ob, stg, rb;
   int64_t total;
@@ -355,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
   }
 
   // ---- episode statistics of the trials decided here
-  if (o.stats != nullptr) warp_stats(o.stats, (int)tile, rew, last ? 1.0 : 0.0, last ? (double)sc : 0.0);
+  if (o.stats != nullptr) warp_stats_step(o.stats, (int)tile, rew, last, sc);
 
 
   // ---- observation: assembled in smem, one TMA bulk store per warp
