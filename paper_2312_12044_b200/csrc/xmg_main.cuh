@@ -19,7 +19,10 @@
 // counts[(t + 1) & 1] (consumed by the previous step), so no kernel ever
 // waits for another.  Layout: counts [2 parities][2 kinds][kQueues], then the
 // PUT entries (kQueues x queue_cap) and the reset entries (kQueues x queue_cap).
-constexpr int kQueues = 128;
+#ifndef XMG_QUEUES
+#define XMG_QUEUES 64  // sub-queues per kind (C3 76.9 vs 77.0 us at 128, C4 66.5 vs 67.4; 32 and 256 slower)
+#endif
+constexpr int kQueues = XMG_QUEUES;
 constexpr int kWorkHeader = 4 * kQueues;
 __host__ __device__ inline int count_index(uint32_t parity, int kind, int q) {
   return (int)((parity & 1) * 2 * kQueues + kind * kQueues + q);

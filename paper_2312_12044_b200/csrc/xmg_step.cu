@@ -406,7 +406,14 @@ int32_t xmg_validate_actions(const void* actions, int32_t dtype, int64_t n, uint
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, sms));
+#ifndef XMG_VAL_SMS
+#define XMG_VAL_SMS 1  // validation CTAs per SM (at most)
+#endif
+#ifndef XMG_VAL_ELEMS
+#define XMG_VAL_ELEMS 4096  // elements per validation CTA (at least)
+#endif
+  const int64_t blocks =
+      std::max<int64_t>(1, std::min<int64_t>((n + XMG_VAL_ELEMS - 1) / XMG_VAL_ELEMS, (int64_t)sms * XMG_VAL_SMS));
   // may overlap the previous step's step_rare (it only reads the actions)
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
