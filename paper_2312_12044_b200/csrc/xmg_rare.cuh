@@ -239,6 +239,9 @@ __device__ __forceinline__ void release_envs(uint32_t* pending, bool mine, int64
 #ifndef XMG_PUT_BATCH
 #define XMG_PUT_BATCH 8
 #endif
+#ifndef XMG_BUILD_COST
+#define XMG_BUILD_COST 4.0  // a trial build's cost in PUT_DOWN events (the warp split below)
+#endif
 constexpr int kPutBatch = XMG_PUT_BATCH;  // PUT_DOWN envs a step_rare warp prefetches together
 #ifndef XMG_RARE_WARPS
 #define XMG_RARE_WARPS 4
@@ -365,7 +368,7 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRar
       if (cnt_put == 0) {
         rs_w = per_q;
       } else {
-        const double wr = 4.0 * (double)cnt_reset, wp = (double)cnt_put;
+        const double wr = XMG_BUILD_COST * (double)cnt_reset, wp = (double)cnt_put;
         rs_w = (int)(per_q * wr / (wr + wp) + 0.5);
         rs_w = rs_w < 1 ? 1 : rs_w > per_q - 1 ? per_q - 1 : rs_w;
       }
