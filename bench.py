@@ -480,10 +480,12 @@ def run_ours(args):
         if world > 1:
             tb = _allreduce(dist, coll(tb), dist.ReduceOp.MAX)
         bms = float(tb.item())
+        fused_block = vec5.aligned_fused_choice()
         block = {"value": n * world * K / (bms / 1e3), "unit": "env-steps/s", "ms_per_step": bms / K,
-                 "block_steps": bk,
+                 "block_steps": bk, "kernel": "xmg_rollout (fused)" if fused_block else "xmg_steps (per-call kernels)",
                  "note": "VecEnv.steps: the same K steps and actions as the timed window, block_steps per host call "
-                         "(the fused kernel, xmg_rollout with the given actions), bit-identical to step() "
+                         "(its default kernel choice: the fused kernel, xmg_rollout with the given actions, where it "
+                         "keeps >= 12 warps/SM, else K x the per-call kernels), bit-identical to step() "
                          "(tests/test_rollout_gpu.py)"}
         del traj, vec5
 

@@ -383,22 +383,29 @@ class VecEnv:
 
     # -- many steps per host call
     def steps(self, actions: torch.Tensor, compute_obs: bool = True, validate: bool = True,
-              out: Trajectory | None = None, fused: bool = True) -> Trajectory:
+              out: Trajectory | None = None, fused: bool | None = None) -> Trajectory:
         """``actions.shape[0]`` consecutive ``step`` calls issued by one library
         call: no per-step host round trip.  Record k of the returned
         Trajectory is what ``step`` k would return.  ``validate`` checks the
         whole block once, before anything is launched (ref vecenv.py:297-301,
-        one host sync).  ``fused`` (default) runs the block in the fused
-        kernel (``xmg_rollout`` with the given actions: state on chip for the
-        whole block, one launch); ``fused=False`` issues the per-call kernels
-        K times (``xmg_steps``).  Both are bit-identical to ``step``."""
+        one host sync).  ``fused=True`` runs the block in the fused kernel
+        (``xmg_rollout`` with the given actions: state on chip for the whole
+        block, one launch); ``fused=False`` issues the per-call kernels K times
+        (``xmg_steps``).  Both are bit-identical to ``step``.  ``None``
+        (default) picks the fused kernel when it keeps at least 12 warps per SM
+        resident (16 up to 13x13 with medium rulesets, where it is the faster
+        path), else the per-call kernels (R9-25x25 high: 4 warps/SM fused,
+        6.6e9 vs 8.4e9 env-steps/s per call at 2^19 envs)."""
         n, v, dev = self.num_envs, self.params.view_size, self.device
         if not isinstance(actions, torch.Tensor):
             actions = torch.as_tensor(np.asarray(actions))
         if actions.dim() != 2 or actions.shape[1] != n:
             raise InvalidAction(f"expected (K, {n}) actions, got shape {tuple(actions.shape)}")
         k = actions.shape[0]
-        if not fused and compute_obs and (n * 2 * v * v) % 16:
+        aligned = not compute_obs or (n * 2 * v * v) % 16 == 0
+        if fused is None:
+            fused = not aligned or self.aligned_fused_choice()
+        if not fused and not aligned:
             raise ValueError("steps(fused=False): with observations, num_envs * 2 * v * v must be a multiple of 16 "
                              "(16-byte aligned records); use step() or the fused path")
         if validate and bool(((actions < 0) | (actions >= 6)).any()):
@@ -423,6 +430,16 @@ class VecEnv:
         self.epoch += k
         self.launches += 2 * k
         return out
+
+    def aligned_fused_choice(self) -> bool:
+        """steps(fused=None)'s choice for 16-byte aligned records."""
+        return self._rollout_warps_per_sm() >= 12
+
+    def _rollout_warps_per_sm(self) -> int:
+        """Resident warps per SM of the fused kernel (4-warp CTAs, bounded by
+        shared memory: 228 KB per SM, 1 KB reserved per CTA; <= 16)."""
+        smem = int(_lib.lib().xmg_rollout_smem_bytes(C.byref(self._desc)))
+        return 4 * min(4, (228 * 1024) // (smem + 1024)) if smem > 0 else 0
 
     # -- fused rollout (SURVEY.md 8(f)#3)
     def rollout(self, steps: int, policy_keys: torch.Tensor | None = None, actions: torch.Tensor | None = None,
