@@ -381,6 +381,13 @@ def run_ours(args):
                                else "fallback 6650 GB/s (B200_PROFILING.md)",
                 "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum of one step_main launch "
                                 "(profiles/ncu_summary.json)"}
+    if traffic is not None:
+        # the DRAM bytes step_main actually moves over its measured launch
+        # time: where the window reads less than the read-once-grid model
+        # (25x25 grids), `frac` is an effective bandwidth and this is the
+        # physical one
+        roofline["dram_achieved"] = traffic / (main_ms / 1e3) / 1e9
+        roofline["dram_frac"] = roofline["dram_achieved"] / peak
 
     # ---- e2e through the public API with HOST buffers (pinned), per step:
     # H2D of the step's actions, the step, D2H of the whole VecTimeStep.  The
