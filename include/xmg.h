@@ -21,7 +21,10 @@
  *   grids  u8  [n][H*W]   row-major entity codes tile*16+color
  *                          (allocation must extend >= 64 bytes past n*H*W:
  *                          the step kernel reads 16-byte aligned chunks)
- *   agent  u64 [n][2]     word 0: r | c<<8 | dir<<16 | pocket<<24 | step_count<<32
+ *   agent  u64 [n][2]     word 0: r | c<<8 | dir<<16 | pocket<<24 | step_count<<32,
+ *                         bits 18-19 = the reset-ahead stage (scheduling metadata,
+ *                         not env state: 0 none, 1 next trial queued for pre-build
+ *                         this step, 2 pre-built; see next_* below)
  *                         word 1: goal | task<<32, where goal = encoding bytes
  *                         (kind, a1, a2, a3) little-endian and task = the row
  *                         of the task table this env runs (one 16-byte load)
@@ -45,7 +48,7 @@
 extern "C" {
 #endif
 
-#define XMG_ABI_VERSION 1
+#define XMG_ABI_VERSION 2
 
 /* scenario ids: ref scenarios.py:415-423 (SCENARIOS) */
 enum {
@@ -91,6 +94,15 @@ typedef struct xmg_state {
     uint32_t* work;    /* [xmg_work_words(n)], zero-initialised once: the queues of
                         * rare work (PUT_DOWN events, trial resets) handed from
                         * the streaming kernel to the warp-per-env kernel */
+    /* Reset-ahead buffers (all NULL: off).  A trial's successor depends only
+     * on the env's rng key and task (ref vecenv.py:224-233, 359-361), both
+     * fixed while the trial runs, so xmg_step pre-builds it during the trial
+     * (one env in (budget - 2) per step) and the auto-reset that ends the
+     * trial becomes a copy of these records instead of a build.  16-byte
+     * aligned; contents are scratch owned by the library. */
+    uint8_t* next_grids;   /* [n][H*W] (+64 B pad, like grids) the next trial's grid */
+    uint64_t* next_state;  /* [n][4]: next state word 0, word 1, next rng (hi, lo) */
+    uint8_t* next_obs;     /* [n][v][v][2] the next trial's first observation */
 } xmg_state;
 
 /* VecTimeStep (vecenv.py:95-105): observations may be NULL (compute_obs=False) */

@@ -23,7 +23,7 @@ HEADER = os.path.join(ROOT, "include", "xmg.h")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xptxas", "-v", "-shared", "-Xcompiler", "-fPIC"]
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # scenario ids of include/xmg.h (ref scenarios.py:415-423)
 SCENARIO_IDS = {"xland": 0, "empty": 1, "empty_random": 2, "door_key": 3, "four_rooms": 4,
@@ -51,7 +51,8 @@ class EnvDesc(C.Structure):
 
 
 class State(C.Structure):
-    _fields_ = [("grids", C.c_void_p), ("agent", C.c_void_p), ("rng", C.c_void_p), ("work", C.c_void_p)]
+    _fields_ = [("grids", C.c_void_p), ("agent", C.c_void_p), ("rng", C.c_void_p), ("work", C.c_void_p),
+                ("next_grids", C.c_void_p), ("next_state", C.c_void_p), ("next_obs", C.c_void_p)]
 
 
 class Out(C.Structure):

@@ -27,7 +27,32 @@ constexpr int kWorkHeader = 4 * kQueues;
 __host__ __device__ inline int count_index(uint32_t parity, int kind, int q) {
   return (int)((parity & 1) * 2 * kQueues + kind * kQueues + q);
 }
-constexpr uint32_t kQPut = 1u << 31, kQReset = 1u << 30, kQEnv = (1u << 30) - 1;
+constexpr uint32_t kQPut = 1u << 31, kQReset = 1u << 30, kQPre = 1u << 29, kQEnv = (1u << 30) - 1;
+// reset-queue entries: env index | kEntPre for a pre-build (reset-ahead:
+// the env's NEXT trial, built into state.next_*, not released via `pending`)
+constexpr uint32_t kEntPre = 1u << 31;
+
+// ------------------------------------------------------- reset-ahead
+// A trial's successor is a function of the env's rng key and task only
+// (ref:vecenv.py:224-233 via :359-361), both fixed while the trial runs.  So
+// step_main queues each env once per trial, at step count >= prebuild_slot(e),
+// for step_rare to build its next trial into state.next_* (stage 1 in state
+// word bits 18-19); one step later the stage becomes 2.  A kernel launched
+// after the queueing step's step_rare finished may read the records: step_rare
+// of step t is a plain launch, so it starts only after everything before it
+// on the stream (step_rare of step t-1) has completed, and step_main of step
+// t+1 launches (programmatically) after it started.  When a trial ends at
+// stage 2, step_main copies the records (grid, state word, rng, first
+// observation) instead of queueing a rebuild; otherwise (a goal reached
+// before the pre-build was ready, or a PUT_DOWN that ends the trial) the
+// in-place rebuild of round 1 runs.  The slots spread the pre-builds
+// uniformly: 1 + e mod (budget - 2) <= budget - 2, so every budget end is
+// covered.
+constexpr uint64_t kStageMask = 3ull << 18;
+__host__ __device__ inline uint32_t prebuild_slot(int64_t e, int budget) {
+  return 1u + (uint32_t)(e % (int64_t)(budget - 2));
+}
+__device__ __forceinline__ bool ahead_on(const xmg_state& s, int budget) { return s.next_grids != nullptr && budget >= 3; }
 
 // capacity of one sub-queue: every env of the step_main CTAs (128 envs each) feeding it
 __host__ __device__ inline int64_t queue_cap(int64_t n) {
@@ -155,6 +180,55 @@ __device__ __forceinline__ void warp_stats_step(double* stats, int slot, float r
   }
 }
 
+// Warp copy of nbytes from src to dst (equal alignment mod 16), the body in
+// 16-byte chunks; the source is read through L2 (.cg: records written by an
+// earlier kernel, never cached in this SM's L1).
+__device__ __forceinline__ void warp_copy_cg(uint8_t* dst, const uint8_t* src, int nbytes, int lane) {
+  const int head = min((int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15), nbytes);
+  if (lane < head) dst[lane] = __ldcg(src + lane);
+  const int body = (nbytes - head) >> 4;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+  uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+  int i = lane;
+  for (; i + 96 < body; i += 128) {  // four chunks in flight per lane
+    const uint4 a = __ldcg(s4 + i), b = __ldcg(s4 + i + 32), c = __ldcg(s4 + i + 64), d = __ldcg(s4 + i + 96);
+    d4[i] = a;
+    d4[i + 32] = b;
+    d4[i + 64] = c;
+    d4[i + 96] = d;
+  }
+  for (; i < body; i += 32) d4[i] = __ldcg(s4 + i);
+  for (int t = head + 16 * body + lane; t < nbytes; t += 32) dst[t] = __ldcg(src + t);
+}
+
+#ifndef XMG_CONSUME_INLINE
+#define XMG_CONSUME_INLINE __forceinline__  // inlined: fewer spills in step_main than a call
+#endif
+// The auto-resets of the envs in `cm` (lanes of the warp's 32-env chunk
+// starting at w0) from their pre-built records: state word and rng per lane,
+// then grid bytes and first observations (into the warp's observation stage)
+// copied by the whole warp, one contiguous run of envs at a time (a burst of
+// budget ends is one run of 32).
+__device__ XMG_CONSUME_INLINE void consume_next(const xmg_state s, uint32_t cm, int64_t w0, int HW, int ob,
+                                          uint8_t* obs_stage, int lane) {
+  __syncwarp();  // the lanes' own grid writes of this step precede the copy
+  if ((cm >> lane) & 1) {
+    const ulonglong2* ns = reinterpret_cast<const ulonglong2*>(s.next_state) + 2 * (w0 + lane);
+    const ulonglong2 a = __ldcg(ns), b = __ldcg(ns + 1);
+    reinterpret_cast<ulonglong2*>(s.agent)[w0 + lane] = a;
+    reinterpret_cast<ulonglong2*>(s.rng)[w0 + lane] = b;
+  }
+  for (uint32_t m = cm; m;) {
+    const int a = __ffs(m) - 1;
+    const uint32_t gap = ~m & ~((1u << a) - 1u);
+    const int b = gap ? __ffs(gap) - 1 : 32;
+    m = b < 32 ? m & (~0u << b) : 0u;
+    warp_copy_cg(s.grids + (w0 + a) * HW, s.next_grids + (w0 + a) * HW, (b - a) * HW, lane);
+    if (obs_stage != nullptr) warp_copy_cg(obs_stage + a * ob, s.next_obs + (w0 + a) * ob, (b - a) * ob, lane);
+  }
+  __syncwarp();
+}
+
 struct MainGeo {
   int ob, stg, rb;
   int64_t total;
@@ -269,7 +343,8 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
 
   uint32_t qflags = 0;
   float rew = 0.f;
-  bool last = false;
+  bool last = false, consume = false;
+  const bool ahead = ahead_on(s, d.budget);
   if (valid) {
     // ---- stage the post-action window (MOVE: both candidate poses) and,
     // for actions that can raise an event, the env's rule row
@@ -331,6 +406,8 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
     }
     // ---- counters and reward, ref:vecenv.py:351-357
     sc += 1;
+    const uint32_t stage_old = (uint32_t)(ag.x >> 18) & 3u;
+    uint32_t stage = stage_old == 1u ? 2u : stage_old;
     if (ev == 2) {
       qflags = kQPut;  // rules, goal and reward resolved by step_rare
     } else {
@@ -345,39 +422,56 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
       o.discount[e] = last ? 0.f : 1.f;
       o.step_type[e] = last ? 2 : 1;
 #endif
-      if (last) qflags = kQReset;
+      // auto-reset: the pre-built next trial when it is ready, else a rebuild
+      if (last) {
+        if (ahead && stage_old == 2u) consume = true;
+        else qflags = kQReset;
+      } else if (ahead && stage_old == 0u && sc >= prebuild_slot(e, d.budget)) {
+        qflags = kQPre;
+        stage = 1u;
+      }
     }
+    if (!consume) {
 #if XMG_L2HINT
-    st_hint_u64(s.agent + 2 * e, pack_agent(r, c, dir, pocket, sc), pol_keep);
+      st_hint_u64(s.agent + 2 * e, pack_agent(r, c, dir | (int)(stage << 2), pocket, sc), pol_keep);
 #else
-    s.agent[2 * e] = pack_agent(r, c, dir, pocket, sc);
+      s.agent[2 * e] = pack_agent(r, c, dir | (int)(stage << 2), pocket, sc);
 #endif
+    }
   }
 
   // ---- defer the rare work: warp-aggregated append to this CTA's sub-queue
-  const uint32_t qm = __ballot_sync(0xffffffffu, qflags != 0);
-  if (qm) {
+  const uint32_t am = __ballot_sync(0xffffffffu, qflags != 0);
+  if (am) {
     const int k = (int)(tile % kQueues);
-    if (lane == 0) {
+    // envs step_rare rewrites (PUT_DOWN, rebuild) hold the chunk for the next
+    // step_main; pre-builds write only the next_* records and hold nothing
+    const uint32_t qm = __ballot_sync(0xffffffffu, (qflags & (kQPut | kQReset)) != 0);
+    if (lane == 0 && qm) {
       atomicAdd(pending, (uint32_t)__popc(qm));
       *dirty = epoch;
     }
-    // PUT_DOWN and reset entries go to their own queues
+    // PUT_DOWN entries to their queue; rebuilds and pre-builds to the reset queue
 #pragma unroll
     for (int kind = 0; kind < 2; ++kind) {
-      const uint32_t want = kind ? kQReset : kQPut;
-      const uint32_t km = __ballot_sync(0xffffffffu, qflags == want);
+      const bool mine = kind ? (qflags & (kQReset | kQPre)) != 0 : qflags == kQPut;
+      const uint32_t km = __ballot_sync(0xffffffffu, mine);
       if (!km) continue;
       const int leader = __ffs(km) - 1;
       uint32_t base = 0;
       if (lane == leader) base = atomicAdd(s.work + count_index(epoch, kind, k), (uint32_t)__popc(km));
       base = __shfl_sync(0xffffffffu, base, leader);
-      if (qflags == want) {
+      if (mine) {
         XMG_ASSERT(base + __popc(km & ((1u << lane) - 1)) < queue_cap(n));
-        s.work[queue_base(n, epoch, kind, k) + base + __popc(km & ((1u << lane) - 1))] = (uint32_t)e;
+        s.work[queue_base(n, epoch, kind, k) + base + __popc(km & ((1u << lane) - 1))] =
+            (uint32_t)e | (qflags == kQPre ? kEntPre : 0u);
       }
     }
   }
+
+  // ---- auto-resets from the pre-built records (reset-ahead)
+  const uint32_t cm = __ballot_sync(0xffffffffu, consume);
+  if (cm) consume_next(s, cm, e0 + warp * 32, HW, 2 * V * V, o.obs != nullptr ? obs_stage : nullptr, lane);
 
   // ---- episode statistics of the trials decided here
   if (o.stats != nullptr) warp_stats_step(o.stats, (int)tile, rew, last, sc);
@@ -387,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
   // (envs queued for step_rare get theirs rewritten there)
   if (o.obs != nullptr) {
     __syncwarp();  // every lane is done with its rule row
-    if (valid) {
+    if (valid && !consume) {  // (consumed envs: copied from next_obs above)
       uint8_t* dst = obs_stage + lane * geo.ob;
       if (d.see_through_walls) {
         if (V == 5) obs_see<5>(vw.stage, vw.sbase, dst, r, c, dir, H, W, V);

@@ -273,26 +273,38 @@ __host__ __device__ inline RareGeo make_rare_geo(int H, int W, int R) {
 }
 
 // Rebuild env e's trial (ref:vecenv.py:359-361 -> :224-291), whole warp.
+// pre (reset-ahead): the same build from the same keys, written to the
+// env's next_* records (grid, state word, rng, first observation) for the
+// auto-reset that will end the running trial; nothing of the running trial
+// is touched.
 __device__ __forceinline__ void warp_reset_env(const xmg_env_desc& d, const xmg_env_desc* sd, const xmg_state& s,
                                                const xmg_out& o, uint8_t* wbase, const RareGeo& geo, int lane,
                                                int64_t e, const TrialKeys* key, int task, bool reset_mode,
-                                               ResetOut* rs) {
+                                               ResetOut* rs, bool pre = false) {
   const int H = d.height, W = d.width, HW = H * W, V = d.view_size, ob = 2 * V * V;
   const WarpScratch ws = make_scratch(wbase, geo.hwp);
   const uint32_t g_in = d.scenario == XMG_SCENARIO_XLAND ? d.task_rows[(int64_t)task * d.row_words] : 0u;
-  warp_build(sd, wbase, geo.hwp, lane, key, task, g_in, s.grids + e * (int64_t)HW, rs);
+  warp_build(sd, wbase, geo.hwp, lane, key, task, g_in, (pre ? s.next_grids : s.grids) + e * (int64_t)HW, rs);
   const ResetOut ro = *rs;
+  const ulonglong2 word = make_ulonglong2(pack_agent(ro.r, ro.c, ro.d, 0, 0),
+                                          (uint64_t)ro.goal | ((uint64_t)(uint32_t)ro.task << 32));
   if (lane == 0) {
-    reinterpret_cast<ulonglong2*>(s.rng)[e] = make_ulonglong2(ro.st_hi, ro.st_lo);
-    reinterpret_cast<ulonglong2*>(s.agent)[e] = make_ulonglong2(
-        pack_agent(ro.r, ro.c, ro.d, 0, 0), (uint64_t)ro.goal | ((uint64_t)(uint32_t)ro.task << 32));
+    if (pre) {
+      ulonglong2* ns = reinterpret_cast<ulonglong2*>(s.next_state) + 2 * e;
+      ns[0] = word;
+      ns[1] = make_ulonglong2(ro.st_hi, ro.st_lo);
+    } else {
+      reinterpret_cast<ulonglong2*>(s.rng)[e] = make_ulonglong2(ro.st_hi, ro.st_lo);
+      reinterpret_cast<ulonglong2*>(s.agent)[e] = word;
+    }
     if (reset_mode) {
       o.reward[e] = 0.f;
       o.discount[e] = 1.f;
       o.step_type[e] = 0;
     }
   }
-  if (o.obs != nullptr) warp_obs(ws.grid, o.obs + e * ob, lane, ro.r, ro.c, ro.d, H, W, V, d.see_through_walls != 0);
+  uint8_t* obs = pre ? s.next_obs : o.obs;
+  if (obs != nullptr) warp_obs(ws.grid, obs + e * ob, lane, ro.r, ro.c, ro.d, H, W, V, d.see_through_walls != 0);
   __syncwarp();
   XMG_TRB(6);
 }
@@ -302,7 +314,7 @@ __device__ __forceinline__ void warp_reset_env(const xmg_env_desc& d, const xmg_
 __device__ __forceinline__ void warp_reset_group(const xmg_env_desc& d, const xmg_env_desc* sd, const xmg_state& s,
                                                  const xmg_out& o, uint8_t* wbase, const RareGeo& geo,
                                                  TrialKeys* keys, int lane, bool mine, int64_t e,
-                                                 const uint64_t* reset_keys, int gw = 0) {
+                                                 const uint64_t* reset_keys, int gw = 0, bool pre = false) {
   const bool resample = d.resample_tasks && d.scenario == XMG_SCENARIO_XLAND;
   int task = 0;
   ulonglong2 ek = make_ulonglong2(0, 0);
@@ -325,8 +337,9 @@ __device__ __forceinline__ void warp_reset_group(const xmg_env_desc& d, const xm
       m &= m - 1;
       const int64_t es = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)e, src);
       const int ts = __shfl_sync(0xffffffffu, task, src);
+      const bool ps = __shfl_sync(0xffffffffu, (int)pre, src) != 0;
       warp_reset_env(d, sd, s, o, wbase, geo, lane, es, keys + (src - half), ts, reset_keys != nullptr,
-                     reinterpret_cast<ResetOut*>(make_scratch(wbase, geo.hwp).misc + 40));
+                     reinterpret_cast<ResetOut*>(make_scratch(wbase, geo.hwp).misc + 40), ps);
     }
   }
 }
@@ -514,9 +527,11 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRar
     for (int64_t i0 = jr; i0 < cnt_reset; i0 += 32 * (int64_t)rs_w) {
       const int64_t i = i0 + (int64_t)lane * rs_w;
       const bool mine = i < cnt_reset;
-      const int64_t e = mine ? (int64_t)qp[i] : 0;
-      warp_reset_group(d, sdesc, s, o, wbase, geo, keys, lane, mine, e, nullptr, gw);
-      if (track) release_envs(s.work + pending_base(n), mine, e);
+      const uint32_t ent = mine ? qp[i] : 0u;
+      const bool pre = (ent & kEntPre) != 0;  // reset-ahead: build the next trial's records
+      const int64_t e = (int64_t)(ent & ~kEntPre);
+      warp_reset_group(d, sdesc, s, o, wbase, geo, keys, lane, mine, e, nullptr, gw, pre);
+      if (track) release_envs(s.work + pending_base(n), mine && !pre, e);
     }
   }
 #ifdef XMG_TRACE

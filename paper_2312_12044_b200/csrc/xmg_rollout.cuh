@@ -113,6 +113,9 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
   int r = (int)(ag.x & 0xff), c = (int)((ag.x >> 8) & 0xff), dir = (int)((ag.x >> 16) & 3);
   int pocket = (int)((ag.x >> 24) & 0xff);
   uint32_t sc = (uint32_t)(ag.x >> 32);
+  // reset-ahead stage (xmg_main.cuh): kept while the trial runs (its next_*
+  // records stay valid for step_main), cleared by an in-kernel rebuild
+  int stage = (int)((ag.x >> 18) & 3);
   uint32_t goal_word = (uint32_t)ag.y;
   int task = (int)(ag.y >> 32);
   uint32_t* rbuf = rules_s + lane * (geo.rbw / 4);
@@ -234,6 +237,7 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
           dir = ro.d;
           pocket = 0;
           sc = 0;
+          stage = 0;
           goal_word = ro.goal;
           task = ro.task;
           rk = make_ulonglong2(ro.st_hi, ro.st_lo);
@@ -292,7 +296,8 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
   }
   if (valid) {
     reinterpret_cast<ulonglong2*>(s.agent)[e] =
-        make_ulonglong2(pack_agent(r, c, dir, pocket, sc), (uint64_t)goal_word | ((uint64_t)(uint32_t)task << 32));
+        make_ulonglong2(pack_agent(r, c, dir | (stage << 2), pocket, sc),
+                        (uint64_t)goal_word | ((uint64_t)(uint32_t)task << 32));
     reinterpret_cast<ulonglong2*>(s.rng)[e] = rk;
   }
   if (o.stats != nullptr) warp_stats(o.stats, (int)(chunk / kWarps), st_ret, st_trials, st_len);

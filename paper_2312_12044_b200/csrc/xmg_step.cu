@@ -279,6 +279,11 @@ int launch_rare(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, con
 int validate_desc(const xmg_env_desc* d, const xmg_state* s, int64_t n) {
   if (!d) return fail("null env description");
   if (!s || !s->grids || !s->agent || !s->rng || !s->work) return fail("null state buffer");
+  if ((s->next_grids == nullptr) != (s->next_state == nullptr) || (s->next_grids == nullptr) != (s->next_obs == nullptr))
+    return fail("reset-ahead buffers next_grids / next_state / next_obs: all or none");
+  if ((reinterpret_cast<uintptr_t>(s->next_grids) | reinterpret_cast<uintptr_t>(s->next_state) |
+       reinterpret_cast<uintptr_t>(s->next_obs)) & 15)
+    return fail("reset-ahead buffers must be 16-byte aligned");
   if (n < 1) return fail("n must be >= 1");
   if (n > (int64_t)kQEnv) return fail("n too large for one launch (< 2^30)");
   if (d->height < 1 || d->height > 255 || d->width < 1 || d->width > 255) return fail("grid size outside [1, 255]");

@@ -22,6 +22,7 @@ There is no CPU fallback: without libxmg.so or a GPU every call raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -36,6 +37,7 @@ from .layouts import Layout, bordered, plan_layout
 from .ruleset import Benchmark, Ruleset, TaskTable, pack_rulesets
 
 GRID_PAD = 64  # the step kernel reads 16-byte aligned chunks past the last grid
+STAGE_BITS = 3 << 18  # reset-ahead stage in state word 0 (include/xmg.h)
 
 
 def _stream(device: torch.device) -> int:
@@ -155,7 +157,7 @@ _ACT_DTYPES = {torch.uint8: _lib.ACT_U8, torch.int32: _lib.ACT_I32, torch.int64:
 class VecEnv:
     def __init__(self, params: EnvParams, num_envs: int, rulesets=None, *, device=None, task_ids=None,
                  strict: bool = False, global_offset: int = 0, reuse_outputs: bool = False,
-                 resample_tasks: bool = False):
+                 resample_tasks: bool = False, reset_ahead: bool | None = None):
         if num_envs < 1:
             raise ValueError(f"num_envs must be >= 1, got {num_envs}")
         self.params = params
@@ -242,6 +244,15 @@ class VecEnv:
         self.agent = torch.from_numpy(agent.view(np.int64)).to(dev)
         self.rng = torch.zeros((n, 2), dtype=torch.int64, device=dev)
         self.work = torch.zeros(int(_lib.lib().xmg_work_words(n)), dtype=torch.int32, device=dev)
+        # reset-ahead records (include/xmg.h): each env's next trial, pre-built
+        # while the current one runs, so an auto-reset is a copy
+        self.reset_ahead = reset_ahead if reset_ahead is not None else os.environ.get("XMG_AHEAD", "1") != "0"
+        if self.reset_ahead:
+            self._next_grids = torch.zeros(n * self._hw + GRID_PAD, dtype=torch.uint8, device=dev)
+            self._next_state = torch.zeros((n, 4), dtype=torch.int64, device=dev)
+            self._next_obs = torch.zeros(n * 2 * v * v + 16, dtype=torch.uint8, device=dev)
+        else:
+            self._next_grids = self._next_state = self._next_obs = None
         # validation flag block (include/xmg.h XMG_FLAG_WORDS): [0] epoch of the
         # last rejected batch, [1] epoch of the last finished validation
         self._flag = torch.zeros(4, dtype=torch.int32, device=dev)
@@ -253,7 +264,8 @@ class VecEnv:
                                   table.num_tasks, int(resample_tasks and scen == 0), self._base.data_ptr(),
                                   self._seg_off.data_ptr(), self._seg_cells.data_ptr(), self._table.data_ptr())
         self._state = _lib.State(self.grids_flat.data_ptr(), self.agent.data_ptr(), self.rng.data_ptr(),
-                                 self.work.data_ptr())
+                                 self.work.data_ptr(), _ptr(self._next_grids), _ptr(self._next_state),
+                                 _ptr(self._next_obs))
         if _lib.lib().xmg_step_smem_bytes(C.byref(self._desc)) > 226 * 1024:
             raise _lib.NativeLibraryError(f"{h}x{w} grids exceed the shared-memory budget of this build")
         self._outs = None
@@ -272,8 +284,21 @@ class VecEnv:
     def agent_fields(self) -> torch.Tensor:
         """(N, 5) int64: row, col, dir, pocket, step_count."""
         a = self.agent[:, 0]
-        return torch.stack([a & 0xFF, (a >> 8) & 0xFF, (a >> 16) & 0xFF, (a >> 24) & 0xFF,
+        return torch.stack([a & 0xFF, (a >> 8) & 0xFF, (a >> 16) & 0x3, (a >> 24) & 0xFF,
                             (a >> 32) & 0xFFFFFFFF], dim=1)
+
+    def state_words(self) -> torch.Tensor:
+        """(N, 2) state words without the reset-ahead stage bits (18-19 of
+        word 0: scheduling metadata, not env state): the env state proper,
+        comparable across step / steps / rollout paths."""
+        a = self.agent.clone()
+        a[:, 0] &= ~STAGE_BITS
+        return a
+
+    @property
+    def reset_ahead_stage(self) -> torch.Tensor:
+        """(N,) 0 none / 1 next trial queued / 2 next trial pre-built."""
+        return (self.agent[:, 0] >> 18) & 3
 
     @property
     def goal(self) -> torch.Tensor:

@@ -39,11 +39,18 @@ def fixture_rulesets(fx):
     return out
 
 
-def benchmark_file(config):
-    paths = sorted(glob.glob(os.path.join(DATA, f"{config}-*.xmgb")))
-    if not paths:
-        raise FileNotFoundError(f"no data/{config}-*.xmgb; run data/make_benchmarks.py")
-    return paths[0]
+def benchmark_file(config, rows=None):
+    """data/<config>-<M>.xmgb: the smallest table by default (parity tests),
+    or the one with exactly `rows` rows (e.g. 2**20 for the "1m-style" C3 /
+    C4 tables of SURVEY.md §8(d))."""
+    paths = glob.glob(os.path.join(DATA, f"{config}-*.xmgb"))
+    sized = sorted((int(os.path.basename(p)[len(config) + 1:-5]), p) for p in paths)
+    if rows is not None:
+        sized = [(m, p) for m, p in sized if m == rows]
+    if not sized:
+        want = f"{config}-{rows}" if rows else f"{config}-*"
+        raise FileNotFoundError(f"no data/{want}.xmgb; run data/make_benchmarks.py")
+    return sized[0][1]
 
 
 def oracle_from_table(params, table, ids, threads=0):

@@ -73,5 +73,5 @@ def test_full_batch_slices_vs_oracle(env_name, config, n, steps):
     roll.reset(root)
     roll.rollout(steps, policy_keys=pk, record=())
     assert torch.equal(roll.grids, vec.grids)
-    assert torch.equal(roll.agent, vec.agent)
+    assert torch.equal(roll.state_words(), vec.state_words())
     assert torch.equal(roll.rng, vec.rng)

@@ -28,7 +28,7 @@ def _pair(env_name, config, n, resample=False, see=None, **kw):
 
 def _same_state(a, b, msg):
     torch.testing.assert_close(a.grids, b.grids, rtol=0, atol=0, msg=f"grids {msg}")
-    assert torch.equal(a.agent, b.agent), f"agent word {msg}"
+    assert torch.equal(a.state_words(), b.state_words()), f"agent word {msg}"
     assert torch.equal(a.rng, b.rng), f"rng {msg}"
 
 

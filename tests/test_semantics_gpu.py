@@ -120,4 +120,4 @@ def test_compute_obs_false_skips_only_observations():
         assert ta.observations is None
         assert torch.equal(ta.rewards, tb.rewards) and torch.equal(ta.step_types, tb.step_types)
         assert torch.equal(ta.discounts, tb.discounts)
-    assert torch.equal(a.grids, b.grids) and torch.equal(a.agent, b.agent) and torch.equal(a.rng, b.rng)
+    assert torch.equal(a.grids, b.grids) and torch.equal(a.state_words(), b.state_words()) and torch.equal(a.rng, b.rng)

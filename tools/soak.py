@@ -67,7 +67,7 @@ for c0 in range(0, steps, chunk):
 roll = VecEnv(params, n, bm)
 roll.reset(root)
 roll.rollout(steps, policy_keys=pk, record=())
-same = torch.equal(roll.grids, vec.grids) and torch.equal(roll.agent, vec.agent) and torch.equal(roll.rng, vec.rng)
+same = torch.equal(roll.grids, vec.grids) and torch.equal(roll.state_words(), vec.state_words()) and torch.equal(roll.rng, vec.rng)
 print(f"soak {env_name} n={n} steps={steps}: slice vs oracle {'ok' if not bad else 'FAILED'}; "
       f"full batch vs fused rollout {'identical' if same else 'DIFFERENT'}")
 sys.exit(0 if (not bad and same) else 1)
