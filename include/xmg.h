@@ -178,6 +178,18 @@ int32_t xmg_validate_actions(const void* actions, int32_t action_dtype, int64_t 
 int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* actions, int32_t action_dtype,
                  int64_t n, const xmg_out* out, const uint32_t* abort_flag, uint32_t epoch, void* stream);
 
+/* Reset-ahead (state.next_* non-NULL): xmg_step / xmg_steps of every epoch
+ * that is a multiple of `every` first launch one batch that pre-builds the
+ * next trial of the env class (epoch / every) mod `classes` (envs e with
+ * e mod classes == class) whose running trial has none yet; a trial that
+ * ends with its successor pre-built is reset by a copy.  xmg_ahead_plan
+ * returns (every, classes) for a description (every * classes <= budget - 2,
+ * so a trial that runs to the budget always meets its class);
+ * xmg_prebuild runs one batch explicitly (e.g. right after xmg_reset). */
+int32_t xmg_ahead_plan(const xmg_env_desc* desc, int64_t* every, int64_t* classes);
+int32_t xmg_prebuild(const xmg_env_desc* desc, const xmg_state* state, int64_t cls, int64_t classes, int64_t n,
+                     void* stream);
+
 /* `steps` consecutive xmg_step calls issued from one host call (no per-step
  * host round trip: the path for batches too small to hide ~20-30 us of
  * Python + launch overhead per step).  actions [steps][n] must already be

@@ -34,7 +34,7 @@ EXPORTS = ("xmg_abi_version", "xmg_last_error", "xmg_philox", "xmg_split_batch",
            "xmg_key_from_seed", "xmg_fold_in", "xmg_philox_host", "xmg_reset", "xmg_validate_actions",
            "xmg_step", "xmg_step_smem_bytes", "xmg_work_words", "xmg_profile", "xmg_profile_read", "xmg_rollout",
            "xmg_rollout_smem_bytes", "xmg_sprites", "xmg_image_obs", "xmg_steps", "xmg_image_atlas_bytes",
-           "xmg_image_atlas", "xmg_image_obs_aligned")
+           "xmg_image_atlas", "xmg_image_obs_aligned", "xmg_ahead_plan", "xmg_prebuild")
 
 
 class NativeLibraryError(RuntimeError):
@@ -102,6 +102,8 @@ def _bind(L):
         "xmg_image_atlas_bytes": ([i32], i64),
         "xmg_image_atlas": ([i32, vp, vp, vp], i32),
         "xmg_image_obs_aligned": ([vp, i64, i32, vp, vp, vp], i32),
+        "xmg_ahead_plan": ([C.POINTER(EnvDesc), vp, vp], i32),
+        "xmg_prebuild": ([C.POINTER(EnvDesc), C.POINTER(State), i64, i64, i64, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -44,6 +44,33 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
   return ((uint64_t)hi << 32) | lo;
 }
 
+// n bytes of the scratch grid (16-byte aligned shared memory, readable
+// up to 4 bytes past n) to a grid in global memory at any alignment: a few
+// head / tail bytes and 4-byte words, each assembled from two aligned shared
+// words with a funnel shift.
+__device__ __forceinline__ void warp_store_grid(uint8_t* dst, const uint8_t* src, int n, int lane) {
+  const int head = min((int)((4 - (reinterpret_cast<uintptr_t>(dst) & 3)) & 3), n);
+  if (lane < head) dst[lane] = src[lane];
+  const int words = (n - head) >> 2;
+  const int mis = head & 3;  // src offset of the body mod 4 (src is 16-byte aligned)
+  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src + head - mis);
+  uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + head);
+  for (int w = lane; w < words; w += 32) {
+    const uint32_t lo = s32[w], hi = s32[w + 1];
+    d32[w] = mis ? __funnelshift_r(lo, hi, 8 * mis) : lo;
+  }
+  for (int i = head + 4 * words + lane; i < n; i += 32) dst[i] = src[i];
+}
+
+// x mod d for d < 2^16 with 32-bit arithmetic only (the 64-bit remainder is a
+// long software sequence): x = hi * 2^32 + lo, so
+// x mod d = ((hi mod d) * (2^32 mod d) + lo mod d) mod d, every term < 2^32.
+__device__ __forceinline__ uint32_t mod64_small(uint64_t x, uint32_t d) {
+  const uint32_t t = (uint32_t)((0xFFFFFFFFu % d) + 1u) % d;  // 2^32 mod d
+  const uint32_t a = ((uint32_t)(x >> 32) % d) * t % d;
+  return (a + (uint32_t)x % d) % d;
+}
+
 // Row-major floor cells of the scratch grid into fc[]; returns their count
 // (the free list of ref:core.py:322-325, built with ballots).
 __device__ int build_free_list(const WarpScratch& ws, int HW, int lane) {
@@ -160,19 +187,34 @@ __device__ __forceinline__ int warp_select_fast(const uint64_t* wd, int lane, in
   }
   uint32_t c = cand;
   int tt = t, cc = cnt;
-  for (int b = 31; b >= 0 && cc > 1; --b) {
-    uint32_t z = 0;
+  // two bits (one base-4 digit) per round: the three digit counts are
+  // independent reductions, so a round costs about one reduction's latency
+  for (int b = 31; b >= 1 && cc > 1; b -= 2) {
+    uint32_t za = 0, zb = 0;  // bit b / bit b-1 of each element
 #pragma unroll
-    for (int j = 0; j < 4 * KR; ++j) z |= ((~hi[j] >> b) & 1u) << j;
-    z &= c;
-    const int zeros = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(z));
-    if (tt < zeros) {
-      c = z;
-      cc = zeros;
+    for (int j = 0; j < 4 * KR; ++j) {
+      za |= ((hi[j] >> b) & 1u) << j;
+      zb |= ((hi[j] >> (b - 1)) & 1u) << j;
+    }
+    const uint32_t d0 = c & ~(za | zb), d1 = c & ~za & zb, d2 = c & za & ~zb;
+    const int n0 = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(d0));
+    const int n1 = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(d1));
+    const int n2 = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(d2));
+    if (tt < n0) {
+      c = d0;
+      cc = n0;
+    } else if (tt < n0 + n1) {
+      c = d1;
+      tt -= n0;
+      cc = n1;
+    } else if (tt < n0 + n1 + n2) {
+      c = d2;
+      tt -= n0 + n1;
+      cc = n2;
     } else {
-      c &= ~z;
-      tt -= zeros;
-      cc -= zeros;
+      c &= za & zb;
+      tt -= n0 + n1 + n2;
+      cc -= n0 + n1 + n2;
     }
   }
   if (cc > 1) return warp_select(wd, lane, F, cand, cnt, t);
@@ -247,7 +289,7 @@ __device__ void rank_place(const WarpScratch& ws, int lane, int F, int W, int mo
   XMG_TRB(10);
   const int tail = total - spawn_base;
   if (tail > 0) {
-    const int fs = select_rank(ws.wd, lane, F, valid, total, spawn_base + (int)(spawn_word % (uint64_t)tail));
+    const int fs = select_rank(ws.wd, lane, F, valid, total, spawn_base + (int)mod64_small(spawn_word, (uint32_t)tail));
     if (lane == 0) reinterpret_cast<int*>(ws.misc + 32)[0] = ws.fc[fs];
   }
   __syncwarp();
@@ -287,6 +329,55 @@ __device__ __noinline__ void derive_trial_keys(uint64_t ek_hi, uint64_t ek_lo, b
   *out = k;
 }
 
+// The same keys for up to 16 envs at once, spread over the lanes in two
+// dependent rounds instead of five blocks in series per env: round 1 derives
+// ks = split(ek, 0) and st = split(ek, 1) (+ split(ek, 2) for resample) of
+// every env, round 2 the three children of ks (+ the resample draw).  Env
+// slot k is lane `base + k` of `m` (its episode key in that lane's ek);
+// results go to out[k].  Called by all 32 lanes.
+__device__ __noinline__ void derive_keys_group(uint32_t m, int base, uint64_t ek_hi, uint64_t ek_lo, bool resample,
+                                               TrialKeys* out, int lane) {
+  const int nb1 = resample ? 3 : 2, nb2 = resample ? 4 : 3;
+  const uint32_t slots = (m >> base) & 0xFFFFu;
+  if (!slots) return;
+  const int hi_slot = 32 - __clz(slots);  // slots 0 .. hi_slot-1 cover every env
+  for (int j0 = 0; j0 < nb1 * hi_slot; j0 += 32) {
+    const int j = j0 + lane, k = j / nb1, b = j - k * nb1;
+    const uint64_t eh = shfl64(ek_hi, (base + k) & 31), el = shfl64(ek_lo, (base + k) & 31);
+    if (j < nb1 * hi_slot && ((slots >> k) & 1)) {
+      const Words4 w = philox<2>((uint64_t)b, 0, kDomSplit, 0, eh, el);
+      TrialKeys& t = out[k];
+      if (b == 0) { t.k2h = w.w0; t.k2l = w.w1; }        // ks, parked in k2 until round 2
+      else if (b == 1) { t.st_hi = w.w0; t.st_lo = w.w1; }
+      else { t.task_word = w.w0; t.k0h = w.w1; }        // split(ek, 2), parked
+    }
+  }
+  __syncwarp();
+  for (int j0 = 0; j0 < nb2 * hi_slot; j0 += 32) {
+    const int j = j0 + lane, k = j / nb2, b = j - k * nb2;
+    const bool act = j < nb2 * hi_slot && ((slots >> k) & 1);
+    uint64_t kh = 0, kl = 0;
+    if (act) {
+      const TrialKeys& t = out[k];
+      kh = b < 3 ? t.k2h : t.task_word;
+      kl = b < 3 ? t.k2l : t.k0h;
+    }
+    __syncwarp();
+    if (act) {
+      const Words4 w = b < 3 ? philox<2>((uint64_t)b, 0, kDomSplit, 0, kh, kl) : philox<2>(0, 0, kDomDraw, 0, kh, kl);
+      TrialKeys& t = out[k];
+      if (b == 0) { t.k0h = w.w0; t.k0l = w.w1; }
+      else if (b == 1) { t.k1h = w.w0; t.k1l = w.w1; }
+      else if (b == 2) { t.k2h = w.w0; t.k2l = w.w1; }
+      else t.task_word = w.w0;
+    }
+    __syncwarp();
+  }
+  if (!resample)
+    for (int k = lane; k < hi_slot; k += 32) out[k].task_word = 0;
+  __syncwarp();
+}
+
 // Rebuild one env's trial with the scenario builders ref:scenarios.py:291-412
 // (batched: ref:vecenv.py:242-291).  Called by all 32 lanes with the same
 // arguments; writes the new grid to `gdst` (and leaves it in ws.grid) and
@@ -321,12 +412,13 @@ __device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
     nobj = 1;
     obj_lane = kGreenGoal;
   }
-  // base cells of this scenario (a byte per lane: measured faster in the
-  // rollout kernel than 16-byte read-only loads)
-  for (int i = lane; i < HW; i += 32) ws.grid[i] = d.base_cells[i];
+  // base cells of this scenario, 16 bytes per lane (base_cells and the
+  // scratch grid are 16-byte aligned and padded)
+  for (int i = lane; i < (HW + 15) >> 4; i += 32)
+    reinterpret_cast<uint4*>(ws.grid)[i] = __ldg(reinterpret_cast<const uint4*>(d.base_cells) + i);
   if (sc == XMG_SCENARIO_EMPTY) {  // ref:scenarios.py:320-327
     __syncwarp();
-    for (int i = lane; i < HW; i += 32) gdst[i] = ws.grid[i];
+    warp_store_grid(gdst, ws.grid, HW, lane);
     res.r = 1; res.c = 1; res.d = 1;
     res.goal = 2u | ((uint32_t)kGreenGoal << 8);
     if (lane == 0) *outp = res;
@@ -343,12 +435,12 @@ __device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
     const uint64_t w0 = shfl64(w.w0, 0), w1 = shfl64(w.w1, 0);
     int door_row;
     if (sc == XMG_SCENARIO_DOOR_KEY) {
-      wall_col = 2 + (int)(w0 % (uint64_t)(W - 4));
-      door_row = 1 + (int)(w1 % (uint64_t)(H - 2));
+      wall_col = 2 + (int)mod64_small(w0, (uint32_t)(W - 4));
+      door_row = 1 + (int)mod64_small(w1, (uint32_t)(H - 2));
       color = 7;  // yellow
     } else {
       wall_col = (W - 1) / 2;
-      door_row = 1 + (int)(w0 % (uint64_t)(H - 2));
+      door_row = 1 + (int)mod64_small(w0, (uint32_t)(H - 2));
       color = cGenColors[w1 % 10];
     }
     __syncwarp();
@@ -366,7 +458,7 @@ __device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
   // doors: ref:layouts.py:532-544 (segments never hold free cells)
   if (lane < nseg) {
     const int off = d.seg_off[lane], len = d.seg_off[lane + 1] - off;
-    const int pos = d.fixed_doors ? len / 2 : (int)(ws.misc[2 * lane] % (uint64_t)len);
+    const int pos = d.fixed_doors ? len / 2 : (int)mod64_small(ws.misc[2 * lane], (uint32_t)len);
     ws.grid[d.seg_cells[off + pos]] = (uint8_t)(kClosed * 16 + cGenColors[ws.misc[2 * lane + 1] % 10]);
   }
   const uint64_t a0 = ws.misc[24], a1 = ws.misc[25];
@@ -405,7 +497,7 @@ __device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
   const int spawn_cell = reinterpret_cast<const int*>(ws.misc + 32)[0];
   res.r = spawn_cell / W;
   res.c = spawn_cell - res.r * W;
-  for (int i = lane; i < HW; i += 32) gdst[i] = ws.grid[i];
+  warp_store_grid(gdst, ws.grid, HW, lane);
   if (lane == 0) *outp = res;
   __syncwarp();
   XMG_TRB(5);

@@ -27,32 +27,25 @@ constexpr int kWorkHeader = 4 * kQueues;
 __host__ __device__ inline int count_index(uint32_t parity, int kind, int q) {
   return (int)((parity & 1) * 2 * kQueues + kind * kQueues + q);
 }
-constexpr uint32_t kQPut = 1u << 31, kQReset = 1u << 30, kQPre = 1u << 29, kQEnv = (1u << 30) - 1;
-// reset-queue entries: env index | kEntPre for a pre-build (reset-ahead:
-// the env's NEXT trial, built into state.next_*, not released via `pending`)
-constexpr uint32_t kEntPre = 1u << 31;
+constexpr uint32_t kQPut = 1u << 31, kQReset = 1u << 30, kQEnv = (1u << 30) - 1;
 
 // ------------------------------------------------------- reset-ahead
 // A trial's successor is a function of the env's rng key and task only
 // (ref:vecenv.py:224-233 via :359-361), both fixed while the trial runs.  So
-// step_main queues each env once per trial, at step count >= prebuild_slot(e),
-// for step_rare to build its next trial into state.next_* (stage 1 in state
-// word bits 18-19); one step later the stage becomes 2.  A kernel launched
-// after the queueing step's step_rare finished may read the records: step_rare
-// of step t is a plain launch, so it starts only after everything before it
-// on the stream (step_rare of step t-1) has completed, and step_main of step
-// t+1 launches (programmatically) after it started.  When a trial ends at
-// stage 2, step_main copies the records (grid, state word, rng, first
-// observation) instead of queueing a rebuild; otherwise (a goal reached
-// before the pre-build was ready, or a PUT_DOWN that ends the trial) the
-// in-place rebuild of round 1 runs.  The slots spread the pre-builds
-// uniformly: 1 + e mod (budget - 2) <= budget - 2, so every budget end is
-// covered.
-constexpr uint64_t kStageMask = 3ull << 18;
-__host__ __device__ inline uint32_t prebuild_slot(int64_t e, int budget) {
-  return 1u + (uint32_t)(e % (int64_t)(budget - 2));
-}
-__device__ __forceinline__ bool ahead_on(const xmg_state& s, int budget) { return s.next_grids != nullptr && budget >= 3; }
+// every K-th step (host side, xmg_step) a plain launch of prebuild_kernel
+// builds the next trial of one class of envs (e mod B == class, B = the
+// classes that fit in budget - 2 steps) into state.next_* and marks them
+// stage 2 (state word 0 bits 18-19); the kernels after it see the records.
+// When a trial ends at stage 2, step_main copies the records (grid, state
+// word, rng, first observation) instead of queueing a rebuild; otherwise (a
+// goal reached before the env's class came up, a PUT_DOWN that ends the
+// trial) the in-place rebuild runs.  Every trial that runs to the budget
+// passes one batch of its class, so the synchronized budget resets are all
+// copies; the build work moves out of the burst and is done at full-GPU
+// efficiency once per K steps, without touching the step_rare / step_main
+// overlap.
+constexpr uint64_t kStageReady = 2ull << 18, kStageMask = 3ull << 18;
+__device__ __forceinline__ bool ahead_on(const xmg_state& s) { return s.next_grids != nullptr; }
 
 // capacity of one sub-queue: every env of the step_main CTAs (128 envs each) feeding it
 __host__ __device__ inline int64_t queue_cap(int64_t n) {
@@ -74,7 +67,9 @@ __host__ __device__ inline int64_t queue_base(int64_t n, uint32_t parity, int ki
 __host__ __device__ inline int64_t num_chunks(int64_t n) { return (n + kThreads - 1) / kThreads * kWarps; }
 __host__ __device__ inline int64_t pending_base(int64_t n) { return kWorkHeader + 4 * kQueues * queue_cap(n); }
 __host__ __device__ inline int64_t dirty_base(int64_t n) { return pending_base(n) + num_chunks(n); }
-__host__ __device__ inline int64_t work_words(int64_t n) { return pending_base(n) + 2 * num_chunks(n); }
+// then the two counter words of the reset-ahead batches (prebuild_kernel)
+__host__ __device__ inline int64_t prebuild_ctr_base(int64_t n) { return dirty_base(n) + num_chunks(n); }
+__host__ __device__ inline int64_t work_words(int64_t n) { return prebuild_ctr_base(n) + 2; }
 
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ ulonglong2 ld_cg_u64x2(const ulonglong2* p) {  // fresh from L2, not CSE'd
@@ -344,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
   uint32_t qflags = 0;
   float rew = 0.f;
   bool last = false, consume = false;
-  const bool ahead = ahead_on(s, d.budget);
+  const bool ahead = ahead_on(s);
   if (valid) {
     // ---- stage the post-action window (MOVE: both candidate poses) and,
     // for actions that can raise an event, the env's rule row
@@ -406,8 +401,7 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
     }
     // ---- counters and reward, ref:vecenv.py:351-357
     sc += 1;
-    const uint32_t stage_old = (uint32_t)(ag.x >> 18) & 3u;
-    uint32_t stage = stage_old == 1u ? 2u : stage_old;
+    const int stage = (int)(ag.x >> 18) & 3;  // reset-ahead: 2 = next trial pre-built
     if (ev == 2) {
       qflags = kQPut;  // rules, goal and reward resolved by step_rare
     } else {
@@ -424,47 +418,40 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
 #endif
       // auto-reset: the pre-built next trial when it is ready, else a rebuild
       if (last) {
-        if (ahead && stage_old == 2u) consume = true;
+        if (ahead && stage == 2) consume = true;
         else qflags = kQReset;
-      } else if (ahead && stage_old == 0u && sc >= prebuild_slot(e, d.budget)) {
-        qflags = kQPre;
-        stage = 1u;
       }
     }
     if (!consume) {
 #if XMG_L2HINT
-      st_hint_u64(s.agent + 2 * e, pack_agent(r, c, dir | (int)(stage << 2), pocket, sc), pol_keep);
+      st_hint_u64(s.agent + 2 * e, pack_agent(r, c, dir | (stage << 2), pocket, sc), pol_keep);
 #else
-      s.agent[2 * e] = pack_agent(r, c, dir | (int)(stage << 2), pocket, sc);
+      s.agent[2 * e] = pack_agent(r, c, dir | (stage << 2), pocket, sc);
 #endif
     }
   }
 
   // ---- defer the rare work: warp-aggregated append to this CTA's sub-queue
-  const uint32_t am = __ballot_sync(0xffffffffu, qflags != 0);
-  if (am) {
+  const uint32_t qm = __ballot_sync(0xffffffffu, qflags != 0);
+  if (qm) {
     const int k = (int)(tile % kQueues);
-    // envs step_rare rewrites (PUT_DOWN, rebuild) hold the chunk for the next
-    // step_main; pre-builds write only the next_* records and hold nothing
-    const uint32_t qm = __ballot_sync(0xffffffffu, (qflags & (kQPut | kQReset)) != 0);
-    if (lane == 0 && qm) {
+    if (lane == 0) {
       atomicAdd(pending, (uint32_t)__popc(qm));
       *dirty = epoch;
     }
-    // PUT_DOWN entries to their queue; rebuilds and pre-builds to the reset queue
+    // PUT_DOWN and reset entries go to their own queues
 #pragma unroll
     for (int kind = 0; kind < 2; ++kind) {
-      const bool mine = kind ? (qflags & (kQReset | kQPre)) != 0 : qflags == kQPut;
-      const uint32_t km = __ballot_sync(0xffffffffu, mine);
+      const uint32_t want = kind ? kQReset : kQPut;
+      const uint32_t km = __ballot_sync(0xffffffffu, qflags == want);
       if (!km) continue;
       const int leader = __ffs(km) - 1;
       uint32_t base = 0;
       if (lane == leader) base = atomicAdd(s.work + count_index(epoch, kind, k), (uint32_t)__popc(km));
       base = __shfl_sync(0xffffffffu, base, leader);
-      if (mine) {
+      if (qflags == want) {
         XMG_ASSERT(base + __popc(km & ((1u << lane) - 1)) < queue_cap(n));
-        s.work[queue_base(n, epoch, kind, k) + base + __popc(km & ((1u << lane) - 1))] =
-            (uint32_t)e | (qflags == kQPre ? kEntPre : 0u);
+        s.work[queue_base(n, epoch, kind, k) + base + __popc(km & ((1u << lane) - 1))] = (uint32_t)e;
       }
     }
   }

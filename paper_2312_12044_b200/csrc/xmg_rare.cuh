@@ -329,9 +329,8 @@ __device__ __forceinline__ void warp_reset_group(const xmg_env_desc& d, const xm
   // rebuilds those envs one by one
   for (int half = 0; half < 32; half += kKeySlots) {
     const bool in = mine && lane >= half && lane < half + kKeySlots;
-    if (in) derive_trial_keys(ek.x, ek.y, resample, keys + (lane - half));
     uint32_t m = __ballot_sync(0xffffffffu, in);
-    __syncwarp();
+    derive_keys_group(m, half, ek.x, ek.y, resample, keys, lane);
     while (m) {
       const int src = __ffs(m) - 1;
       m &= m - 1;
@@ -500,11 +499,9 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRar
       // ---- trials the PUT_DOWN finished: keys derived one env per lane, then
       // the envs rebuilt by the whole warp
       if (lastm) {
-        if ((lastm >> lane) & 1) {
-          const ulonglong2 ek = reinterpret_cast<const ulonglong2*>(s.rng)[e_l];
-          derive_trial_keys(ek.x, ek.y, resample, keys + lane);
-        }
-        __syncwarp();
+        ulonglong2 ek = make_ulonglong2(0, 0);
+        if ((lastm >> lane) & 1) ek = reinterpret_cast<const ulonglong2*>(s.rng)[e_l];
+        derive_keys_group(lastm, 0, ek.x, ek.y, resample, keys, lane);
         while (lastm) {
           const int src = __ffs(lastm) - 1;
           lastm &= lastm - 1;
@@ -527,14 +524,80 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRar
     for (int64_t i0 = jr; i0 < cnt_reset; i0 += 32 * (int64_t)rs_w) {
       const int64_t i = i0 + (int64_t)lane * rs_w;
       const bool mine = i < cnt_reset;
-      const uint32_t ent = mine ? qp[i] : 0u;
-      const bool pre = (ent & kEntPre) != 0;  // reset-ahead: build the next trial's records
-      const int64_t e = (int64_t)(ent & ~kEntPre);
-      warp_reset_group(d, sdesc, s, o, wbase, geo, keys, lane, mine, e, nullptr, gw, pre);
-      if (track) release_envs(s.work + pending_base(n), mine && !pre, e);
+      const int64_t e = mine ? (int64_t)qp[i] : 0;
+      warp_reset_group(d, sdesc, s, o, wbase, geo, keys, lane, mine, e, nullptr, gw);
+      if (track) release_envs(s.work + pending_base(n), mine, e);
     }
   }
 #ifdef XMG_TRACE
   XMG_TR(gw, 2, gtime());
 #endif
+}
+
+// ------------------------------------------------------- reset-ahead batch
+// prebuild_kernel (xmg_main.cuh "reset-ahead"): the next trial of every env
+// e = cls + B * i whose running trial has none yet (stage 0), built by a warp
+// per group of kPreGroup envs (keys derived lane-parallel) into state.next_*,
+// then marked stage 2.  Warps take groups from a counter (ctr[0]; the last CTA
+// to finish re-arms it), so no warp idles while groups remain.  A plain
+// launch between two steps: nothing else runs on the state meanwhile.
+#ifndef XMG_PRE_GROUP
+#define XMG_PRE_GROUP 8
+#endif
+#ifndef XMG_PRE_MINB
+#define XMG_PRE_MINB 6  // resident 4-warp CTAs per SM the register allocation targets
+#endif
+constexpr int kPreGroup = XMG_PRE_GROUP;  // envs per warp group (<= kKeySlots)
+static_assert(kPreGroup <= kKeySlots, "a group derives its keys at once");
+
+// per-warp scratch of prebuild_kernel: the build scratch, the trial keys and
+// the description (no PUT_DOWN prefetch area)
+__host__ __device__ inline int pre_warp_bytes(int H, int W) {
+  const int hwp = round16(H * W + 16);
+  return warp_scratch_bytes(hwp) + kKeySlots * (int)sizeof(TrialKeys) + round16((int)sizeof(xmg_env_desc));
+}
+
+__global__ void __launch_bounds__(kRareWarps * 32, XMG_PRE_MINB)
+    prebuild_kernel(const xmg_env_desc d, const xmg_state s, int64_t cls, int64_t B, int64_t n, uint32_t* ctr) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t count = cls < n ? (n - cls + B - 1) / B : 0;
+  const int64_t groups = (count + kPreGroup - 1) / kPreGroup;
+  const int ws_bytes = pre_warp_bytes(d.height, d.width);
+  const int hwp = round16(d.height * d.width + 16);
+  uint8_t* wbase = smem + warp * ws_bytes;
+  TrialKeys* keys = reinterpret_cast<TrialKeys*>(wbase + warp_scratch_bytes(hwp));
+  xmg_env_desc* sdesc = reinterpret_cast<xmg_env_desc*>(wbase + warp_scratch_bytes(hwp) +
+                                                        kKeySlots * (int)sizeof(TrialKeys));
+  if (lane == 0) *sdesc = d;
+  __syncwarp();
+  RareGeo geo;  // the fields warp_reset_env reads
+  geo.hwp = hwp;
+  const xmg_out none = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  for (;;) {
+    int64_t g = 0;
+    if (lane == 0) g = atomicAdd(ctr, 1u);
+    g = __shfl_sync(0xffffffffu, g, 0);
+    if (g >= groups) break;
+    const int64_t i = g * kPreGroup + lane;
+    const int64_t e = cls + B * i;
+    uint64_t w0 = 0;
+    bool need = false;
+    if (lane < kPreGroup && i < count) {
+      w0 = s.agent[2 * e];
+      need = (w0 & kStageMask) == 0;
+    }
+    warp_reset_group(d, sdesc, s, none, wbase, geo, keys, lane, need, e, nullptr, 0, true);
+    if (need) s.agent[2 * e] = w0 | kStageReady;
+  }
+  // the last CTA re-arms the counter for the next batch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+      __threadfence();
+    }
+  }
 }

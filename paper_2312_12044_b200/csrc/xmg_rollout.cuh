@@ -223,8 +223,7 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
       for (int half = 0; half < 32; half += kRollKeySlots) {
       uint32_t hm = lm & (kRollKeySlots == 32 ? 0xffffffffu : (((1u << kRollKeySlots) - 1u) << half));
       if (!hm) continue;
-      if ((hm >> lane) & 1) derive_trial_keys(rk.x, rk.y, resample, keys + (lane - half));
-      __syncwarp();
+      derive_keys_group(hm, half, rk.x, rk.y, resample, keys, lane);
       for (; hm; hm &= hm - 1) {
         const int src = __ffs(hm) - 1;
         const int tk = __shfl_sync(0xffffffffu, task, src);

@@ -186,6 +186,60 @@ cudaError_t allow_smem(K kernel, int64_t dyn) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem - (int)fa.sharedSizeBytes);
 }
 
+// Per-device facts and kernel attributes (SM count, the >48 KB dynamic
+// shared-memory opt-in of the step / rare / pre-build / rollout kernels):
+// attributes belong to the device context, so they are set once per device,
+// not once per process (a process may drive several GPUs).
+struct DevInfo {
+  bool done = false;
+  int sms = 0;
+  cudaError_t err = cudaSuccess;
+  const char* what = "";
+  int64_t rare_smem = -1;  // occupancy cache of step_rare for this scratch size
+  int rare_per_sm = 0;
+};
+constexpr int kMaxDevices = 64;
+DevInfo g_dev[kMaxDevices];
+std::mutex g_dev_mu;
+
+template <typename K>
+bool set_attr(DevInfo& di, K kernel, const char* what) {
+  if (di.err != cudaSuccess) return false;
+  di.err = allow_smem(kernel, kMaxDynSmem - 1024);
+  di.what = what;
+  return di.err == cudaSuccess;
+}
+
+int device_attrs(int dev) {
+  if (dev < 0 || dev >= kMaxDevices) return fail("device index out of range");
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  DevInfo& di = g_dev[dev];
+  if (!di.done) {
+    cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
+    set_attr(di, step_main<6, false>, "step_main") && set_attr(di, step_main<8, false>, "step_main") &&
+        set_attr(di, step_main<12, false>, "step_main") && set_attr(di, step_main<16, false>, "step_main") &&
+        set_attr(di, step_main<32, false>, "step_main") && set_attr(di, step_main<6, true>, "step_main") &&
+        set_attr(di, step_main<8, true>, "step_main") && set_attr(di, step_main<12, true>, "step_main") &&
+        set_attr(di, step_rare, "step_rare") && set_attr(di, prebuild_kernel, "prebuild_kernel") &&
+        set_attr(di, rollout_kernel, "rollout_kernel");
+    di.done = true;
+  }
+  if (di.err != cudaSuccess) return fail(std::string(di.what) + " attributes: " + cudaGetErrorString(di.err));
+  if (di.sms < 1) return fail("no SM count for this device");
+  return 0;
+}
+
+// The current device's entry (after device_attrs); nullptr on failure.
+DevInfo* cur_dev() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    fail("cudaGetDevice failed");
+    return nullptr;
+  }
+  if (device_attrs(dev)) return nullptr;
+  return &g_dev[dev];
+}
+
 // XMG_PDL=0 turns the programmatic (overlapped) launches off
 bool pdl_enabled() {
   static int on = -1;
@@ -198,19 +252,16 @@ bool pdl_enabled() {
 
 template <int MAXCH, bool FULL>
 int launch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
-                const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st) {
+                const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st, bool pdl) {
   const MainGeo geo = make_main_geo(d->view_size, MAXCH, d->rule_width);
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] { attr_err = allow_smem(step_main<MAXCH, FULL>, kMaxDynSmem - 1024); });
-  if (attr_err != cudaSuccess) return fail(std::string("step_main attributes: ") + cudaGetErrorString(attr_err));
+  if (!cur_dev()) return -1;
   const int64_t blocks = (n + kThreads - 1) / kThreads;
   // programmatic dependent of the previous kernel on the stream (the previous
   // step's step_rare, or this step's validation)
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl && pdl_enabled() ? 1 : 0;
   cfg.gridDim = dim3((unsigned)blocks);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = (size_t)geo.total;
@@ -229,30 +280,18 @@ bool grid_fits(const xmg_env_desc* d) { return d->height * d->width <= 1024; }
 int launch_rare(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const uint64_t* keys,
                 const uint32_t* flag, uint32_t epoch, int64_t n, int track, cudaStream_t st) {
   const RareGeo geo = make_rare_geo(d->height, d->width, d->rule_width);
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] { attr_err = allow_smem(step_rare, kMaxDynSmem - 1024); });
-  if (attr_err != cudaSuccess) return fail(std::string("step_rare attributes: ") + cudaGetErrorString(attr_err));
-  // one resident wave (warps stride over their sub-queue's entries); a
-  // multiple of 32 CTAs so every sub-queue gets equal warps
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  DevInfo* di = cur_dev();
+  if (!di) return -1;
+  const int sms = di->sms;
+  // resident CTAs per SM for this scratch size (cached per device: the query
+  // costs microseconds of host time per launch, which small batches feel)
+  if (di->rare_smem != geo.total) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&di->rare_per_sm, step_rare, kRareWarps * 32,
+                                                      (size_t)geo.total) != cudaSuccess)
+      di->rare_per_sm = 0;
+    di->rare_smem = geo.total;
   }
-  // resident CTAs per SM for this scratch size (cached: the query costs
-  // microseconds of host time per launch, which small batches feel)
-  static thread_local int64_t cached_smem = -1;
-  static thread_local int cached_per_sm = 0;
-  if (cached_smem != geo.total) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per_sm, step_rare, kRareWarps * 32,
-                                                      (size_t)geo.total) !=
-        cudaSuccess)
-      cached_per_sm = 0;
-    cached_smem = geo.total;
-  }
-  int per_sm = cached_per_sm;
+  int per_sm = di->rare_per_sm;
   if (per_sm < 1) return fail("step_rare does not fit on an SM");
   // At most ~20 resident step_rare warps per SM: the kernel overlaps the next
   // step's step_main, and beyond that it crowds step_main's CTAs out
@@ -315,29 +354,74 @@ bool use_full(const xmg_env_desc* d) {
 }
 
 int dispatch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
-                  const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st) {
+                  const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st, bool pdl = true) {
   if (use_full(d)) {
     const int fc = full_chunks(d->height * d->width);
-    if (fc <= 6) return launch_main<6, true>(d, s, o, actions, dtype, flag, epoch, n, st);
-    if (fc <= 8) return launch_main<8, true>(d, s, o, actions, dtype, flag, epoch, n, st);
-    return launch_main<12, true>(d, s, o, actions, dtype, flag, epoch, n, st);
+    if (fc <= 6) return launch_main<6, true>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
+    if (fc <= 8) return launch_main<8, true>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
+    return launch_main<12, true>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
   }
   switch (pick_maxch(d)) {
-    case 6: return launch_main<6, false>(d, s, o, actions, dtype, flag, epoch, n, st);
-    case 8: return launch_main<8, false>(d, s, o, actions, dtype, flag, epoch, n, st);
-    case 12: return launch_main<12, false>(d, s, o, actions, dtype, flag, epoch, n, st);
-    case 16: return launch_main<16, false>(d, s, o, actions, dtype, flag, epoch, n, st);
-    default: return launch_main<32, false>(d, s, o, actions, dtype, flag, epoch, n, st);
+    case 6: return launch_main<6, false>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
+    case 8: return launch_main<8, false>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
+    case 12: return launch_main<12, false>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
+    case 16: return launch_main<16, false>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
+    default: return launch_main<32, false>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
   }
+}
+
+// Reset-ahead batches (xmg_main.cuh): every `every`-th epoch, the class
+// (epoch / every) mod B of envs gets its next trial pre-built, B = the number
+// of classes whose cycle fits in budget - 2 steps (so every trial that runs
+// to the budget meets its class once).  XMG_AHEAD_EVERY overrides `every`.
+struct AheadPlan {
+  int64_t every, classes;
+};
+AheadPlan ahead_plan(const xmg_env_desc* d) {
+  static int every_env = -1;
+  if (every_env < 0) {
+    const char* v = getenv("XMG_AHEAD_EVERY");
+    every_env = v ? std::max(1, atoi(v)) : 16;
+  }
+  const int64_t span = std::max<int64_t>(1, (int64_t)d->budget - 2);
+  const int64_t every = std::min<int64_t>(every_env, span);
+  return {every, std::max<int64_t>(1, span / every)};
+}
+
+int launch_prebuild(const xmg_env_desc* d, const xmg_state* s, int64_t cls, int64_t classes, int64_t n,
+                    cudaStream_t st) {
+  const int64_t smem = (int64_t)kRareWarps * pre_warp_bytes(d->height, d->width);
+  const DevInfo* di = cur_dev();
+  if (!di) return -1;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prebuild_kernel, kRareWarps * 32, (size_t)smem) !=
+          cudaSuccess ||
+      per_sm < 1)
+    return fail("prebuild_kernel does not fit on an SM");
+  const int64_t count = (n - cls + classes - 1) / classes;
+  const int64_t need = (count + (int64_t)kRareWarps * kPreGroup - 1) / ((int64_t)kRareWarps * kPreGroup);
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * di->sms, need));
+  prebuild_kernel<<<(unsigned)blocks, kRareWarps * 32, (size_t)smem, st>>>(*d, *s, cls, classes, n,
+                                                                          s->work + prebuild_ctr_base(n));
+  return check_launch("prebuild_kernel");
+}
+
+// The reset-ahead batch of this epoch, if any; returns 1 when one was
+// launched (the step's first kernel then waits for it: no programmatic
+// overlap with it), 0 when not, <0 on error.
+int maybe_prebuild(const xmg_env_desc* d, const xmg_state* s, uint32_t epoch, int64_t n, cudaStream_t st) {
+  if (s->next_grids == nullptr) return 0;
+  const AheadPlan p = ahead_plan(d);
+  if (epoch % (uint64_t)p.every != 0) return 0;
+  const int64_t cls = (int64_t)((epoch / (uint64_t)p.every) % (uint64_t)p.classes);
+  if (cls >= n) return 0;
+  return launch_prebuild(d, s, cls, p.classes, n, st) ? -1 : 1;
 }
 
 int launch_rollout(const xmg_env_desc* d, const xmg_state* s, const uint64_t* pkeys, const uint8_t* actions,
                    int64_t t0, int64_t steps, int64_t n, const xmg_out* o, cudaStream_t st) {
   const RollGeo geo = make_roll_geo(d->height, d->width, d->view_size, d->rule_width);
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] { attr_err = allow_smem(rollout_kernel, kMaxDynSmem - 1024); });
-  if (attr_err != cudaSuccess) return fail(std::string("rollout_kernel attributes: ") + cudaGetErrorString(attr_err));
+  if (!cur_dev()) return -1;
   if (geo.total > kMaxDynSmem - 1024) return fail("grid too large for the rollout kernel's shared-memory state");
   const int64_t chunks = (n + 31) / 32;
   const int64_t blocks = (chunks + kRollWarps - 1) / kRollWarps;
@@ -405,12 +489,9 @@ int32_t xmg_validate_actions(const void* actions, int32_t dtype, int64_t n, uint
   if (n <= 0) return 0;
   if (dtype < 0 || dtype > 2) return fail("unknown action dtype");
   if (!flag) return fail("null flag");
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const DevInfo* di = cur_dev();
+  if (!di) return -1;
+  const int sms = di->sms;
 #ifndef XMG_VAL_SMS
 #define XMG_VAL_SMS 1  // validation CTAs per SM (at most)
 #endif
@@ -451,8 +532,11 @@ int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* a
     return fail("actions / grids / agent / obs buffers must be 16-byte aligned");
   cudaEvent_t ev[3];
   const bool prof = g_prof.on && prof_events(ev);
+  const int pre = maybe_prebuild(desc, state, epoch, n, (cudaStream_t)stream);
+  if (pre < 0) return -1;
   if (prof) cudaEventRecord(ev[0], (cudaStream_t)stream);
-  if (dispatch_main(desc, state, out, actions, action_dtype, abort_flag, epoch, n, (cudaStream_t)stream)) return -1;
+  if (dispatch_main(desc, state, out, actions, action_dtype, abort_flag, epoch, n, (cudaStream_t)stream, pre == 0))
+    return -1;
   if (prof) cudaEventRecord(ev[1], (cudaStream_t)stream);
   // step_main (window mode) records the tiles step_rare must release
   const int track = 1;
@@ -482,7 +566,9 @@ int32_t xmg_steps(const xmg_env_desc* desc, const xmg_state* state, const void* 
     if (o.step_type) o.step_type += k * n;
     const uint32_t ep = epoch0 + (uint32_t)k + 1u;
     const void* a = reinterpret_cast<const uint8_t*>(actions) + k * n * asz;
-    if (dispatch_main(desc, state, &o, a, action_dtype, nullptr, ep, n, (cudaStream_t)stream)) return -1;
+    const int pre = maybe_prebuild(desc, state, ep, n, (cudaStream_t)stream);
+    if (pre < 0) return -1;
+    if (dispatch_main(desc, state, &o, a, action_dtype, nullptr, ep, n, (cudaStream_t)stream, pre == 0)) return -1;
     if (launch_rare(desc, state, &o, nullptr, nullptr, ep, n, track, (cudaStream_t)stream)) return -1;
   }
   return 0;
@@ -522,6 +608,23 @@ int64_t xmg_step_smem_bytes(const xmg_env_desc* desc) {
 
 int64_t xmg_work_words(int64_t n) { return work_words(n); }
 
+int32_t xmg_prebuild(const xmg_env_desc* desc, const xmg_state* state, int64_t cls, int64_t classes, int64_t n,
+                     void* stream) {
+  if (validate_desc(desc, state, n)) return -1;
+  if (!state->next_grids) return fail("xmg_prebuild needs the reset-ahead buffers");
+  if (classes < 1 || cls < 0 || cls >= classes) return fail("need 0 <= cls < classes");
+  if (cls >= n) return 0;
+  return launch_prebuild(desc, state, cls, classes, n, (cudaStream_t)stream);
+}
+
+int32_t xmg_ahead_plan(const xmg_env_desc* desc, int64_t* every, int64_t* classes) {
+  if (!desc) return fail("null env description");
+  const AheadPlan p = ahead_plan(desc);
+  if (every) *every = p.every;
+  if (classes) *classes = p.classes;
+  return 0;
+}
+
 int32_t xmg_rollout(const xmg_env_desc* desc, const xmg_state* state, const uint64_t* policy_keys,
                     const uint8_t* actions, int64_t t0, int64_t steps, int64_t n, const xmg_out* traj,
                     void* stream) {
@@ -550,12 +653,9 @@ int32_t xmg_image_obs(const uint8_t* obs, int64_t n, int32_t view, const uint8_t
   if (!obs || !atlas || !out) return fail("null buffer");
   if (reinterpret_cast<uintptr_t>(out) & 15) return fail("image buffer must be 16-byte aligned");
   if (n <= 0) return 0;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const DevInfo* di = cur_dev();
+  if (!di) return -1;
+  const int sms = di->sms;
   const int64_t blocks = std::min<int64_t>(n, (int64_t)sms * 12);
   image_kernel<<<(unsigned)blocks, kImageWords, 0, (cudaStream_t)stream>>>(obs, n, view, kImageSide / view, atlas,
                                                                           out);
@@ -582,12 +682,9 @@ int32_t xmg_image_obs_aligned(const uint8_t* obs, int64_t n, int32_t view, const
   if (!obs || !aligned || !out) return fail("null buffer");
   if (reinterpret_cast<uintptr_t>(out) & 15) return fail("image buffer must be 16-byte aligned");
   if (n <= 0) return 0;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const DevInfo* di = cur_dev();
+  if (!di) return -1;
+  const int sms = di->sms;
   const int64_t blocks = std::min<int64_t>(n, (int64_t)sms * 12);
   image_kernel_aligned<<<(unsigned)blocks, kImgThreads, 0, (cudaStream_t)stream>>>(obs, n, view, aligned, out);
   return check_launch("image_kernel_aligned");
