@@ -584,6 +584,10 @@ def run_ours(args):
     if not args.no_block and (n * 2 * v ** 2) % 16 == 0:
         from paper_2312_12044_b200.vecenv import Trajectory
         bk = int(max(1, min(64, 8e9 // (n * (2 * v ** 2 + 9)))))  # record buffer <= 8 GB
+
+        def part(tr, k):  # the first k records of the reused buffer (no allocation in the window)
+            return tr if k == bk else Trajectory(tr.observations[:k], tr.rewards[:k], tr.discounts[:k],
+                                                 tr.step_types[:k])
         traj = Trajectory(torch.empty((bk, n, v, v, 2), dtype=torch.uint8, device=dev),
                           torch.empty((bk, n), dtype=torch.float32, device=dev),
                           torch.empty((bk, n), dtype=torch.float32, device=dev),
@@ -592,7 +596,7 @@ def run_ours(args):
         t = 0
         while t < start:
             k = min(bk, start - t)
-            vec.steps(actions[t:t + k], validate=False, out=traj if k == bk else None)
+            vec.steps(actions[t:t + k], validate=False, out=part(traj, k))
             t += k
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -601,7 +605,7 @@ def run_ours(args):
         b0.record(stream)
         while t < total:
             k = min(bk, total - t)
-            vec.steps(actions[t:t + k], validate=False, out=traj if k == bk else None)
+            vec.steps(actions[t:t + k], validate=False, out=part(traj, k))
             t += k
         b1.record(stream)
         torch.cuda.synchronize(dev)
@@ -627,6 +631,12 @@ def run_ours(args):
             if start:
                 vec.rollout(start, policy_keys=pkeys, t0=0, record=())
             traj = vec.rollout(chunk, policy_keys=pkeys, t0=start, record=rec) if rec else None  # allocate
+            if traj is not None:
+                from paper_2312_12044_b200.vecenv import Trajectory as _T
+
+                def rpart(k, tr=traj):  # the first k records of the reused buffer
+                    return tr if k == chunk else _T(tr.observations[:k], tr.rewards[:k], tr.discounts[:k],
+                                                    tr.step_types[:k])
             vec.reset(key_from_seed(0))
             if start:
                 vec.rollout(start, policy_keys=pkeys, t0=0, record=())
@@ -640,7 +650,7 @@ def run_ours(args):
             while t < total:
                 k = min(chunk, total - t)
                 if rec:
-                    vec.rollout(k, policy_keys=pkeys, t0=t, record=rec, out=traj if k == chunk else None)
+                    vec.rollout(k, policy_keys=pkeys, t0=t, record=rec, out=rpart(k))
                 else:
                     vec.rollout(k, policy_keys=pkeys, t0=t, record=())
                 t += k

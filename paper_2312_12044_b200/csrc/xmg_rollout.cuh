@@ -64,6 +64,28 @@ __device__ XMG_ROLL_POLICY_INLINE uint32_t policy_block(uint64_t kh, uint64_t kl
          ((uint32_t)(w.w3 % 6) << 24);
 }
 
+// The auto-resets of the lanes in cm from their pre-built records: the grid
+// bytes into the warp's shared grids (runs of consecutive lanes are
+// contiguous in both), and each lane's next state words returned.
+__device__ __noinline__ ulonglong4 roll_consume(const xmg_state s, uint32_t cm, int64_t e0, int HW, uint8_t* grids,
+                                                int lane) {
+  ulonglong4 out = make_ulonglong4(0, 0, 0, 0);
+  if ((cm >> lane) & 1) {
+    const ulonglong2* ns = reinterpret_cast<const ulonglong2*>(s.next_state) + 2 * (e0 + lane);
+    const ulonglong2 w = __ldcg(ns), k = __ldcg(ns + 1);
+    out = make_ulonglong4(w.x, w.y, k.x, k.y);
+  }
+  for (uint32_t m = cm; m;) {
+    const int a = __ffs(m) - 1;
+    const uint32_t gap = ~m & ~((1u << a) - 1u);
+    const int b = gap ? __ffs(gap) - 1 : 32;
+    m = b < 32 ? m & (~0u << b) : 0u;
+    warp_copy_cg(grids + a * HW, s.next_grids + (e0 + a) * HW, (b - a) * HW, lane);
+  }
+  __syncwarp();
+  return out;
+}
+
 __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel(const xmg_env_desc d, const xmg_state s,
                                                                  const uint64_t* pkeys, const uint8_t* actions,
                                                                  int64_t t0, int64_t T, int64_t n, const xmg_out o) {
@@ -113,8 +135,10 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
   int r = (int)(ag.x & 0xff), c = (int)((ag.x >> 8) & 0xff), dir = (int)((ag.x >> 16) & 3);
   int pocket = (int)((ag.x >> 24) & 0xff);
   uint32_t sc = (uint32_t)(ag.x >> 32);
-  // reset-ahead stage (xmg_main.cuh): kept while the trial runs (its next_*
-  // records stay valid for step_main), cleared by an in-kernel rebuild
+  // reset-ahead (xmg_main.cuh): stage 2 = the next trial's records are in
+  // next_* (pre-built by the batches VecEnv.rollout launches before this
+  // kernel, or by earlier steps); a trial ending at stage 2 is reset by
+  // copying them into the warp's grid (roll_consume)
   int stage = (int)((ag.x >> 18) & 3);
   uint32_t goal_word = (uint32_t)ag.y;
   int task = (int)(ag.y >> 32);
@@ -220,6 +244,27 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
     if (lm) {
       if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // obs buffers free
       __syncwarp();
+      // pre-built successors: the records in (out of line: keeps the step
+      // loop's code small), state into the lane's registers
+      const uint32_t cm = __ballot_sync(0xffffffffu, last && stage == 2);
+      if (cm) {
+        const ulonglong4 w = roll_consume(s, cm, e0, HW, grids, lane);
+        if ((cm >> lane) & 1) {
+          r = (int)(w.x & 0xff);
+          c = (int)((w.x >> 8) & 0xff);
+          dir = (int)((w.x >> 16) & 3);
+          pocket = 0;
+          sc = 0;
+          stage = 0;
+          goal_word = (uint32_t)w.y;
+          task = (int)(w.y >> 32);
+          rk = make_ulonglong2(w.z, w.w);
+        }
+        if (resample)
+          for (uint32_t m = cm; m; m &= m - 1) load_row(__ffs(m) - 1, __shfl_sync(0xffffffffu, task, __ffs(m) - 1));
+        __syncwarp();
+        lm &= ~cm;
+      }
       for (int half = 0; half < 32; half += kRollKeySlots) {
       uint32_t hm = lm & (kRollKeySlots == 32 ? 0xffffffffu : (((1u << kRollKeySlots) - 1u) << half));
       if (!hm) continue;

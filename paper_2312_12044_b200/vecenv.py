@@ -270,6 +270,14 @@ class VecEnv:
             raise _lib.NativeLibraryError(f"{h}x{w} grids exceed the shared-memory budget of this build")
         self._outs = None
         self._out_cache: dict = {}
+        # reset-ahead batch plan (xmg_ahead_plan): every `every`-th step one
+        # class (e mod classes) of envs gets its next trial pre-built; step()
+        # schedules by epoch inside libxmg, rollout() by its own step clock
+        if self.reset_ahead:
+            ev, cl = C.c_int64(), C.c_int64()
+            _lib.check(_lib.lib().xmg_ahead_plan(C.byref(self._desc), C.byref(ev), C.byref(cl)), "xmg_ahead_plan")
+            self._ahead_every, self._ahead_classes = int(ev.value), int(cl.value)
+        self._roll_clock = 0
         self._desc_ref = C.byref(self._desc)
         self._state_ref = C.byref(self._state)
         self._flag_ptr = self._flag.data_ptr()
@@ -506,7 +514,25 @@ class VecEnv:
                 torch.empty((steps, n), dtype=torch.int8, device=dev) if "step_types" in record else None)
         return self._launch_rollout(steps, policy_keys, actions, t0, out)
 
+    def _rollout_prebuilds(self, steps: int) -> None:
+        """The reset-ahead batches `steps` step() calls would launch (one per
+        `every` steps of the rollout clock), run before the fused kernel: the
+        trials that end inside the rollout are then reset by copies."""
+        if not self.reset_ahead:
+            return
+        ev, cl = self._ahead_every, self._ahead_classes
+        L = _lib.lib()
+        stream = _stream(self.device)
+        first = self._roll_clock // ev + 1
+        last = (self._roll_clock + steps) // ev
+        for j in range(first, last + 1)[:cl]:  # one cycle covers every class
+            _lib.check(L.xmg_prebuild(self._desc_ref, self._state_ref, j % cl, cl, self.num_envs, stream),
+                       "xmg_prebuild")
+            self.launches += 1
+        self._roll_clock += steps
+
     def _launch_rollout(self, steps: int, policy_keys, actions, t0: int, out: Trajectory) -> Trajectory:
+        self._rollout_prebuilds(steps)
         o = _lib.Out(_ptr(out.observations), _ptr(out.rewards), _ptr(out.discounts), _ptr(out.step_types),
                      _ptr(self.stats))
         _lib.check(_lib.lib().xmg_rollout(C.byref(self._desc), C.byref(self._state), _ptr(policy_keys),

@@ -28,7 +28,13 @@ vec.reset(key_from_seed(0))
 pk = policy_keys(key_from_seed(1), n, device=dev)
 vec.rollout(pre, policy_keys=pk, t0=0, record=())
 rec = ("observations", "rewards", "discounts", "step_types") if records else ()
-traj = None
+from paper_2312_12044_b200.vecenv import Trajectory  # noqa: E402
+v = params.view_size
+traj = Trajectory(torch.zeros((chunk, n, v, v, 2), dtype=torch.uint8, device=dev),
+                  torch.zeros((chunk, n), dtype=torch.float32, device=dev),
+                  torch.zeros((chunk, n), dtype=torch.float32, device=dev),
+                  torch.zeros((chunk, n), dtype=torch.int8, device=dev)) if records else None
+torch.cuda.synchronize()
 t = pre
 times = []
 for i in range(launches):
