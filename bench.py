@@ -399,7 +399,7 @@ def run_ours(args):
     if args.envs:
         n = args.envs
     offset, n = shard_range(n * world, rank, world)  # weak scaling: n envs per GPU
-    params, bm, vec = make_workload(args.workload, dev, n, offset)
+    params, bm, vec = make_workload(args.workload, dev, n, offset, graph=args.graph)
     budget = params.step_budget
     K, W = args.steps, args.warmup
     pre, start = window_plan(budget, K, W)
@@ -485,8 +485,11 @@ def run_ours(args):
     import ctypes as C
     m_ms, r_ms, nst = C.c_double(), C.c_double(), C.c_int64()
     L.xmg_profile_read(C.byref(m_ms), C.byref(r_ms), C.byref(nst))
-    main_ms = m_ms.value / max(nst.value, 1)
-    rare_ms = r_ms.value / max(nst.value, 1)
+    if nst.value:
+        main_ms = m_ms.value / nst.value
+        rare_ms = r_ms.value / nst.value
+    else:  # graph mode: the one fused kernel per step is the whole step
+        main_ms, rare_ms = ms_max / K, 0.0
     rules = vec.table.rule_width if params.scenario == "xland" else 0
     h, w, v = params.height, params.width, params.view_size
     bpe = algorithmic_bytes(h, w, rules, v)
@@ -534,8 +537,9 @@ def run_ours(args):
     # t+1 computes while the record of step t crosses PCIe.
     e2e = None
     if not args.no_e2e:
-        vec.reuse_outputs = False
-        vec._outs = None
+        if not vec.graph:
+            vec.reuse_outputs = False
+            vec._outs = None
         advance(vec, start)
         copy_stream = torch.cuda.Stream(dev)
         ke = min(K, args.e2e_steps)
@@ -566,6 +570,8 @@ def run_ours(args):
                     dst.copy_(src, non_blocking=True)
                     src.record_stream(copy_stream)
                 done_ev[sl].record(copy_stream)
+            if vec.graph:  # graph mode writes fixed record buffers: the copy precedes the next step
+                stream.wait_event(done_ev[sl])
         stream.wait_stream(copy_stream)
         e1.record(stream)
         torch.cuda.synchronize(dev)
@@ -717,6 +723,8 @@ def run_ours(args):
                                                                  if shared else ""),
                        "timed_window": f"steps [{start}, {total}) incl. budget reset burst at t={budget}",
                        "reset_ahead": bool(vec.reset_ahead),
+                       "step_path": "graph: xmg_step_fused (one kernel per step) replayed from a CUDA graph"
+                                    if vec.graph else "xmg_step: validate + step_main + step_rare (PDL-overlapped)",
                        "l2": "inputs larger than L2" if n * params.height * params.width > 126e6
                              else "state resident in L2 (small workload)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
@@ -757,6 +765,8 @@ def main():
     ap.add_argument("--no-block", action="store_true")
     ap.add_argument("--fused-chunk", type=int, default=32)
     ap.add_argument("--no-windows", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="VecEnv(graph=True): one fused kernel per step replayed from a CUDA graph (small batches)")
     ap.add_argument("--no-rulegrid", action="store_true")
     ap.add_argument("--rulegrid-envs", type=int, default=2048, help="envs per rulegrid worker")
     ap.add_argument("--rulegrid-steps", type=int, default=20)

@@ -225,6 +225,27 @@ int32_t xmg_rollout(const xmg_env_desc* desc, const xmg_state* state, const uint
                     const uint8_t* actions, int64_t t0, int64_t steps, int64_t n, const xmg_out* traj,
                     void* stream);
 
+/* One xmg_step as ONE kernel (the fused rollout kernel for a single step),
+ * for small batches where launches dominate, and capturable in a CUDA graph:
+ * every CTA first checks all n u8 actions against [0, 6) (ref
+ * vecenv.py:297-301) and an invalid batch changes nothing; the step number is
+ * a device counter, so a replayed graph needs no host epoch.
+ * gflag: XMG_FLAG_WORDS device u32, zero-initialised once, used only by this
+ * entry point: [0] the number of the last rejected step, [2] CTA counter,
+ * [3] steps issued (read it after a sync to match [0]).  Same records as
+ * xmg_step (obs nullable; reward / discount / step type required); does not
+ * consume an epoch of the two-kernel path (state.work unused). */
+int32_t xmg_step_fused(const xmg_env_desc* desc, const xmg_state* state, const uint8_t* actions /*[n] u8*/, int64_t n,
+                       const xmg_out* out, uint32_t* gflag, void* stream);
+
+/* xmg_step_fused captured once into an executable CUDA graph bound to these
+ * buffers (actions: a fixed staging buffer the caller fills before each
+ * launch); xmg_graph_launch replays one step (host cost: one graph launch). */
+int32_t xmg_graph_create(const xmg_env_desc* desc, const xmg_state* state, const uint8_t* actions, int64_t n,
+                         const xmg_out* out, uint32_t* gflag, void** graph_exec);
+int32_t xmg_graph_launch(void* graph_exec, void* stream);
+int32_t xmg_graph_destroy(void* graph_exec);
+
 /* Dynamic shared memory per 128-env CTA of the rollout kernel (<0: unsupported). */
 int64_t xmg_rollout_smem_bytes(const xmg_env_desc* desc);
 

@@ -34,7 +34,8 @@ EXPORTS = ("xmg_abi_version", "xmg_last_error", "xmg_philox", "xmg_split_batch",
            "xmg_key_from_seed", "xmg_fold_in", "xmg_philox_host", "xmg_reset", "xmg_validate_actions",
            "xmg_step", "xmg_step_smem_bytes", "xmg_work_words", "xmg_profile", "xmg_profile_read", "xmg_rollout",
            "xmg_rollout_smem_bytes", "xmg_sprites", "xmg_image_obs", "xmg_steps", "xmg_image_atlas_bytes",
-           "xmg_image_atlas", "xmg_image_obs_aligned", "xmg_ahead_plan", "xmg_prebuild")
+           "xmg_image_atlas", "xmg_image_obs_aligned", "xmg_ahead_plan", "xmg_prebuild",
+           "xmg_step_fused", "xmg_graph_create", "xmg_graph_launch", "xmg_graph_destroy")
 
 
 class NativeLibraryError(RuntimeError):
@@ -104,6 +105,11 @@ def _bind(L):
         "xmg_image_obs_aligned": ([vp, i64, i32, vp, vp, vp], i32),
         "xmg_ahead_plan": ([C.POINTER(EnvDesc), vp, vp], i32),
         "xmg_prebuild": ([C.POINTER(EnvDesc), C.POINTER(State), i64, i64, i64, vp], i32),
+        "xmg_step_fused": ([C.POINTER(EnvDesc), C.POINTER(State), vp, i64, C.POINTER(Out), vp, vp], i32),
+        "xmg_graph_create": ([C.POINTER(EnvDesc), C.POINTER(State), vp, i64, C.POINTER(Out), vp,
+                              C.POINTER(C.c_void_p)], i32),
+        "xmg_graph_launch": ([vp, vp], i32),
+        "xmg_graph_destroy": ([vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

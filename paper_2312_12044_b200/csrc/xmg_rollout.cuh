@@ -86,11 +86,46 @@ __device__ __noinline__ ulonglong4 roll_consume(const xmg_state s, uint32_t cm, 
   return out;
 }
 
+// gflag (xmg_step_fused, the one-kernel step for small batches and CUDA-graph
+// replay): before anything changes, every CTA checks the whole batch of
+// actions (u8, [n]) against [0, 6) (ref vecenv.py:297-301); an invalid batch
+// is skipped by all CTAs and CTA 0 tags gflag[0] with the step's number.
+// gflag[3] counts the steps (advanced by the last CTA to finish, so a
+// replayed graph needs no host-side epoch); gflag[2] is the CTA counter.
+__device__ __forceinline__ bool fused_batch_rejected(const uint8_t* actions, int64_t n, uint32_t* gflag) {
+  const uint32_t clk = *reinterpret_cast<volatile uint32_t*>(gflag + 3);
+  bool bad = false;
+  const int64_t head = (int64_t)((16 - (reinterpret_cast<uintptr_t>(actions) & 15)) & 15);
+  const int64_t h = head < n ? head : n;
+  const int64_t nvec = (n - h) >> 4;
+  const uint4* body = reinterpret_cast<const uint4*>(actions + h);
+  const uint32_t six = 0x06060606u;
+  for (int64_t i = threadIdx.x; i < nvec; i += blockDim.x) {
+    const uint4 v = body[i];
+    bad |= (__vcmpgeu4(v.x, six) | __vcmpgeu4(v.y, six) | __vcmpgeu4(v.z, six) | __vcmpgeu4(v.w, six)) != 0;
+  }
+  for (int64_t i = threadIdx.x; i < h; i += blockDim.x) bad |= actions[i] >= 6;
+  for (int64_t i = h + 16 * nvec + threadIdx.x; i < n; i += blockDim.x) bad |= actions[i] >= 6;
+  bad = __syncthreads_or(bad) != 0;
+  if (threadIdx.x == 0) {
+    if (bad && blockIdx.x == 0) atomicMax(gflag, clk + 1);
+    __threadfence();
+    if (atomicAdd(gflag + 2, 1u) == gridDim.x - 1) {  // every CTA has read the clock
+      gflag[2] = 0;
+      __threadfence();
+      gflag[3] = clk + 1;
+    }
+  }
+  return bad;
+}
+
 __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel(const xmg_env_desc d, const xmg_state s,
                                                                  const uint64_t* pkeys, const uint8_t* actions,
-                                                                 int64_t t0, int64_t T, int64_t n, const xmg_out o) {
+                                                                 int64_t t0, int64_t T, int64_t n, const xmg_out o,
+                                                                 uint32_t* gflag) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (gflag != nullptr && fused_batch_rejected(actions, n, gflag)) return;
   const int64_t chunk = (int64_t)blockIdx.x * kRollWarps + warp;
   const int64_t e0 = 32 * chunk;
   if (e0 >= n) return;  // warp-uniform

@@ -419,14 +419,14 @@ int maybe_prebuild(const xmg_env_desc* d, const xmg_state* s, uint32_t epoch, in
 }
 
 int launch_rollout(const xmg_env_desc* d, const xmg_state* s, const uint64_t* pkeys, const uint8_t* actions,
-                   int64_t t0, int64_t steps, int64_t n, const xmg_out* o, cudaStream_t st) {
+                   int64_t t0, int64_t steps, int64_t n, const xmg_out* o, cudaStream_t st, uint32_t* gflag = nullptr) {
   const RollGeo geo = make_roll_geo(d->height, d->width, d->view_size, d->rule_width);
   if (!cur_dev()) return -1;
   if (geo.total > kMaxDynSmem - 1024) return fail("grid too large for the rollout kernel's shared-memory state");
   const int64_t chunks = (n + 31) / 32;
   const int64_t blocks = (chunks + kRollWarps - 1) / kRollWarps;
   rollout_kernel<<<(unsigned)blocks, kRollWarps * 32, (size_t)geo.total, st>>>(*d, *s, pkeys, actions, t0, steps, n,
-                                                                             *o);
+                                                                             *o, gflag);
   return check_launch("rollout_kernel");
 }
 
@@ -637,6 +637,59 @@ int32_t xmg_rollout(const xmg_env_desc* desc, const xmg_state* state, const uint
       (policy_keys && (reinterpret_cast<uintptr_t>(policy_keys) & 15)))
     return fail("agent / rng / policy key buffers must be 16-byte aligned");
   return launch_rollout(desc, state, policy_keys, actions, t0, steps, n, traj, (cudaStream_t)stream);
+}
+
+int32_t xmg_step_fused(const xmg_env_desc* desc, const xmg_state* state, const uint8_t* actions, int64_t n,
+                       const xmg_out* out, uint32_t* gflag, void* stream) {
+  if (validate_desc(desc, state, n)) return -1;
+  if (!out || !actions || !gflag) return fail("null out / actions / gflag");
+  if (!out->reward || !out->discount || !out->step_type) return fail("reward / discount / step_type are required");
+  if ((reinterpret_cast<uintptr_t>(state->agent) & 15) || (reinterpret_cast<uintptr_t>(state->rng) & 15))
+    return fail("agent / rng buffers must be 16-byte aligned");
+  return launch_rollout(desc, state, nullptr, actions, 0, 1, n, out, (cudaStream_t)stream, gflag);
+}
+
+// One fused step captured into an executable CUDA graph (the pointers and
+// the description are baked in; the step number lives in gflag[3]).
+int32_t xmg_graph_create(const xmg_env_desc* desc, const xmg_state* state, const uint8_t* actions, int64_t n,
+                         const xmg_out* out, uint32_t* gflag, void** graph_exec) {
+  if (!graph_exec) return fail("null graph handle");
+  *graph_exec = nullptr;
+  if (validate_desc(desc, state, n)) return -1;
+  if (!out || !actions || !gflag) return fail("null out / actions / gflag");
+  if (!out->reward || !out->discount || !out->step_type) return fail("reward / discount / step_type are required");
+  if (!cur_dev()) return -1;  // attributes set before the capture
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return fail("cudaStreamCreate failed");
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int rc = 0;
+  if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    rc = fail("cudaStreamBeginCapture failed");
+  } else {
+    rc = launch_rollout(desc, state, nullptr, actions, 0, 1, n, out, st, gflag);
+    const cudaError_t e = cudaStreamEndCapture(st, &graph);
+    if (!rc && e != cudaSuccess) rc = fail(std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e));
+  }
+  if (!rc) {
+    const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    if (e != cudaSuccess) rc = fail(std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+  }
+  if (graph) cudaGraphDestroy(graph);
+  cudaStreamDestroy(st);
+  if (!rc) *graph_exec = exec;
+  return rc;
+}
+
+int32_t xmg_graph_launch(void* graph_exec, void* stream) {
+  if (!graph_exec) return fail("null graph handle");
+  const cudaError_t e = cudaGraphLaunch((cudaGraphExec_t)graph_exec, (cudaStream_t)stream);
+  return e == cudaSuccess ? 0 : fail(std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
+}
+
+int32_t xmg_graph_destroy(void* graph_exec) {
+  if (graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)graph_exec);
+  return 0;
 }
 
 int32_t xmg_sprites(int32_t px, uint8_t* atlas, void* stream) {

@@ -157,7 +157,7 @@ _ACT_DTYPES = {torch.uint8: _lib.ACT_U8, torch.int32: _lib.ACT_I32, torch.int64:
 class VecEnv:
     def __init__(self, params: EnvParams, num_envs: int, rulesets=None, *, device=None, task_ids=None,
                  strict: bool = False, global_offset: int = 0, reuse_outputs: bool = False,
-                 resample_tasks: bool = False, reset_ahead: bool | None = None):
+                 resample_tasks: bool = False, reset_ahead: bool | None = None, graph: bool = False):
         if num_envs < 1:
             raise ValueError(f"num_envs must be >= 1, got {num_envs}")
         self.params = params
@@ -246,7 +246,10 @@ class VecEnv:
         self.work = torch.zeros(int(_lib.lib().xmg_work_words(n)), dtype=torch.int32, device=dev)
         # reset-ahead records (include/xmg.h): each env's next trial, pre-built
         # while the current one runs, so an auto-reset is a copy
-        self.reset_ahead = reset_ahead if reset_ahead is not None else os.environ.get("XMG_AHEAD", "1") != "0"
+        # (off by default for the Empty scenario, whose trials are all the same
+        # constant build: nothing to move out of the reset)
+        default_ahead = os.environ.get("XMG_AHEAD", "1") != "0" and params.scenario != "empty"
+        self.reset_ahead = reset_ahead if reset_ahead is not None else default_ahead
         if self.reset_ahead:
             self._next_grids = torch.zeros(n * self._hw + GRID_PAD, dtype=torch.uint8, device=dev)
             self._next_state = torch.zeros((n, 4), dtype=torch.int64, device=dev)
@@ -283,6 +286,16 @@ class VecEnv:
         self._flag_ptr = self._flag.data_ptr()
         self.stats: torch.Tensor | None = None
         self.launches = 0  # kernels of ours launched by this VecEnv
+        # graph mode (small batches): step() = ONE fused kernel (xmg_step_fused,
+        # in-kernel validation, device step counter) replayed from a CUDA graph;
+        # actions are staged in a fixed buffer, the records are reused buffers
+        self.graph = graph
+        if graph:
+            self.reuse_outputs = True
+            self._gflag = torch.zeros(4, dtype=torch.int32, device=dev)
+            self._gact = torch.zeros(n + 16, dtype=torch.uint8, device=dev)[:n]
+            self._graphs: dict = {}
+            self._gchecked = 0
 
     # -- views
     @property
@@ -374,6 +387,8 @@ class VecEnv:
 
     # -- step
     def step(self, actions, compute_obs: bool = True, validate: bool = True) -> VecTimeStep:
+        if self.graph:
+            return self._step_graph(actions, compute_obs)
         n = self.num_envs
         L = _lib.lib()
         stream = _stream(self.device)
@@ -413,6 +428,73 @@ class VecEnv:
         if self.strict and flag_ptr is not None:
             self.check()
         return VecTimeStep(*outs)
+
+    # -- graph mode
+    @property
+    def action_buffer(self) -> torch.Tensor:
+        """(N,) uint8 staging buffer of graph mode: actions written here need
+        no copy (step(vec.action_buffer))."""
+        return self._gact
+
+    def _stage_actions(self, actions) -> None:
+        n = self.num_envs
+        if isinstance(actions, torch.Tensor) and actions.is_cuda:
+            if actions.shape != (n,):
+                raise InvalidAction(f"expected {n} actions, got shape {tuple(actions.shape)}")
+            if actions.data_ptr() == self._gact.data_ptr() and actions.dtype == torch.uint8:
+                return
+            if actions.dtype == torch.uint8:
+                self._gact.copy_(actions)
+            else:  # out-of-range values map to 255 so the kernel rejects the batch
+                a = actions.to(torch.int64)
+                self._gact.copy_(torch.where((a >= 0) & (a < 6), a, 255).to(torch.uint8))
+        else:
+            a = np.asarray(actions)
+            if a.shape != (n,):
+                raise InvalidAction(f"expected {n} actions, got shape {a.shape}")
+            if ((a < 0) | (a >= 6)).any():
+                raise InvalidAction("action outside [0, 5]")
+            self._gact.copy_(torch.from_numpy(a.astype(np.uint8)), non_blocking=False)
+
+    def _fused_call(self, o_ref) -> None:
+        _lib.check(_lib.lib().xmg_step_fused(self._desc_ref, self._state_ref, self._gact.data_ptr(), self.num_envs,
+                                             o_ref, self._gflag.data_ptr(), _stream(self.device)), "xmg_step_fused")
+
+    def _step_graph(self, actions, compute_obs: bool) -> VecTimeStep:
+        """step() in graph mode: the same transition (bit-identical, the fused
+        kernel at T = 1), one kernel per step replayed from a CUDA graph
+        (captured once per record layout by libxmg: xmg_graph_create)."""
+        if actions is not self._gact:
+            self._stage_actions(actions)
+        if self.reset_ahead:
+            self._roll_clock += 1
+            if self._roll_clock % self._ahead_every == 0:  # this step's reset-ahead batch (outside the graph)
+                cls = (self._roll_clock // self._ahead_every) % self._ahead_classes
+                _lib.check(_lib.lib().xmg_prebuild(self._desc_ref, self._state_ref, cls, self._ahead_classes,
+                                                   self.num_envs, _stream(self.device)), "xmg_prebuild")
+                self.launches += 1
+        key = (compute_obs, id(self.stats))
+        ent = self._graphs.get(key)
+        if ent is None:
+            outs = self._alloc_out(compute_obs)
+            o = self._out_struct(outs)
+            h = C.c_void_p()
+            _lib.check(_lib.lib().xmg_graph_create(self._desc_ref, self._state_ref, self._gact.data_ptr(),
+                                                   self.num_envs, C.byref(o), self._gflag.data_ptr(), C.byref(h)),
+                       "xmg_graph_create")
+            ent = self._graphs[key] = (h, o, VecTimeStep(*outs))
+        _lib.check(_lib.lib().xmg_graph_launch(ent[0], _stream(self.device)), "xmg_graph_launch")
+        self.launches += 1
+        if self.strict:
+            self.check()
+        return ent[2]
+
+    def __del__(self):
+        for h, _, _ in getattr(self, "_graphs", {}).values():
+            try:
+                _lib.lib().xmg_graph_destroy(h)
+            except Exception:
+                pass
 
     # -- many steps per host call
     def steps(self, actions: torch.Tensor, compute_obs: bool = True, validate: bool = True,
@@ -547,6 +629,11 @@ class VecEnv:
         if flagged > self._checked_epoch:
             self._checked_epoch = flagged
             raise InvalidAction(f"action outside [0, 5] at step {flagged}; that batch was not applied")
+        if self.graph:
+            gf = int(self._gflag[0].item()) & 0xFFFFFFFF
+            if gf > self._gchecked:
+                self._gchecked = gf
+                raise InvalidAction(f"action outside [0, 5] at graph step {gf}; that batch was not applied")
 
     # -- inspection
     def ruleset_of(self, i: int) -> Ruleset:

@@ -1,6 +1,3 @@
-python -m pytest tests/test_reset_ahead_gpu.py tests/test_rollout_gpu.py -x -q 2>&1 | tail -2
-for a in 1 0; do
-XMG_AHEAD=$a timeout 300 python tools/prof_rollout.py c3 100 32 4 1 2>&1 | tail -1
-XMG_AHEAD=$a timeout 300 python tools/prof_rollout.py c3 100 32 4 0 2>&1 | tail -1
-XMG_AHEAD=$a timeout 300 python tools/prof_rollout.py c3 490 32 2 1 2>&1 | tail -1
-done
+python tools/graph_probe.py c1 2000
+python tools/graph_probe.py c2 1000
+python tools/graph_probe.py c1 200 > /dev/null && timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -s 400 -c 30 --csv --log-file gpurun_out/c1_graph_launches.csv python tools/graph_probe.py c1 200 > /dev/null 2>&1; echo ncu=$?
