@@ -138,9 +138,11 @@ int32_t xmg_random_actions(const uint64_t* keys /*[n][2]*/, int64_t n, int64_t t
                            uint8_t* actions /*[steps][n]*/, void* stream);
 
 /* Host-side scalar helpers: ref key_from_seed rng.py:96-99 and
- * fold_in rng.py:107-110 (domain: 1 draw, 2 split, 3 fold, 4 seed). */
+ * fold_in rng.py:107-110 (domain: 1 draw, 2 split, 3 fold, 4 seed); data is
+ * the 128-bit counter value (data & 2^64-1, data >> 64 & 2^64-1), so a
+ * negative or >= 2^64 Python integer folds in exactly as in the reference. */
 void xmg_key_from_seed(uint64_t seed_lo, uint64_t seed_hi, uint64_t* out2);
-void xmg_fold_in(uint64_t hi, uint64_t lo, uint64_t data, int32_t domain, uint64_t* out2);
+void xmg_fold_in(uint64_t hi, uint64_t lo, uint64_t data_lo, uint64_t data_hi, int32_t domain, uint64_t* out2);
 void xmg_philox_host(const uint64_t ctr[4], uint64_t k0, uint64_t k1, uint64_t out[4]);
 
 /* ---- the batched environment (ref vecenv.py) ----------------------------- */
@@ -183,10 +185,11 @@ int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* a
  * next trial of the env class (epoch / every) mod `classes` (envs e with
  * e mod classes == class) whose running trial has none yet; a trial that
  * ends with its successor pre-built is reset by a copy.  xmg_ahead_plan
- * returns (every, classes) for a description (every * classes <= budget - 2,
- * so a trial that runs to the budget always meets its class);
+ * returns (every, classes) for a description and batch size (every *
+ * classes <= budget - 2, so a trial that runs to the budget always meets its
+ * class; every >= 16, larger for small batches of expensive builds);
  * xmg_prebuild runs one batch explicitly (e.g. right after xmg_reset). */
-int32_t xmg_ahead_plan(const xmg_env_desc* desc, int64_t* every, int64_t* classes);
+int32_t xmg_ahead_plan(const xmg_env_desc* desc, int64_t n, int64_t* every, int64_t* classes);
 int32_t xmg_prebuild(const xmg_env_desc* desc, const xmg_state* state, int64_t cls, int64_t classes, int64_t n,
                      void* stream);
 

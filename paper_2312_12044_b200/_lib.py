@@ -86,7 +86,7 @@ def _bind(L):
         "xmg_split_batch": ([u64, u64, i64, i64, vp, vp], i32),
         "xmg_random_actions": ([vp, i64, i64, i64, vp, vp], i32),
         "xmg_key_from_seed": ([u64, u64, vp], None),
-        "xmg_fold_in": ([u64, u64, u64, i32, vp], None),
+        "xmg_fold_in": ([u64, u64, u64, u64, i32, vp], None),
         "xmg_philox_host": ([vp, u64, u64, vp], None),
         "xmg_reset": ([C.POINTER(EnvDesc), C.POINTER(State), vp, i64, C.POINTER(Out), vp], i32),
         "xmg_validate_actions": ([vp, i32, i64, C.c_uint32, vp, vp], i32),
@@ -103,7 +103,7 @@ def _bind(L):
         "xmg_image_atlas_bytes": ([i32], i64),
         "xmg_image_atlas": ([i32, vp, vp, vp], i32),
         "xmg_image_obs_aligned": ([vp, i64, i32, vp, vp, vp], i32),
-        "xmg_ahead_plan": ([C.POINTER(EnvDesc), vp, vp], i32),
+        "xmg_ahead_plan": ([C.POINTER(EnvDesc), i64, vp, vp], i32),
         "xmg_prebuild": ([C.POINTER(EnvDesc), C.POINTER(State), i64, i64, i64, vp], i32),
         "xmg_step_fused": ([C.POINTER(EnvDesc), C.POINTER(State), vp, i64, C.POINTER(Out), vp, vp], i32),
         "xmg_graph_create": ([C.POINTER(EnvDesc), C.POINTER(State), vp, i64, C.POINTER(Out), vp,

@@ -163,7 +163,7 @@ def key_from_seed(seed: int) -> Key:
 
 def fold_in(key: Key, data: int, _domain: int = DOMAIN_FOLD) -> Key:
     out = (C.c_uint64 * 2)()
-    _lib.lib().xmg_fold_in(key[0], key[1], data & _MASK64, _domain, out)
+    _lib.lib().xmg_fold_in(key[0], key[1], data & _MASK64, (data >> 64) & _MASK64, _domain, out)
     return Key(int(out[0]), int(out[1]))
 
 

@@ -355,6 +355,7 @@ bool use_full(const xmg_env_desc* d) {
 
 int dispatch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
                   const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st, bool pdl = true) {
+
   if (use_full(d)) {
     const int fc = full_chunks(d->height * d->width);
     if (fc <= 6) return launch_main<6, true>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
@@ -373,35 +374,45 @@ int dispatch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, c
 // Reset-ahead batches (xmg_main.cuh): every `every`-th epoch, the class
 // (epoch / every) mod B of envs gets its next trial pre-built, B = the number
 // of classes whose cycle fits in budget - 2 steps (so every trial that runs
-// to the budget meets its class once).  XMG_AHEAD_EVERY overrides `every`.
+// to the budget meets its class once).  `every` is the smallest power of two
+// >= 16 that gives a batch about four builds per resident warp (a build is
+// latency-bound: small batches pay a whole build chain for a few envs; C4's
+// 25x25 builds take ~25 us each), capped by budget - 2.  XMG_AHEAD_EVERY
+// overrides it.
 struct AheadPlan {
   int64_t every, classes;
 };
-AheadPlan ahead_plan(const xmg_env_desc* d) {
+AheadPlan ahead_plan(const xmg_env_desc* d, int64_t n, int sms) {
   static int every_env = -1;
   if (every_env < 0) {
     const char* v = getenv("XMG_AHEAD_EVERY");
-    every_env = v ? std::max(1, atoi(v)) : 16;
+    every_env = v ? std::max(1, atoi(v)) : 0;
   }
   const int64_t span = std::max<int64_t>(1, (int64_t)d->budget - 2);
-  const int64_t every = std::min<int64_t>(every_env, span);
+  int64_t every = every_env;
+  if (every <= 0) {
+    const int64_t target = 4LL * 24 * std::max(sms, 1);  // builds per batch: ~4 per resident warp
+    every = 16;
+    while (every < span && n * every < target * span) every *= 2;
+  }
+  every = std::min<int64_t>(every, span);
   return {every, std::max<int64_t>(1, span / every)};
 }
 
 int launch_prebuild(const xmg_env_desc* d, const xmg_state* s, int64_t cls, int64_t classes, int64_t n,
                     cudaStream_t st) {
-  const int64_t smem = (int64_t)kRareWarps * pre_warp_bytes(d->height, d->width);
+  const int64_t smem = (int64_t)kPreWarps * pre_warp_bytes(d->height, d->width);
   const DevInfo* di = cur_dev();
   if (!di) return -1;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prebuild_kernel, kRareWarps * 32, (size_t)smem) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prebuild_kernel, kPreWarps * 32, (size_t)smem) !=
           cudaSuccess ||
       per_sm < 1)
     return fail("prebuild_kernel does not fit on an SM");
   const int64_t count = (n - cls + classes - 1) / classes;
-  const int64_t need = (count + (int64_t)kRareWarps * kPreGroup - 1) / ((int64_t)kRareWarps * kPreGroup);
+  const int64_t need = (count + (int64_t)kPreWarps * kPreGroup - 1) / ((int64_t)kPreWarps * kPreGroup);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * di->sms, need));
-  prebuild_kernel<<<(unsigned)blocks, kRareWarps * 32, (size_t)smem, st>>>(*d, *s, cls, classes, n,
+  prebuild_kernel<<<(unsigned)blocks, kPreWarps * 32, (size_t)smem, st>>>(*d, *s, cls, classes, n,
                                                                           s->work + prebuild_ctr_base(n));
   return check_launch("prebuild_kernel");
 }
@@ -411,7 +422,9 @@ int launch_prebuild(const xmg_env_desc* d, const xmg_state* s, int64_t cls, int6
 // overlap with it), 0 when not, <0 on error.
 int maybe_prebuild(const xmg_env_desc* d, const xmg_state* s, uint32_t epoch, int64_t n, cudaStream_t st) {
   if (s->next_grids == nullptr) return 0;
-  const AheadPlan p = ahead_plan(d);
+  const DevInfo* di = cur_dev();
+  if (!di) return -1;
+  const AheadPlan p = ahead_plan(d, n, di->sms);
   if (epoch % (uint64_t)p.every != 0) return 0;
   const int64_t cls = (int64_t)((epoch / (uint64_t)p.every) % (uint64_t)p.classes);
   if (cls >= n) return 0;
@@ -451,8 +464,8 @@ void xmg_key_from_seed(uint64_t seed_lo, uint64_t seed_hi, uint64_t* out2) {
   out2[1] = w[1];
 }
 
-void xmg_fold_in(uint64_t hi, uint64_t lo, uint64_t data, int32_t domain, uint64_t* out2) {
-  const uint64_t ctr[4] = {data, 0, (uint64_t)domain, 0};
+void xmg_fold_in(uint64_t hi, uint64_t lo, uint64_t data_lo, uint64_t data_hi, int32_t domain, uint64_t* out2) {
+  const uint64_t ctr[4] = {data_lo, data_hi, (uint64_t)domain, 0};
   uint64_t w[4];
   philox_host(ctr, hi, lo, w);
   out2[0] = w[0];
@@ -617,9 +630,11 @@ int32_t xmg_prebuild(const xmg_env_desc* desc, const xmg_state* state, int64_t c
   return launch_prebuild(desc, state, cls, classes, n, (cudaStream_t)stream);
 }
 
-int32_t xmg_ahead_plan(const xmg_env_desc* desc, int64_t* every, int64_t* classes) {
+int32_t xmg_ahead_plan(const xmg_env_desc* desc, int64_t n, int64_t* every, int64_t* classes) {
   if (!desc) return fail("null env description");
-  const AheadPlan p = ahead_plan(desc);
+  const DevInfo* di = cur_dev();
+  if (!di) return -1;
+  const AheadPlan p = ahead_plan(desc, n, di->sms);
   if (every) *every = p.every;
   if (classes) *classes = p.classes;
   return 0;

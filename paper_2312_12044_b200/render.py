@@ -22,7 +22,7 @@ import threading
 import torch
 
 from . import _lib
-from .vecenv import _device, _stream
+from .vecenv import _device, _device_ctx, _stream
 
 IMAGE_SIDE = 224
 
@@ -44,7 +44,8 @@ def sprite_atlas(px: int, device=None) -> torch.Tensor:
             # unaligned offsets (up to 4 bytes before / 8 after a sprite row)
             flat = torch.zeros(210 * px * px * 3 + 32, dtype=torch.uint8, device=dev)
             atlas = flat[16: 16 + 210 * px * px * 3].view(15, 14, px, px, 3)
-            _lib.check(_lib.lib().xmg_sprites(px, atlas.data_ptr(), _stream(dev)), "xmg_sprites")
+            with _device_ctx(dev):
+                _lib.check(_lib.lib().xmg_sprites(px, atlas.data_ptr(), _stream(dev)), "xmg_sprites")
             _ATLAS[key] = atlas
     return atlas
 
@@ -65,7 +66,9 @@ def aligned_atlas(view: int, device=None) -> torch.Tensor | None:
     if al is None:
         base = sprite_atlas(IMAGE_SIDE // view, dev)
         al = torch.empty(size, dtype=torch.uint8, device=dev)
-        _lib.check(_lib.lib().xmg_image_atlas(view, base.data_ptr(), al.data_ptr(), _stream(dev)), "xmg_image_atlas")
+        with _device_ctx(dev):
+            _lib.check(_lib.lib().xmg_image_atlas(view, base.data_ptr(), al.data_ptr(), _stream(dev)),
+                       "xmg_image_atlas")
         with _atlas_lock:
             _ALIGNED[key] = al
     return al
@@ -81,6 +84,13 @@ def sprite(tile: int, color: int, px: int, device=None) -> torch.Tensor:
 def image_observations(obs: torch.Tensor, out: torch.Tensor | None = None, check: bool = True) -> torch.Tensor:
     """(N, 224, 224, 3) uint8 images of (N, v, v, 2) observations on the GPU,
     each equal to ref render.py:225-243 image_observation(obs[i])."""
+    if obs.is_cuda:
+        with _device_ctx(obs.device):
+            return _image_observations(obs, out, check)
+    return _image_observations(obs, out, check)
+
+
+def _image_observations(obs: torch.Tensor, out: torch.Tensor | None, check: bool) -> torch.Tensor:
     if obs.dim() != 4 or obs.shape[1] != obs.shape[2] or obs.shape[3] != 2:
         raise ValueError(f"expected square (N, v, v, 2) observations, got shape {tuple(obs.shape)}")
     if not obs.is_cuda:

@@ -22,6 +22,7 @@ There is no CPU fallback: without libxmg.so or a GPU every call raises.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import os
 from dataclasses import dataclass
 from typing import Sequence
@@ -42,6 +43,24 @@ STAGE_BITS = 3 << 18  # reset-ahead stage in state word 0 (include/xmg.h)
 
 def _stream(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
+
+
+def _on_device(fn):
+    """Run a method with its VecEnv's GPU current: libxmg launches on the
+    current device (kernels, attributes and the stream all belong to it), so a
+    VecEnv on cuda:1 must not launch while cuda:0 is current."""
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kwargs):
+        if torch.cuda.current_device() == self._dev_index:
+            return fn(self, *args, **kwargs)
+        with torch.cuda.device(self._dev_index):
+            return fn(self, *args, **kwargs)
+    return wrapper
+
+
+def _device_ctx(dev: torch.device):
+    """Context making `dev` current (a no-op when it already is)."""
+    return torch.cuda.device(dev.index if dev.index is not None else torch.cuda.current_device())
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -69,8 +88,9 @@ def split_batch(key: Key, num: int, offset: int = 0, device=None) -> torch.Tenso
     fold_in(key, offset + i, SPLIT): ref split_batch rng.py:142-145."""
     dev = _device(device)
     out = torch.empty((num, 2), dtype=torch.int64, device=dev)
-    _lib.check(_lib.lib().xmg_split_batch(key[0], key[1], offset, num, out.data_ptr(), _stream(dev)),
-               "xmg_split_batch")
+    with _device_ctx(dev):
+        _lib.check(_lib.lib().xmg_split_batch(key[0], key[1], offset, num, out.data_ptr(), _stream(dev)),
+                   "xmg_split_batch")
     return out
 
 
@@ -90,8 +110,9 @@ def policy_keys(key: Key, num: int, offset: int = 0, device=None) -> torch.Tenso
     ctr_t = torch.from_numpy(ctr.view(np.int64)).to(dev)
     key_t = torch.from_numpy(kk.view(np.int64)).to(dev)
     out = torch.empty((num, 4), dtype=torch.int64, device=dev)
-    _lib.check(_lib.lib().xmg_philox(ctr_t.data_ptr(), key_t.data_ptr(), out.data_ptr(), num, _stream(dev)),
-               "xmg_philox")
+    with _device_ctx(dev):
+        _lib.check(_lib.lib().xmg_philox(ctr_t.data_ptr(), key_t.data_ptr(), out.data_ptr(), num, _stream(dev)),
+                   "xmg_philox")
     return out[:, :2].contiguous()
 
 
@@ -100,8 +121,9 @@ def random_actions(keys: torch.Tensor, t0: int, steps: int) -> torch.Tensor:
     random policy of ref harness.py:269-275 evaluated on the GPU."""
     n = keys.shape[0]
     out = torch.empty((steps, n), dtype=torch.uint8, device=keys.device)
-    _lib.check(_lib.lib().xmg_random_actions(keys.data_ptr(), n, t0, steps, out.data_ptr(), _stream(keys.device)),
-               "xmg_random_actions")
+    with _device_ctx(keys.device):
+        _lib.check(_lib.lib().xmg_random_actions(keys.data_ptr(), n, t0, steps, out.data_ptr(),
+                                                 _stream(keys.device)), "xmg_random_actions")
     return out
 
 
@@ -109,8 +131,9 @@ def philox(ctr: torch.Tensor, key: torch.Tensor) -> torch.Tensor:
     """Batched Philox4x64-10 blocks on the device (KAT hook)."""
     n = ctr.shape[0]
     out = torch.empty((n, 4), dtype=torch.int64, device=ctr.device)
-    _lib.check(_lib.lib().xmg_philox(ctr.data_ptr(), key.data_ptr(), out.data_ptr(), n, _stream(ctr.device)),
-               "xmg_philox")
+    with _device_ctx(ctr.device):
+        _lib.check(_lib.lib().xmg_philox(ctr.data_ptr(), key.data_ptr(), out.data_ptr(), n, _stream(ctr.device)),
+                   "xmg_philox")
     return out
 
 
@@ -163,6 +186,7 @@ class VecEnv:
         self.params = params
         self.num_envs = n = num_envs
         self.device = dev = _device(device)
+        self._dev_index = dev.index if dev.index is not None else torch.cuda.current_device()
         self.strict = strict
         self.global_offset = global_offset
         self.reuse_outputs = reuse_outputs
@@ -278,7 +302,9 @@ class VecEnv:
         # schedules by epoch inside libxmg, rollout() by its own step clock
         if self.reset_ahead:
             ev, cl = C.c_int64(), C.c_int64()
-            _lib.check(_lib.lib().xmg_ahead_plan(C.byref(self._desc), C.byref(ev), C.byref(cl)), "xmg_ahead_plan")
+            with torch.cuda.device(self._dev_index):
+                _lib.check(_lib.lib().xmg_ahead_plan(C.byref(self._desc), n, C.byref(ev), C.byref(cl)),
+                           "xmg_ahead_plan")
             self._ahead_every, self._ahead_classes = int(ev.value), int(cl.value)
         self._roll_clock = 0
         self._desc_ref = C.byref(self._desc)
@@ -359,11 +385,13 @@ class VecEnv:
         return self.enable_stats().sum(dim=0)
 
     # -- reset
+    @_on_device
     def reset(self, key: Key, compute_obs: bool = True) -> VecTimeStep:
         keys = split_batch(key, self.num_envs, self.global_offset, self.device)
         self.launches += 1
         return self._reset_keys(keys, compute_obs)
 
+    @_on_device
     def reset_with_keys(self, k0, k1, compute_obs: bool = True) -> VecTimeStep:
         if isinstance(k0, torch.Tensor):
             keys = torch.stack([k0.to(self.device, torch.int64), k1.to(self.device, torch.int64)], dim=1)
@@ -386,6 +414,7 @@ class VecEnv:
         return VecTimeStep(*outs)
 
     # -- step
+    @_on_device
     def step(self, actions, compute_obs: bool = True, validate: bool = True) -> VecTimeStep:
         if self.graph:
             return self._step_graph(actions, compute_obs)
@@ -497,6 +526,7 @@ class VecEnv:
                 pass
 
     # -- many steps per host call
+    @_on_device
     def steps(self, actions: torch.Tensor, compute_obs: bool = True, validate: bool = True,
               out: Trajectory | None = None, fused: bool | None = None) -> Trajectory:
         """``actions.shape[0]`` consecutive ``step`` calls issued by one library
@@ -557,6 +587,7 @@ class VecEnv:
         return 4 * min(4, (228 * 1024) // (smem + 1024)) if smem > 0 else 0
 
     # -- fused rollout
+    @_on_device
     def rollout(self, steps: int, policy_keys: torch.Tensor | None = None, actions: torch.Tensor | None = None,
                 t0: int = 0, record: Sequence[str] = ("observations", "rewards", "discounts", "step_types"),
                 out: Trajectory | None = None) -> Trajectory:

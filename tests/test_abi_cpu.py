@@ -66,3 +66,18 @@ def test_vecenv_refuses_cpu_device():
     from paper_2312_12044_b200 import EnvParams, NativeLibraryError, VecEnv
     with pytest.raises(NativeLibraryError):
         VecEnv(EnvParams(), 4, device="cpu")
+
+
+def test_fold_in_takes_the_full_128_bit_counter():
+    """ref rng.py:107-110 folds in (data & 2^64-1, data >> 64 & 2^64-1):
+    negative and >= 2^64 data must match the reference (values from
+    rulegrid.rng.fold_in(key_from_seed(7), data), computed with the
+    reference in the build container)."""
+    k = key_from_seed(7)
+    assert tuple(k) == (5153160078105390988, 9456252307694779705)
+    want = {-1: (7204942696657869296, 9289732693193205544),
+            2 ** 64 + 5: (12675942302801154926, 15253322680772628831),
+            2 ** 70 - 3: (14688658413190397962, 14771808042739616059),
+            12345: (3444096608153625987, 1418527488995923867)}
+    for data, key in want.items():
+        assert tuple(fold_in(k, data)) == key, data

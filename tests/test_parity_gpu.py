@@ -295,3 +295,28 @@ def test_view_sizes_and_layouts_vs_oracle(env_name, config, v, see):
         np.testing.assert_array_equal(ts.step_types.cpu().numpy(), s)
     np.testing.assert_array_equal(vec.grids.cpu().numpy(), ora.grids)
     vec.check()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_vecenv_on_a_non_current_device():
+    """A VecEnv on cuda:1 while cuda:0 is current launches on its own GPU
+    (libxmg uses the current device; VecEnv makes its device current per call)
+    and equals the same batch on cuda:0, including the >48 KB rollout kernel
+    whose attributes are set per device."""
+    from paper_2312_12044_b200 import VecEnv, key_from_seed, load_benchmark, make, policy_keys, random_actions
+    _, params = make("XLand-MiniGrid-R4-13x13")
+    bm = load_benchmark(benchmark_file("medium"))
+    torch.cuda.set_device(0)
+    a = VecEnv(params, 1024, bm, device="cuda:0")
+    b = VecEnv(params, 1024, bm, device="cuda:1")
+    a.reset(key_from_seed(1))
+    b.reset(key_from_seed(1))
+    acts = random_actions(policy_keys(key_from_seed(2), 1024, device="cuda:0"), 0, 40)
+    for t in range(20):
+        ta, tb = a.step(acts[t]), b.step(acts[t].to("cuda:1"))
+        assert torch.equal(ta.observations.cpu(), tb.observations.cpu())
+    ra = a.rollout(20, actions=acts[20:40])
+    rb = b.rollout(20, actions=acts[20:40].to("cuda:1"))
+    assert torch.equal(ra.observations.cpu(), rb.observations.cpu())
+    assert torch.equal(a.grids.cpu(), b.grids.cpu()) and torch.equal(a.state_words().cpu(), b.state_words().cpu())
+    assert torch.cuda.current_device() == 0

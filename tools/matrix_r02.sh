@@ -1,3 +1,2 @@
-python tools/graph_probe.py c1 2000
-python tools/graph_probe.py c2 1000
-python tools/graph_probe.py c1 200 > /dev/null && timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -s 400 -c 30 --csv --log-file gpurun_out/c1_graph_launches.csv python tools/graph_probe.py c1 200 > /dev/null 2>&1; echo ncu=$?
+for L in build_variants/*.so; do XMG_LIB=$L timeout 300 python tools/time_prebuild.py c3 2>&1 | tail -1; done
+for L in build_variants/p1g4.so build_variants/p4g4.so; do XMG_LIB=$L timeout 300 python tools/time_prebuild.py c4 2>&1 | tail -1; XMG_LIB=$L timeout 300 python tools/time_prebuild.py doorkey 2>&1 | tail -1; done

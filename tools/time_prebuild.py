@@ -18,7 +18,7 @@ wl = sys.argv[1] if len(sys.argv) > 1 else "c3"
 dev = torch.device("cuda", 0)
 params, bm, vec = bench.make_workload(wl, dev, bench.WORKLOADS[wl][2], 0)
 every, classes = C.c_int64(), C.c_int64()
-_lib.lib().xmg_ahead_plan(C.byref(vec._desc), C.byref(every), C.byref(classes))
+_lib.lib().xmg_ahead_plan(C.byref(vec._desc), vec.num_envs, C.byref(every), C.byref(classes))
 B = int(sys.argv[2]) if len(sys.argv) > 2 else classes.value
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
 vec.reset(key_from_seed(0))
