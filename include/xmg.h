@@ -50,7 +50,7 @@ extern "C" {
 
 #define XMG_ABI_VERSION 2
 
-/* scenario ids: ref scenarios.py:415-423 (SCENARIOS) */
+/* scenario ids: ref scenarios.py:177-185 (SCENARIOS) */
 enum {
     XMG_SCENARIO_XLAND = 0,
     XMG_SCENARIO_EMPTY = 1,
@@ -65,13 +65,13 @@ enum {
 enum { XMG_ACT_U8 = 0, XMG_ACT_I32 = 1, XMG_ACT_I64 = 2 };
 
 /* Static environment description: ref EnvParams (env.py:50-73) plus the
- * layout plan (layouts.py:474-529) and the task table, all pre-resolved on
+ * layout plan (layouts.py:51-106) and the task table, all pre-resolved on
  * the host.  Pointers are device pointers. */
 typedef struct xmg_env_desc {
     int32_t height, width, view_size, budget;
     int32_t scenario;            /* XMG_SCENARIO_* */
     int32_t see_through_walls;   /* 0: exact-integer line of sight, observation.py:46-87 */
-    int32_t num_segments;        /* door segments, layouts.py:509-520 */
+    int32_t num_segments;        /* door segments, layouts.py:86-97 */
     int32_t fixed_doors;         /* R6: doors at segment midpoints */
     int32_t rule_width;          /* R (max active rules over the table) */
     int32_t obj_width;           /* O (max active objects over the table) */
@@ -113,7 +113,7 @@ typedef struct xmg_out {
     int8_t* step_type;  /* [n]  FIRST 0 / MID 1 / LAST 2 */
     /* nullable episode statistics, one slot per 128-env CTA (no atomics
      * contention): stats[3*cta + 0] += sum of rewards, [+1] += finished
-     * trials, [+2] += their lengths (ref RolloutStats, harness.py:314-354) */
+     * trials, [+2] += their lengths (ref RolloutStats, harness.py:103-143) */
     double* stats;
 } xmg_out;
 
@@ -133,7 +133,7 @@ int32_t xmg_split_batch(uint64_t root_hi, uint64_t root_lo, int64_t offset, int6
                         void* stream);
 
 /* Random policy: actions[t][i] = word (t0+t) of keys[i]'s draw stream mod 6,
- * ref harness.py:269-275 (random_policy) with per-env keys. */
+ * ref harness.py:58-64 (random_policy) with per-env keys. */
 int32_t xmg_random_actions(const uint64_t* keys /*[n][2]*/, int64_t n, int64_t t0, int64_t steps,
                            uint8_t* actions /*[steps][n]*/, void* stream);
 

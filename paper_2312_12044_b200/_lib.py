@@ -25,7 +25,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 ABI_VERSION = 2
 
-# scenario ids of include/xmg.h (ref scenarios.py:415-423)
+# scenario ids of include/xmg.h (ref scenarios.py:177-185)
 SCENARIO_IDS = {"xland": 0, "empty": 1, "empty_random": 2, "door_key": 3, "four_rooms": 4,
                 "unlock": 5, "unlock_pickup": 6}
 ACT_U8, ACT_I32, ACT_I64 = 0, 1, 2

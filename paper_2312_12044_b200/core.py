@@ -3,7 +3,7 @@
 Mirrors the public vocabulary of the reference's primitives so code written
 against ``rulegrid`` reads the same here:
   * tile / color ids and codes          ref core.py:17-70
-  * Direction, Position, AgentState, Grid ref core.py:256-325
+  * Direction, Position, AgentState, Grid ref core.py:106-175
   * exception types                      ref errors.py:4-45
   * Key + key derivation                 ref rng.py:35-145
 Key derivation calls the scalar host helpers of libxmg.so (xmg_key_from_seed,

@@ -72,7 +72,7 @@ __device__ __forceinline__ uint32_t mod64_small(uint64_t x, uint32_t d) {
 }
 
 // Row-major floor cells of the scratch grid into fc[]; returns their count
-// (the free list of ref:core.py:322-325, built with ballots).
+// (the free list of ref:core.py:172-175, built with ballots).
 __device__ int build_free_list(const WarpScratch& ws, int HW, int lane) {
   int count = 0;
   for (int base = 0; base < HW; base += 32) {
@@ -119,7 +119,7 @@ __device__ __forceinline__ bool col_ok(int mode, int cell, int W, int x) {
   return mode == 1 ? c < x : c > x;
 }
 
-// Warp radix-select over the draw words (ref:core.py:328-333,
+// Warp radix-select over the draw words (ref:core.py:178-183,
 // ref:vecenv.py:261-265: cells ordered by (word, index), a stable argsort).
 // Element f (free-cell index) is owned by lane (f >> 2) & 31, bit
 // 4 * (f >> 7) + (f & 3) of that lane's masks (the lane that drew its
@@ -234,7 +234,7 @@ __device__ __forceinline__ int select_rank(const uint64_t* wd, int lane, int F, 
 
 // Places `nobj` objects on the (filtered) free cells of ranks 0..nobj-1 and
 // records in misc[32] the cell of rank spawn_base + spawn_word % (count -
-// spawn_base) (ref:scenarios.py:281-288), via warp_select: the element of
+// spawn_base) (ref:scenarios.py:43-50), via warp_select: the element of
 // rank nobj - 1 bounds the object cells, which are then ordered exactly
 // among themselves.
 __device__ void rank_place(const WarpScratch& ws, int lane, int F, int W, int mode, int x, int obj_lane,
@@ -297,7 +297,7 @@ __device__ void rank_place(const WarpScratch& ws, int lane, int F, int W, int mo
 
 // Every key a trial reset consumes, derived from the episode key ek:
 // ref:vecenv.py:224-227 (ks = split(ek, 0), next state key st = split(ek, 1))
-// and ref:scenarios.py:293,344,363,376 (k0, k1, k2 = split(ks, 3)); see
+// and ref:scenarios.py:55,106,125,138 (k0, k1, k2 = split(ks, 3)); see
 // warp_trial_keys.
 struct TrialKeys {
   uint64_t st_hi, st_lo, k0h, k0l, k1h, k1l, k2h, k2l, task_word;
@@ -378,7 +378,7 @@ __device__ __noinline__ void derive_keys_group(uint32_t m, int base, uint64_t ek
   __syncwarp();
 }
 
-// Rebuild one env's trial with the scenario builders ref:scenarios.py:291-412
+// Rebuild one env's trial with the scenario builders ref:scenarios.py:53-174
 // (batched: ref:vecenv.py:242-291).  Called by all 32 lanes with the same
 // arguments; writes the new grid to `gdst` (and leaves it in ws.grid) and
 // returns the new pose / goal / task on every lane.
@@ -403,7 +403,7 @@ __device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
   const uint32_t* row = d.task_rows + (int64_t)res.task * d.row_words;
   // the objects this trial places, one per lane, read now so the load is in
   // flight during the draws (ref:vecenv.py:261-270; FourRooms: the goal,
-  // ref:scenarios.py:361-370; EmptyRandom: none)
+  // ref:scenarios.py:123-132; EmptyRandom: none)
   int nobj = 0, obj_lane = 0;
   if (sc == XMG_SCENARIO_XLAND) {
     nobj = (int)((row[1] >> 8) & 0xff);
@@ -416,7 +416,7 @@ __device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
   // scratch grid are 16-byte aligned and padded)
   for (int i = lane; i < (HW + 15) >> 4; i += 32)
     reinterpret_cast<uint4*>(ws.grid)[i] = __ldg(reinterpret_cast<const uint4*>(d.base_cells) + i);
-  if (sc == XMG_SCENARIO_EMPTY) {  // ref:scenarios.py:320-327
+  if (sc == XMG_SCENARIO_EMPTY) {  // ref:scenarios.py:82-89
     __syncwarp();
     warp_store_grid(gdst, ws.grid, HW, lane);
     res.r = 1; res.c = 1; res.d = 1;
@@ -429,7 +429,7 @@ __device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
 
   int wall_col = -1, color = 0;
   const bool two_rooms = sc == XMG_SCENARIO_DOOR_KEY || sc == XMG_SCENARIO_UNLOCK || sc == XMG_SCENARIO_UNLOCK_PICKUP;
-  if (two_rooms) {  // ref:scenarios.py:341-353, 373-385
+  if (two_rooms) {  // ref:scenarios.py:103-115, 135-147
     Words4 w = {0, 0, 0, 0};
     if (lane == 0) w = philox<2>(0, 0, kDomDraw, 0, k0h, k0l);
     const uint64_t w0 = shfl64(w.w0, 0), w1 = shfl64(w.w1, 0);
@@ -455,7 +455,7 @@ __device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
   const int nseg = (sc == XMG_SCENARIO_XLAND || sc == XMG_SCENARIO_FOUR_ROOMS) ? d.num_segments : 0;
   draw_all(ws, lane, F, k1h, k1l, nseg, k0h, k0l, k2h, k2l);
   XMG_TRB(3);
-  // doors: ref:layouts.py:532-544 (segments never hold free cells)
+  // doors: ref:layouts.py:109-121 (segments never hold free cells)
   if (lane < nseg) {
     const int off = d.seg_off[lane], len = d.seg_off[lane + 1] - off;
     const int pos = d.fixed_doors ? len / 2 : (int)mod64_small(ws.misc[2 * lane], (uint32_t)len);
@@ -464,15 +464,15 @@ __device__ __noinline__ void warp_build(const xmg_env_desc* dp, uint8_t* wbase, 
   const uint64_t a0 = ws.misc[24], a1 = ws.misc[25];
   res.d = (int)(a1 & 3);  // a1 % 4
   if (sc == XMG_SCENARIO_XLAND || sc == XMG_SCENARIO_FOUR_ROOMS || sc == XMG_SCENARIO_EMPTY_RANDOM) {
-    if (sc != XMG_SCENARIO_XLAND) res.goal = 2u | ((uint32_t)kGreenGoal << 8);  // ref:scenarios.py:330-370
+    if (sc != XMG_SCENARIO_XLAND) res.goal = 2u | ((uint32_t)kGreenGoal << 8);  // ref:scenarios.py:92-132
     rank_place(ws, lane, F, W, 0, 0, obj_lane, nobj, nobj, a0);
   } else {  // two-room ports: shuffle all free cells, keep the left room
     rank_place(ws, lane, F, W, 1, wall_col, kKey * 16 + color, 1, 1, a0);
     if (sc == XMG_SCENARIO_DOOR_KEY) {
       res.goal = 2u | ((uint32_t)kGreenGoal << 8);
-    } else if (sc == XMG_SCENARIO_UNLOCK) {  // ref:scenarios.py:393-397
+    } else if (sc == XMG_SCENARIO_UNLOCK) {  // ref:scenarios.py:155-159
       res.goal = 2u | ((uint32_t)(kOpen * 16 + color) << 8);
-    } else {  // UNLOCK_PICKUP, ref:scenarios.py:400-412: reshuffle with the key placed
+    } else {  // UNLOCK_PICKUP, ref:scenarios.py:162-174: reshuffle with the key placed
       const int ball = kBall * 16 + cGenColors[ws.wd[2] % 10];
       const int F2 = build_free_list(ws, HW, lane);  // draw words for indices < F2 are unchanged
       uint64_t bw = ~0ull;

@@ -66,11 +66,11 @@ __constant__ uint8_t cGenColors[10] = {3, 4, 5, 6, 7, 8, 10, 11, 12, 13};
 constexpr uint32_t kWalkable = (1u << kFloor) | (1u << kGoal) | (1u << kOpen);
 constexpr uint32_t kPickable = (1u << 5) | (1u << 6) | (1u << 7) | (1u << 9) | (1u << 13) | (1u << 14);
 constexpr uint32_t kOpaque = (1u << kWall) | (1u << kClosed) | (1u << kLocked);
-// trigger gates as event bitmasks (ref:rules.py:60-72, ref:goals.py:268-283)
+// trigger gates as event bitmasks (ref:rules.py:60-72, ref:goals.py:51-66)
 __constant__ uint8_t cRuleGate[12] = {0, 0x2, 0x7, 0x4, 0x4, 0x4, 0x4, 0x4, 0x7, 0x7, 0x7, 0x7};
 __constant__ uint8_t cGoalGate[15] = {0, 0x2, 0x7, 0x7, 0x4, 0x7, 0x4, 0x4, 0x4, 0x4, 0x4, 0x7, 0x7, 0x7, 0x7};
 
-// direction deltas (ref:core.py:272)
+// direction deltas (ref:core.py:122)
 __device__ __forceinline__ int dir_dr(int d) { return d == 0 ? -1 : (d == 2 ? 1 : 0); }
 __device__ __forceinline__ int dir_dc(int d) { return d == 1 ? 1 : (d == 3 ? -1 : 0); }
 // NEAR_OFFSETS = up, left, right, down (ref:rules.py:76)
@@ -226,7 +226,7 @@ __device__ __forceinline__ void stage_issue(View& vw, int lo, int hi, int HW, co
 // AGENT_NEAR, AGENT_NEAR_{UP,RIGHT,DOWN,LEFT}) and agent-relative goals, so
 // they are resolved per lane from the staged window.  Every grid-wide
 // predicate (TILE_NEAR* rules, TILE_* goals) is gated on PUT_DOWN only
-// (ref:rules.py:60-72, ref:goals.py:268-283): PUT_DOWN events are queued and
+// (ref:rules.py:60-72, ref:goals.py:51-66): PUT_DOWN events are queued and
 // resolved by step_rare (warp_put_env).
 // The agent's four neighbour cells in NEAR_OFFSETS order (up, left, right,
 // down; ref:rules.py:76), 0x100 when off the grid, plus their flat indices.
@@ -269,7 +269,7 @@ __device__ __forceinline__ Nbrs load_nbrs(const VW& vw, int H, int W, int ar, in
 }
 
 // NEAR_OFFSETS slot of the directional offsets up, right, down, left
-// (ref:rules.py:80-89, ref:goals.py:287-296)
+// (ref:rules.py:80-89, ref:goals.py:70-79)
 __device__ __forceinline__ int dir_slot(int d) { return d == 0 ? 0 : d == 1 ? 2 : d == 2 ? 3 : 1; }
 
 // Rules gated on MOVE / PICK_UP (only the slots in `slots`, stored order).
@@ -300,7 +300,7 @@ __device__ XMG_RARE int agent_rules(VW vw, Nbrs& nb, const uint32_t* rules, uint
   return pocket;
 }
 
-// Agent-relative goals (ref:goals.py:361-378); the TILE_* kinds never pass the
+// Agent-relative goals (ref:goals.py:144-161); the TILE_* kinds never pass the
 // gate of a MOVE / PICK_UP event.
 __device__ __forceinline__ bool agent_goal(const Nbrs& nb, int own, uint32_t goal, int ev, int ar, int ac,
                                            int pocket) {

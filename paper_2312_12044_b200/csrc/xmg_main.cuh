@@ -138,7 +138,7 @@ __device__ __forceinline__ float goal_reward(uint32_t sc, int budget) {
   return __double2float_rn(__dsub_rn(1.0, __dmul_rn(0.9, frac)));
 }
 
-// Per-CTA episode statistics slot (ref RolloutStats, harness.py:314-354).
+// Per-CTA episode statistics slot (ref RolloutStats, harness.py:103-143).
 __device__ __forceinline__ void warp_stats(double* stats, int slot, double rs, double trl, double ln) {
 #pragma unroll
   for (int off = 16; off; off >>= 1) {

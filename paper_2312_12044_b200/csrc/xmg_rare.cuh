@@ -107,7 +107,7 @@ __device__ __forceinline__ int warp_tile_find(const uint8_t* G, const uint32_t* 
   return -1;
 }
 
-// The PUT_DOWN rule pass then the goal (ref:goals.py:347-394) of one env,
+// The PUT_DOWN rule pass then the goal (ref:goals.py:130-177) of one env,
 // whole warp; rewritten cells go to G and through to `genv` in global
 // memory.  Returns goal | dirty << 1 on every lane.
 __device__ __noinline__ int warp_put_env(uint8_t* G, uint8_t* genv, uint32_t* cand, int lane, int H, int W, int ar,

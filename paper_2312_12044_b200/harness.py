@@ -29,9 +29,9 @@ from .env import EnvParams, make
 from .ruleset import Ruleset
 from .vecenv import VecEnv, policy_keys, random_actions
 
-GRID_SIZE_VALUES = (9, 13, 17, 25)        # ref harness.py:43
-NUM_RULES_VALUES = (1, 3, 6, 12, 24)      # ref harness.py:44
-SCALING_TRIAL_STEPS = 256                 # ref harness.py:51
+GRID_SIZE_VALUES = (9, 13, 17, 25)        # ref harness.py:44
+NUM_RULES_VALUES = (1, 3, 6, 12, 24)      # ref harness.py:45
+SCALING_TRIAL_STEPS = 256                 # ref harness.py:52
 MODES = ("step", "steps", "rollout")
 
 

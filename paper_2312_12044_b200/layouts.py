@@ -1,6 +1,6 @@
 """Room layouts: static geometry resolved on the host, uploaded once.
 
-Behaviour follows the reference (ref layouts.py:441-550): a bordered grid
+Behaviour follows the reference (ref layouts.py:18-127): a bordered grid
 split into 1/2/4/6/9 rooms by wall lines at ``i*(size-1)//rooms``, one door
 segment per shared wall, enumerated vertical walls first (room row, then
 wall column) and then horizontal walls (wall row, then room column); that
@@ -74,7 +74,7 @@ def plan_layout(layout: Layout, height: int, width: int) -> LayoutPlan:
 
 def bordered(height: int, width: int, goal: bool) -> np.ndarray:
     """Single-room grid of the classic ports, optionally with the green goal
-    square at (H-2, W-2) (ref scenarios.py:307-327)."""
+    square at (H-2, W-2) (ref scenarios.py:69-89)."""
     g = np.full((height, width), FLOOR_CODE, np.uint8)
     g[[0, -1], :] = WALL_CODE
     g[:, [0, -1]] = WALL_CODE

@@ -8,7 +8,7 @@ shard's trajectories identical to the same envs of a single-GPU run -- the
 property the reference tests for its process pool (ref
 tests/test_harness.py:105-122).  After a run one all-reduce (NCCL on GPUs,
 gloo in the CPU tests) sums the episode statistics (ref RolloutStats,
-harness.py:314-354).
+harness.py:103-143).
 """
 
 from __future__ import annotations

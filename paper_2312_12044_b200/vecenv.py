@@ -118,7 +118,7 @@ def policy_keys(key: Key, num: int, offset: int = 0, device=None) -> torch.Tenso
 
 def random_actions(keys: torch.Tensor, t0: int, steps: int) -> torch.Tensor:
     """(steps, n) uint8: word (t0+t) of each key's draw stream mod 6, the
-    random policy of ref harness.py:269-275 evaluated on the GPU."""
+    random policy of ref harness.py:58-64 evaluated on the GPU."""
     n = keys.shape[0]
     out = torch.empty((steps, n), dtype=torch.uint8, device=keys.device)
     with _device_ctx(keys.device):
@@ -375,7 +375,7 @@ class VecEnv:
     def enable_stats(self) -> torch.Tensor:
         """Accumulate episode statistics inside the step kernel: returns the
         (num_ctas, 3) float64 tensor of per-CTA [sum reward, finished trials,
-        sum of their lengths] (ref RolloutStats, harness.py:314-354)."""
+        sum of their lengths] (ref RolloutStats, harness.py:103-143)."""
         if self.stats is None:
             self.stats = torch.zeros(((self.num_envs + 127) // 128, 3), dtype=torch.float64, device=self.device)
         return self.stats
