@@ -18,21 +18,36 @@ from .helpers import benchmark_file, oracle_from_table
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("env_name,config,n,steps", [
-    ("XLand-MiniGrid-R4-13x13", "medium", 1 << 20, 520),
-    ("XLand-MiniGrid-R9-25x25", "high", 1 << 19, 300),
+_TABLES = {}
+
+
+def _table(config, rows):
+    from paper_2312_12044_b200 import load_benchmark
+    key = (config, rows)
+    if key not in _TABLES:
+        _TABLES[key] = load_benchmark(benchmark_file(config, rows))
+    return _TABLES[key]
+
+
+# The bench's tables: the "1m-style" M = 2^20 rows of SURVEY.md 8(d) for C3 /
+# C4 (every env of a 2^20 batch runs its own task row).  C3 at 2^21 envs is
+# the north_star's per-GPU share of 2^24 over 8 GPUs; C4's shard runs past
+# its 1875-step budget.
+@pytest.mark.parametrize("env_name,config,n,steps,width", [
+    ("XLand-MiniGrid-R4-13x13", "medium", 1 << 20, 520, 256),
+    ("XLand-MiniGrid-R4-13x13", "medium", 1 << 21, 512, 128),
+    ("XLand-MiniGrid-R9-25x25", "high", 1 << 19, 1880, 96),
 ])
-def test_full_batch_slices_vs_oracle(env_name, config, n, steps):
+def test_full_batch_slices_vs_oracle(env_name, config, n, steps, width):
     from oracle import oracle as O
-    from paper_2312_12044_b200 import VecEnv, key_from_seed, load_benchmark, make, policy_keys, random_actions
+    from paper_2312_12044_b200 import VecEnv, key_from_seed, make, policy_keys, random_actions
     _, params = make(env_name)
-    bm = load_benchmark(benchmark_file(config))
+    bm = _table(config, 1 << 20)
     table = bm.task_table()
     vec = VecEnv(params, n, bm)
     stats = vec.enable_stats()
     root, pol = key_from_seed(0), key_from_seed(1)
     ts = vec.reset(root)
-    width = 256
     offs = [0, n // 2 + 77, n - width]
     oras = []
     for off in offs:
@@ -49,12 +64,18 @@ def test_full_batch_slices_vs_oracle(env_name, config, n, steps):
     acts = random_actions(pk, 0, steps)
     rew_sum = torch.zeros((), dtype=torch.float64, device=vec.device)
     last_sum = torch.zeros((), dtype=torch.float64, device=vec.device)
+    budget = params.step_budget
     for t in range(steps):
         ts = vec.step(acts[t])
         rew_sum += ts.rewards.double().sum()
         last_sum += (ts.step_types == 2).double().sum()
+        # the oracle slices step every time; the records are compared every
+        # 4th step, around the budget reset and at the end
+        check = t % 4 == 0 or abs(t - (budget - 1)) <= 3 or t == steps - 1
         for off, ora, a in oras:
             o, r, d, s = ora.step(a[t])
+            if not check:
+                continue
             sl = slice(off, off + width)
             np.testing.assert_array_equal(ts.step_types[sl].cpu().numpy(), s, err_msg=f"{off} t={t}")
             np.testing.assert_array_equal(ts.rewards[sl].cpu().numpy(), r.astype(np.float32))
