@@ -175,10 +175,14 @@ __device__ __forceinline__ void warp_stats_step(double* stats, int slot, float r
   }
 }
 
-// Warp copy of nbytes from src to dst (equal alignment mod 16), the body in
-// 16-byte chunks; the source is read through L2 (.cg: records written by an
+// Warp copy of nbytes from src to dst, the body in 16-byte chunks when both
+// share their alignment mod 16 (else byte by byte); the source is read through L2 (.cg: records written by an
 // earlier kernel, never cached in this SM's L1).
 __device__ __forceinline__ void warp_copy_cg(uint8_t* dst, const uint8_t* src, int nbytes, int lane) {
+  if ((reinterpret_cast<uintptr_t>(dst) ^ reinterpret_cast<uintptr_t>(src)) & 15) {  // different alignment: bytes
+    for (int t = lane; t < nbytes; t += 32) dst[t] = __ldcg(src + t);
+    return;
+  }
   const int head = min((int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15), nbytes);
   if (lane < head) dst[lane] = __ldcg(src + lane);
   const int body = (nbytes - head) >> 4;

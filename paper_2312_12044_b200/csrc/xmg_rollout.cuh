@@ -122,12 +122,15 @@ __device__ __forceinline__ bool fused_batch_rejected(const uint8_t* actions, int
 __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel(const xmg_env_desc d, const xmg_state s,
                                                                  const uint64_t* pkeys, const uint8_t* actions,
                                                                  int64_t t0, int64_t T, int64_t n, const xmg_out o,
-                                                                 uint32_t* gflag) {
+                                                                 uint32_t* gflag, int epw) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (gflag != nullptr && fused_batch_rejected(actions, n, gflag)) return;
   const int64_t chunk = (int64_t)blockIdx.x * kRollWarps + warp;
-  const int64_t e0 = 32 * chunk;
+  // epw envs per warp (lanes >= epw idle): 32 for throughput; fewer for the
+  // one-kernel step of small batches, where a warp's serial PUT_DOWN / reset
+  // work (not occupancy) sets the latency
+  const int64_t e0 = (int64_t)epw * chunk;
   if (e0 >= n) return;  // warp-uniform
   const int H = d.height, W = d.width, HW = H * W, V = d.view_size, R = d.rule_width;
   const RollGeo geo = make_roll_geo(H, W, V, R);
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
   xmg_env_desc* sdesc = reinterpret_cast<xmg_env_desc*>(smem + kRollWarps * geo.warp_bytes);
   ResetOut* rout = reinterpret_cast<ResetOut*>(make_scratch(scratch, geo.hwp).misc + 40);
 
-  const int nvalid = (int)min((int64_t)32, n - e0);
+  const int nvalid = (int)min((int64_t)epw, n - e0);
   const int64_t e = e0 + lane;
   const bool valid = lane < nvalid;
   const bool xland = d.scenario == XMG_SCENARIO_XLAND;
@@ -379,6 +382,6 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
                         (uint64_t)goal_word | ((uint64_t)(uint32_t)task << 32));
     reinterpret_cast<ulonglong2*>(s.rng)[e] = rk;
   }
-  if (o.stats != nullptr) warp_stats(o.stats, (int)(chunk / kWarps), st_ret, st_trials, st_len);
+  if (o.stats != nullptr) warp_stats(o.stats, (int)(e0 / kThreads), st_ret, st_trials, st_len);
   if (lane == 0 && o.obs != nullptr) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }

@@ -431,15 +431,30 @@ int maybe_prebuild(const xmg_env_desc* d, const xmg_state* s, uint32_t epoch, in
   return launch_prebuild(d, s, cls, p.classes, n, st) ? -1 : 1;
 }
 
+// envs per warp of the one-kernel step (xmg_step_fused): 32; XMG_FUSED_EPW
+// (1..32, a power of two) for experiments — fewer envs per warp measured
+// slower at C2 (17.4 -> 22.8 / 36.5 / 61 us per step at 16 / 8 / 4) and flat
+// at C1: the step is throughput-, not chain-bound
+int fused_epw(int64_t) {
+  static int e = -1;
+  if (e < 0) {
+    const char* v = getenv("XMG_FUSED_EPW");
+    e = v ? atoi(v) : 32;
+    if (e != 1 && e != 2 && e != 4 && e != 8 && e != 16) e = 32;
+  }
+  return e;
+}
+
 int launch_rollout(const xmg_env_desc* d, const xmg_state* s, const uint64_t* pkeys, const uint8_t* actions,
-                   int64_t t0, int64_t steps, int64_t n, const xmg_out* o, cudaStream_t st, uint32_t* gflag = nullptr) {
+                   int64_t t0, int64_t steps, int64_t n, const xmg_out* o, cudaStream_t st, uint32_t* gflag = nullptr,
+                   int epw = 32) {
   const RollGeo geo = make_roll_geo(d->height, d->width, d->view_size, d->rule_width);
   if (!cur_dev()) return -1;
   if (geo.total > kMaxDynSmem - 1024) return fail("grid too large for the rollout kernel's shared-memory state");
-  const int64_t chunks = (n + 31) / 32;
+  const int64_t chunks = (n + epw - 1) / epw;
   const int64_t blocks = (chunks + kRollWarps - 1) / kRollWarps;
   rollout_kernel<<<(unsigned)blocks, kRollWarps * 32, (size_t)geo.total, st>>>(*d, *s, pkeys, actions, t0, steps, n,
-                                                                             *o, gflag);
+                                                                             *o, gflag, epw);
   return check_launch("rollout_kernel");
 }
 
@@ -661,7 +676,7 @@ int32_t xmg_step_fused(const xmg_env_desc* desc, const xmg_state* state, const u
   if (!out->reward || !out->discount || !out->step_type) return fail("reward / discount / step_type are required");
   if ((reinterpret_cast<uintptr_t>(state->agent) & 15) || (reinterpret_cast<uintptr_t>(state->rng) & 15))
     return fail("agent / rng buffers must be 16-byte aligned");
-  return launch_rollout(desc, state, nullptr, actions, 0, 1, n, out, (cudaStream_t)stream, gflag);
+  return launch_rollout(desc, state, nullptr, actions, 0, 1, n, out, (cudaStream_t)stream, gflag, fused_epw(n));
 }
 
 // One fused step captured into an executable CUDA graph (the pointers and
@@ -682,7 +697,7 @@ int32_t xmg_graph_create(const xmg_env_desc* desc, const xmg_state* state, const
   if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
     rc = fail("cudaStreamBeginCapture failed");
   } else {
-    rc = launch_rollout(desc, state, nullptr, actions, 0, 1, n, out, st, gflag);
+    rc = launch_rollout(desc, state, nullptr, actions, 0, 1, n, out, st, gflag, fused_epw(n));
     const cudaError_t e = cudaStreamEndCapture(st, &graph);
     if (!rc && e != cudaSuccess) rc = fail(std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e));
   }

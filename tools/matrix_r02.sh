@@ -1,2 +1,3 @@
-for L in build_variants/*.so; do XMG_LIB=$L timeout 300 python tools/time_prebuild.py c3 2>&1 | tail -1; done
-for L in build_variants/p1g4.so build_variants/p4g4.so; do XMG_LIB=$L timeout 300 python tools/time_prebuild.py c4 2>&1 | tail -1; XMG_LIB=$L timeout 300 python tools/time_prebuild.py doorkey 2>&1 | tail -1; done
+python -m pytest tests/test_graph_gpu.py -x -q 2>&1 | tail -1
+for e in 32 16 8 4; do XMG_FUSED_EPW=$e python tools/graph_probe.py c1 1000 2>&1 | grep "graph=True" | sed "s/^/epw=$e /"; XMG_FUSED_EPW=$e python tools/graph_probe.py c2 500 2>&1 | grep "graph=True" | sed "s/^/epw=$e /"; done
+XMG_FUSED_EPW=4 python -m pytest tests/test_graph_gpu.py -x -q 2>&1 | tail -1
