@@ -387,6 +387,9 @@ def run_ours(args):
         if shared:
             dist.init_process_group("gloo")
         else:
+            # the communicator's init lines stay visible on stderr (rank count, devices)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
 
     def coll(t: torch.Tensor) -> torch.Tensor:  # tensor placement the backend reduces

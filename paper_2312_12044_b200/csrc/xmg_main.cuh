@@ -47,16 +47,19 @@ constexpr uint32_t kQPut = 1u << 31, kQReset = 1u << 30, kQEnv = (1u << 30) - 1;
 constexpr uint64_t kStageReady = 2ull << 18, kStageMask = 3ull << 18;
 __device__ __forceinline__ bool ahead_on(const xmg_state& s) { return s.next_grids != nullptr; }
 
-// capacity of one sub-queue: every env of the step_main CTAs (128 envs each) feeding it
+// capacity of one sub-queue: every env of the step_main CTAs (128 envs each)
+// feeding it.  Unsigned arithmetic: n < 2^30 (validate_desc), and signed
+// 64-bit divisions cost a sign fix-up in every kernel prologue.
 __host__ __device__ inline int64_t queue_cap(int64_t n) {
-  const int64_t blocks = (n + kThreads - 1) / kThreads;
-  return (blocks + kQueues - 1) / kQueues * kThreads;
+  const uint64_t blocks = ((uint64_t)n + kThreads - 1) / kThreads;
+  return (int64_t)((blocks + kQueues - 1) / kQueues * kThreads);
 }
 
 // Entry slots of sub-queue (parity, kind, q): double-buffered like the counts,
 // so step t + 1's step_main appends while step t's step_rare still drains.
 __host__ __device__ inline int64_t queue_base(int64_t n, uint32_t parity, int kind, int q) {
-  return kWorkHeader + ((int64_t)(parity & 1) * 2 * kQueues + kind * kQueues + q) * queue_cap(n);
+  return (int64_t)(kWorkHeader + ((uint64_t)(parity & 1) * 2 * kQueues + (uint64_t)(kind * kQueues + q)) *
+                                     (uint64_t)queue_cap(n));
 }
 
 // Chunk bookkeeping after the queues (chunk = the 32 envs of one step_main warp):
@@ -64,8 +67,12 @@ __host__ __device__ inline int64_t queue_base(int64_t n, uint32_t parity, int ki
 //   dirty[nchunks]    epoch of the last step that queued envs of the chunk
 // Only the chunk's own warp reads and writes its dirty word, so the tag needs
 // no clearing.
-__host__ __device__ inline int64_t num_chunks(int64_t n) { return (n + kThreads - 1) / kThreads * kWarps; }
-__host__ __device__ inline int64_t pending_base(int64_t n) { return kWorkHeader + 4 * kQueues * queue_cap(n); }
+__host__ __device__ inline int64_t num_chunks(int64_t n) {
+  return (int64_t)(((uint64_t)n + kThreads - 1) / kThreads * kWarps);
+}
+__host__ __device__ inline int64_t pending_base(int64_t n) {
+  return (int64_t)(kWorkHeader + 4ull * kQueues * (uint64_t)queue_cap(n));
+}
 __host__ __device__ inline int64_t dirty_base(int64_t n) { return pending_base(n) + num_chunks(n); }
 // then the two counter words of the reset-ahead batches (prebuild_kernel)
 __host__ __device__ inline int64_t prebuild_ctr_base(int64_t n) { return dirty_base(n) + num_chunks(n); }
