@@ -257,90 +257,24 @@ __device__ __forceinline__ bool batch_rejected(const uint32_t* flag, uint32_t ep
   return flag != nullptr && *reinterpret_cast<volatile const uint32_t*>(flag) == epoch;
 }
 
-// FULL: small grids are staged whole, issued before the state word arrives
-// (one DRAM round trip per env instead of two: state word -> view window).
+// The step of one 128-env tile after its loads (state word `ag` of this
+// thread's env, its action, the chunk wait done): window staging, action,
+// rules, goal, counters, queues, reset-ahead copies, statistics and the
+// observation.
 template <int MAXCH, bool FULL>
-__global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_desc d, const xmg_state s,
-                                                                const xmg_out o, const void* actions, int act_dtype,
-                                                                const uint32_t* abort_flag, uint32_t epoch,
-                                                                int64_t n) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // Launched as a programmatic dependent of the previous kernel (the previous
-  // step's step_rare, or this step's validation), so it runs concurrently with
-  // the previous step_rare: with a validation it waits for the verdict, and
-  // per 32-env chunk it waits only where the previous step queued envs (below).
+__device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_state& s, const xmg_out& o,
+                                               uint32_t epoch, int64_t n, int64_t tile, int tid, int lane, int warp,
+                                               const MainGeo& geo, WView& vw, uint32_t* rbuf, uint8_t* obs_stage,
+                                               ulonglong2 ag, int act, uint64_t pol_keep, uint64_t pol_stream) {
   const int H = d.height, W = d.width, HW = H * W, V = d.view_size, R = d.rule_width;
-  const MainGeo geo = make_main_geo(V, MAXCH, R);
-  const int64_t tile = blockIdx.x;
   const int64_t e0 = tile * kThreads;
   const int64_t chunk = tile * kWarps + warp;
   uint32_t* pending = s.work + pending_base(n) + chunk;
   uint32_t* dirty = s.work + dirty_base(n) + chunk;
   const int64_t e = e0 + tid;
   const bool valid = e < n;
-
-  uint8_t* rb_base = smem + kThreads * geo.stg;
-  uint8_t* obs_stage = rb_base + warp * 32 * geo.rb;  // aliases the warp's rule rows
-  WView vw;
-  vw.g = s.grids + (valid ? e : 0) * (int64_t)HW;
-  vw.stage = smem + tid * geo.stg;
-  vw.sbase = vw.slo = vw.shi = 0;
-  uint32_t* rbuf = reinterpret_cast<uint32_t*>(rb_base + tid * geo.rb);
-  if (FULL && valid) stage_issue<MAXCH>(vw, 0, HW, HW);
-
-  // ---- load: the 16-byte state word and the action
-  ulonglong2 ag = make_ulonglong2(0, 0);
-  int act = 1;
-  const uint32_t was_dirty = e0 + warp * 32 < n ? *dirty : 0u;  // issued together with the state loads
-#if XMG_L2HINT
-  const uint64_t pol_keep = l2_policy_last(), pol_stream = l2_policy_first();
-#endif
-  if (valid) {
-#if XMG_L2HINT
-    ag = ld_hint_u64x2(reinterpret_cast<const ulonglong2*>(s.agent) + e, pol_keep);
-#else
-    ag = reinterpret_cast<const ulonglong2*>(s.agent)[e];
-#endif
-    act = load_action(actions, act_dtype, e);
-  }
-  // the loads above are in flight while the verdict is awaited (reads only:
-  // a rejected batch writes nothing; state step_rare may still rewrite is
-  // reloaded below)
-  if (abort_flag != nullptr) {  // this epoch's validation verdict (published by its last CTA)
-    if (lane == 0)
-      for (uint32_t spins = 0; ld_acquire(abort_flag + 1) != epoch; ++spins) {
-        if (spins > (1u << 25)) __trap();
-        __nanosleep(64);
-      }
-    __syncwarp();
-  }
-  // the previous step_rare has read these counts (it reads them before it
-  // lets this grid launch); this step appends to the other parity
-  if (blockIdx.x == 0)
-    for (int i = tid; i < 2 * kQueues; i += blockDim.x) s.work[count_index(epoch + 1, 0, 0) + i] = 0;
-  if (batch_rejected(abort_flag, epoch)) {
-    if (FULL) cp_async_wait_all();  // no copy may still target shared memory at exit
-    return;
-  }
-  if (was_dirty == epoch - 1 && e0 + warp * 32 < n) {
-    // the previous step queued envs of this chunk: wait until its step_rare has
-    // released them all, then reload the state word it may have rewritten
-    if (lane == 0) {
-      // bounded: a lost release is a bug, trap (launch error) rather than hang
-      for (uint32_t spins = 0; ld_acquire(pending) != 0; ++spins) {
-        if (spins > (1u << 25)) __trap();
-        __nanosleep(128);
-      }
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
-    __syncwarp();
-    if (valid) ag = ld_cg_u64x2(reinterpret_cast<const ulonglong2*>(s.agent) + e);
-    if (FULL && valid) {  // the early grid copy may predate step_rare's writes
-      cp_async_wait_all();
-      stage_issue<MAXCH>(vw, 0, HW, HW);
-    }
-  }
+  (void)pol_keep;
+  (void)pol_stream;
   int r = (int)(ag.x & 0xff), c = (int)((ag.x >> 8) & 0xff), dir = (int)((ag.x >> 16) & 3);
   int pocket = (int)((ag.x >> 24) & 0xff);
   uint32_t sc = (uint32_t)(ag.x >> 32);
@@ -509,4 +443,95 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
     for (uint32_t k = bulk + lane; k < bytes; k += 32) gdst[k] = obs_stage[k];
     if (lane == 0 && bulk) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
+}
+
+// FULL: small grids are staged whole, issued before the state word arrives
+// (one DRAM round trip per env instead of two: state word -> view window).
+template <int MAXCH, bool FULL>
+__global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_desc d, const xmg_state s,
+                                                                const xmg_out o, const void* actions, int act_dtype,
+                                                                const uint32_t* abort_flag, uint32_t epoch,
+                                                                int64_t n) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // Launched as a programmatic dependent of the previous kernel (the previous
+  // step's step_rare, or this step's validation), so it runs concurrently with
+  // the previous step_rare: with a validation it waits for the verdict, and
+  // per 32-env chunk it waits only where the previous step queued envs (below).
+  const int H = d.height, W = d.width, HW = H * W, V = d.view_size, R = d.rule_width;
+  const MainGeo geo = make_main_geo(V, MAXCH, R);
+  const int64_t tile = blockIdx.x;
+  const int64_t e0 = tile * kThreads;
+  const int64_t chunk = tile * kWarps + warp;
+  uint32_t* pending = s.work + pending_base(n) + chunk;
+  uint32_t* dirty = s.work + dirty_base(n) + chunk;
+  const int64_t e = e0 + tid;
+  const bool valid = e < n;
+
+  uint8_t* rb_base = smem + kThreads * geo.stg;
+  uint8_t* obs_stage = rb_base + warp * 32 * geo.rb;  // aliases the warp's rule rows
+  WView vw;
+  vw.g = s.grids + (valid ? e : 0) * (int64_t)HW;
+  vw.stage = smem + tid * geo.stg;
+  vw.sbase = vw.slo = vw.shi = 0;
+  uint32_t* rbuf = reinterpret_cast<uint32_t*>(rb_base + tid * geo.rb);
+  if (FULL && valid) stage_issue<MAXCH>(vw, 0, HW, HW);
+
+  // ---- load: the 16-byte state word and the action
+  ulonglong2 ag = make_ulonglong2(0, 0);
+  int act = 1;
+  const uint32_t was_dirty = e0 + warp * 32 < n ? *dirty : 0u;  // issued together with the state loads
+#if XMG_L2HINT
+  const uint64_t pol_keep = l2_policy_last(), pol_stream = l2_policy_first();
+#endif
+  if (valid) {
+#if XMG_L2HINT
+    ag = ld_hint_u64x2(reinterpret_cast<const ulonglong2*>(s.agent) + e, pol_keep);
+#else
+    ag = reinterpret_cast<const ulonglong2*>(s.agent)[e];
+#endif
+    act = load_action(actions, act_dtype, e);
+  }
+  // the loads above are in flight while the verdict is awaited (reads only:
+  // a rejected batch writes nothing; state step_rare may still rewrite is
+  // reloaded below)
+  if (abort_flag != nullptr) {  // this epoch's validation verdict (published by its last CTA)
+    if (lane == 0)
+      for (uint32_t spins = 0; ld_acquire(abort_flag + 1) != epoch; ++spins) {
+        if (spins > (1u << 25)) __trap();
+        __nanosleep(64);
+      }
+    __syncwarp();
+  }
+  // the previous step_rare has read these counts (it reads them before it
+  // lets this grid launch); this step appends to the other parity
+  if (blockIdx.x == 0)
+    for (int i = tid; i < 2 * kQueues; i += blockDim.x) s.work[count_index(epoch + 1, 0, 0) + i] = 0;
+  if (batch_rejected(abort_flag, epoch)) {
+    if (FULL) cp_async_wait_all();  // no copy may still target shared memory at exit
+    return;
+  }
+  if (was_dirty == epoch - 1 && e0 + warp * 32 < n) {
+    // the previous step queued envs of this chunk: wait until its step_rare has
+    // released them all, then reload the state word it may have rewritten
+    if (lane == 0) {
+      // bounded: a lost release is a bug, trap (launch error) rather than hang
+      for (uint32_t spins = 0; ld_acquire(pending) != 0; ++spins) {
+        if (spins > (1u << 25)) __trap();
+        __nanosleep(128);
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncwarp();
+    if (valid) ag = ld_cg_u64x2(reinterpret_cast<const ulonglong2*>(s.agent) + e);
+    if (FULL && valid) {  // the early grid copy may predate step_rare's writes
+      cp_async_wait_all();
+      stage_issue<MAXCH>(vw, 0, HW, HW);
+    }
+  }  main_tile_body<MAXCH, FULL>(d, s, o, epoch, n, tile, tid, lane, warp, geo, vw, rbuf, obs_stage, ag, act,
+#if XMG_L2HINT
+                              pol_keep, pol_stream);
+#else
+                              0, 0);
+#endif
 }

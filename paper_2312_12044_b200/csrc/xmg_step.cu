@@ -182,7 +182,8 @@ cudaError_t allow_smem(K kernel, int64_t dyn) {
   cudaFuncAttributes fa;
   cudaError_t err = cudaFuncGetAttributes(&fa, kernel);
   if (err != cudaSuccess) return err;
-  if (dyn + (int64_t)fa.sharedSizeBytes > kMaxDynSmem + 1024) return cudaErrorInvalidValue;
+  (void)dyn;  // the opt-in covers any size up to the per-block limit left beside the static shared memory
+  if ((int64_t)fa.sharedSizeBytes >= kMaxDynSmem) return cudaErrorInvalidValue;
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem - (int)fa.sharedSizeBytes);
 }
 
@@ -220,6 +221,7 @@ int device_attrs(int dev) {
         set_attr(di, step_main<12, false>, "step_main") && set_attr(di, step_main<16, false>, "step_main") &&
         set_attr(di, step_main<32, false>, "step_main") && set_attr(di, step_main<6, true>, "step_main") &&
         set_attr(di, step_main<8, true>, "step_main") && set_attr(di, step_main<12, true>, "step_main") &&
+
         set_attr(di, step_rare, "step_rare") && set_attr(di, prebuild_kernel, "prebuild_kernel") &&
         set_attr(di, rollout_kernel, "rollout_kernel");
     di.done = true;
@@ -355,6 +357,7 @@ bool use_full(const xmg_env_desc* d) {
 
 int dispatch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
                   const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st, bool pdl = true) {
+
 
   if (use_full(d)) {
     const int fc = full_chunks(d->height * d->width);

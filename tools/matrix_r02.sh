@@ -1,3 +1,3 @@
-python -m pytest tests/test_graph_gpu.py -x -q 2>&1 | tail -1
-for e in 32 16 8 4; do XMG_FUSED_EPW=$e python tools/graph_probe.py c1 1000 2>&1 | grep "graph=True" | sed "s/^/epw=$e /"; XMG_FUSED_EPW=$e python tools/graph_probe.py c2 500 2>&1 | grep "graph=True" | sed "s/^/epw=$e /"; done
-XMG_FUSED_EPW=4 python -m pytest tests/test_graph_gpu.py -x -q 2>&1 | tail -1
+XMG_MAIN_P=1 timeout 600 python -m pytest tests/test_parity_gpu.py tests/test_reset_ahead_gpu.py -x -q 2>&1 | tail -2
+for p in 0 1; do XMG_MAIN_P=$p timeout 300 python tools/main_probe.py c3 2>&1 | tail -2; XMG_MAIN_P=$p timeout 300 python tools/steady.py c3 100 200 2>&1 | tail -1; done
+for p in 0 1; do XMG_MAIN_P=$p timeout 300 python tools/steady.py doorkey 100 200 2>&1 | tail -1; XMG_MAIN_P=$p timeout 300 python tools/steady.py c4 100 200 2>&1 | tail -1; done
