@@ -65,10 +65,20 @@ __device__ __forceinline__ void warp_store_grid(uint8_t* dst, const uint8_t* src
 // x mod d for d < 2^16 with 32-bit arithmetic only (the 64-bit remainder is a
 // long software sequence): x = hi * 2^32 + lo, so
 // x mod d = ((hi mod d) * (2^32 mod d) + lo mod d) mod d, every term < 2^32.
+// y mod d for y < 2^53 and 1 <= d < 2^16: the quotient from a double product
+// (exact inputs; the estimate is within one of the quotient) then corrected.
+__device__ __forceinline__ uint32_t mod_small(uint64_t y, uint32_t d, double rd) {
+  const uint64_t q = (uint64_t)__dmul_rz((double)y, rd);
+  int64_t r = (int64_t)(y - q * d);
+  r += r < 0 ? (int64_t)d : 0;
+  r -= r >= (int64_t)d ? (int64_t)d : 0;
+  return (uint32_t)r;
+}
 __device__ __forceinline__ uint32_t mod64_small(uint64_t x, uint32_t d) {
-  const uint32_t t = (uint32_t)((0xFFFFFFFFu % d) + 1u) % d;  // 2^32 mod d
-  const uint32_t a = ((uint32_t)(x >> 32) % d) * t % d;
-  return (a + (uint32_t)x % d) % d;
+  const double rd = __drcp_rn((double)d);
+  const uint32_t a = mod_small(x >> 32, d, rd);  // hi mod d
+  // x mod d = (a * 2^32 + lo) mod d, and a * 2^32 + lo < 2^48
+  return mod_small(((uint64_t)a << 32) | (uint32_t)x, d, rd);
 }
 
 // Row-major floor cells of the scratch grid into fc[]; returns their count

@@ -10,7 +10,7 @@ __device__ __forceinline__ uint16_t obs_cell(const uint8_t* G, int r, int c, int
                                              bool see) {
   const int h = V / 2;
   const int fr = dir_dr(d), fc = dir_dc(d), rr = fc, rc = -fr;
-  const int i = cell / V, j = cell - (cell / V) * V;
+  const int i = V == 5 ? cell / 5 : cell / V, j = cell - i * V;  // (the registered views are 5)
   const int ahead = V - 1 - i, lat = j - h;
   const int wr = r + ahead * fr + lat * rr, wc = c + ahead * fc + lat * rc;
   if (wr < 0 || wr >= H || wc < 0 || wc >= W) return 0;

@@ -453,7 +453,7 @@ class VecEnv:
         self.epoch += 1
         _lib.check(L.xmg_step(self._desc_ref, self._state_ref, actions.data_ptr(), dt, n, o[1], flag_ptr,
                               self.epoch & 0xFFFFFFFF, stream), "xmg_step")
-        self.launches += 2  # streaming pass + rare-work pass
+        self.launches += 2 + self._batches_in(self.epoch - 1, self.epoch)  # streaming + rare passes (+ batch)
         if self.strict and flag_ptr is not None:
             self.check()
         return VecTimeStep(*outs)
@@ -573,7 +573,7 @@ class VecEnv:
         _lib.check(_lib.lib().xmg_steps(self._desc_ref, self._state_ref, actions.data_ptr(), dt, k, n, C.byref(o),
                                         self.epoch & 0xFFFFFFFF, _stream(dev)), "xmg_steps")
         self.epoch += k
-        self.launches += 2 * k
+        self.launches += 2 * k + self._batches_in(self.epoch - k, self.epoch)
         return out
 
     def aligned_fused_choice(self) -> bool:
@@ -626,6 +626,14 @@ class VecEnv:
                 torch.empty((steps, n), dtype=torch.float32, device=dev) if "discounts" in record else None,
                 torch.empty((steps, n), dtype=torch.int8, device=dev) if "step_types" in record else None)
         return self._launch_rollout(steps, policy_keys, actions, t0, out)
+
+    def _batches_in(self, e0: int, e1: int) -> int:
+        """Reset-ahead batches libxmg launched for epochs (e0, e1] (one per
+        multiple of `every`, include/xmg.h)."""
+        if not self.reset_ahead:
+            return 0
+        ev = self._ahead_every
+        return (e1 & 0xFFFFFFFF) // ev - (e0 & 0xFFFFFFFF) // ev if e1 >= e0 else 0
 
     def _rollout_prebuilds(self, steps: int) -> None:
         """The reset-ahead batches `steps` step() calls would launch (one per
