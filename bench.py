@@ -165,10 +165,11 @@ def dist_env():
 
 def table_path(config):
     """The workload's ruleset table: the specified size when it is present,
-    else the largest table of the config (named in the JSON line)."""
+    else the largest table of the config (named in the JSON line).
+    XMG_BENCH_ROWS=<M> picks another size (development comparisons)."""
     from helpers import benchmark_file
     try:
-        return benchmark_file(config, TABLE_ROWS.get(config))
+        return benchmark_file(config, int(os.environ.get("XMG_BENCH_ROWS", 0)) or TABLE_ROWS.get(config))
     except FileNotFoundError:
         import glob
         paths = glob.glob(os.path.join(ROOT, "data", f"{config}-*.xmgb"))
