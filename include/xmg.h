@@ -193,6 +193,12 @@ int32_t xmg_ahead_plan(const xmg_env_desc* desc, int64_t n, int64_t* every, int6
 int32_t xmg_prebuild(const xmg_env_desc* desc, const xmg_state* state, int64_t cls, int64_t classes, int64_t n,
                      void* stream);
 
+/* xmg_validate_actions then xmg_step for the same epoch, from one host call
+ * (the per-call path of VecEnv.step with device actions). */
+int32_t xmg_step_validated(const xmg_env_desc* desc, const xmg_state* state, const void* actions,
+                           int32_t action_dtype, int64_t n, const xmg_out* out, uint32_t* flag, uint32_t epoch,
+                           void* stream);
+
 /* `steps` consecutive xmg_step calls issued from one host call (no per-step
  * host round trip: the path for batches too small to hide ~20-30 us of
  * Python + launch overhead per step).  actions [steps][n] must already be
@@ -241,12 +247,15 @@ int32_t xmg_rollout(const xmg_env_desc* desc, const xmg_state* state, const uint
 int32_t xmg_step_fused(const xmg_env_desc* desc, const xmg_state* state, const uint8_t* actions /*[n] u8*/, int64_t n,
                        const xmg_out* out, uint32_t* gflag, void* stream);
 
-/* xmg_step_fused captured once into an executable CUDA graph bound to these
- * buffers (actions: a fixed staging buffer the caller fills before each
- * launch); xmg_graph_launch replays one step (host cost: one graph launch). */
+/* xmg_step_fused as a one-node executable CUDA graph bound to these buffers
+ * (handle = opaque library object); xmg_graph_launch replays one step with
+ * the actions buffer it was given (host cost: one graph launch). */
 int32_t xmg_graph_create(const xmg_env_desc* desc, const xmg_state* state, const uint8_t* actions, int64_t n,
                          const xmg_out* out, uint32_t* gflag, void** graph_exec);
 int32_t xmg_graph_launch(void* graph_exec, void* stream);
+/* One step on the actions src [n] u8 (device; NULL = staging): the graph's
+ * node is re-pointed at src when it changed (no copy), then one launch. */
+int32_t xmg_graph_step(void* graph_exec, const uint8_t* src, uint8_t* staging, int64_t n, void* stream);
 int32_t xmg_graph_destroy(void* graph_exec);
 
 /* Dynamic shared memory per 128-env CTA of the rollout kernel (<0: unsupported). */

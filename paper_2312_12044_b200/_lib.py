@@ -35,7 +35,8 @@ EXPORTS = ("xmg_abi_version", "xmg_last_error", "xmg_philox", "xmg_split_batch",
            "xmg_step", "xmg_step_smem_bytes", "xmg_work_words", "xmg_profile", "xmg_profile_read", "xmg_rollout",
            "xmg_rollout_smem_bytes", "xmg_sprites", "xmg_image_obs", "xmg_steps", "xmg_image_atlas_bytes",
            "xmg_image_atlas", "xmg_image_obs_aligned", "xmg_ahead_plan", "xmg_prebuild",
-           "xmg_step_fused", "xmg_graph_create", "xmg_graph_launch", "xmg_graph_destroy")
+           "xmg_step_fused", "xmg_graph_create", "xmg_graph_launch", "xmg_graph_destroy", "xmg_step_validated",
+           "xmg_graph_step")
 
 
 class NativeLibraryError(RuntimeError):
@@ -91,6 +92,8 @@ def _bind(L):
         "xmg_reset": ([C.POINTER(EnvDesc), C.POINTER(State), vp, i64, C.POINTER(Out), vp], i32),
         "xmg_validate_actions": ([vp, i32, i64, C.c_uint32, vp, vp], i32),
         "xmg_step": ([C.POINTER(EnvDesc), C.POINTER(State), vp, i32, i64, C.POINTER(Out), vp, C.c_uint32, vp], i32),
+        "xmg_step_validated": ([C.POINTER(EnvDesc), C.POINTER(State), vp, i32, i64, C.POINTER(Out), vp, C.c_uint32,
+                                vp], i32),
         "xmg_step_smem_bytes": ([C.POINTER(EnvDesc)], i64),
         "xmg_work_words": ([i64], i64),
         "xmg_profile": ([i32], i32),
@@ -109,6 +112,7 @@ def _bind(L):
         "xmg_graph_create": ([C.POINTER(EnvDesc), C.POINTER(State), vp, i64, C.POINTER(Out), vp,
                               C.POINTER(C.c_void_p)], i32),
         "xmg_graph_launch": ([vp, vp], i32),
+        "xmg_graph_step": ([vp, vp, vp, i64, vp], i32),
         "xmg_graph_destroy": ([vp], i32),
     }
     for name, (args, res) in sig.items():

@@ -576,6 +576,14 @@ int32_t xmg_step(const xmg_env_desc* desc, const xmg_state* state, const void* a
   return rc;
 }
 
+int32_t xmg_step_validated(const xmg_env_desc* desc, const xmg_state* state, const void* actions,
+                           int32_t action_dtype, int64_t n, const xmg_out* out, uint32_t* flag, uint32_t epoch,
+                           void* stream) {
+  if (!flag) return fail("null flag");
+  if (xmg_validate_actions(actions, action_dtype, n, epoch, flag, stream)) return -1;
+  return xmg_step(desc, state, actions, action_dtype, n, out, flag, epoch, stream);
+}
+
 int32_t xmg_steps(const xmg_env_desc* desc, const xmg_state* state, const void* actions, int32_t action_dtype,
                   int64_t steps, int64_t n, const xmg_out* traj, uint32_t epoch0, void* stream) {
   if (validate_desc(desc, state, n)) return -1;
@@ -682,8 +690,26 @@ int32_t xmg_step_fused(const xmg_env_desc* desc, const xmg_state* state, const u
   return launch_rollout(desc, state, nullptr, actions, 0, 1, n, out, (cudaStream_t)stream, gflag, fused_epw(n));
 }
 
-// One fused step captured into an executable CUDA graph (the pointers and
-// the description are baked in; the step number lives in gflag[3]).
+// One fused step as a one-node executable CUDA graph (built from explicit
+// kernel-node parameters, not a stream capture, so the actions pointer of
+// the node can be re-pointed at each launch: no staging copy).
+struct GraphStep {
+  cudaGraph_t graph = nullptr;  // kept: the node handle belongs to it
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphNode_t node = nullptr;
+  cudaKernelNodeParams params = {};
+  // the kernel's arguments (rollout_kernel), pointed to by params.kernelParams
+  xmg_env_desc d;
+  xmg_state s;
+  const uint64_t* pkeys = nullptr;
+  const uint8_t* actions = nullptr;
+  int64_t t0 = 0, T = 1, n = 0;
+  xmg_out o;
+  uint32_t* gflag = nullptr;
+  int epw = 32;
+  void* args[10];
+};
+
 int32_t xmg_graph_create(const xmg_env_desc* desc, const xmg_state* state, const uint8_t* actions, int64_t n,
                          const xmg_out* out, uint32_t* gflag, void** graph_exec) {
   if (!graph_exec) return fail("null graph handle");
@@ -691,37 +717,72 @@ int32_t xmg_graph_create(const xmg_env_desc* desc, const xmg_state* state, const
   if (validate_desc(desc, state, n)) return -1;
   if (!out || !actions || !gflag) return fail("null out / actions / gflag");
   if (!out->reward || !out->discount || !out->step_type) return fail("reward / discount / step_type are required");
-  if (!cur_dev()) return -1;  // attributes set before the capture
-  cudaStream_t st = nullptr;
-  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return fail("cudaStreamCreate failed");
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
+  if (!cur_dev()) return -1;  // kernel attributes are set before the node is built
+  const RollGeo geo = make_roll_geo(desc->height, desc->width, desc->view_size, desc->rule_width);
+  if (geo.total > kMaxDynSmem - 1024) return fail("grid too large for the rollout kernel's shared-memory state");
+  GraphStep* g = new GraphStep();
+  g->d = *desc;
+  g->s = *state;
+  g->actions = actions;
+  g->n = n;
+  g->o = *out;
+  g->gflag = gflag;
+  g->epw = fused_epw(n);
+  void* args[10] = {&g->d, &g->s, &g->pkeys, &g->actions, &g->t0, &g->T, &g->n, &g->o, &g->gflag, &g->epw};
+  for (int i = 0; i < 10; ++i) g->args[i] = args[i];
+  const int64_t blocks = ((n + g->epw - 1) / g->epw + kRollWarps - 1) / kRollWarps;
+  g->params.func = reinterpret_cast<void*>(rollout_kernel);
+  g->params.gridDim = dim3((unsigned)blocks);
+  g->params.blockDim = dim3(kRollWarps * 32);
+  g->params.sharedMemBytes = (unsigned)geo.total;
+  g->params.kernelParams = g->args;
+  g->params.extra = nullptr;
   int rc = 0;
-  if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
-    rc = fail("cudaStreamBeginCapture failed");
-  } else {
-    rc = launch_rollout(desc, state, nullptr, actions, 0, 1, n, out, st, gflag, fused_epw(n));
-    const cudaError_t e = cudaStreamEndCapture(st, &graph);
-    if (!rc && e != cudaSuccess) rc = fail(std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e));
+  if (cudaGraphCreate(&g->graph, 0) != cudaSuccess) rc = fail("cudaGraphCreate failed");
+  if (!rc) {
+    const cudaError_t e = cudaGraphAddKernelNode(&g->node, g->graph, nullptr, 0, &g->params);
+    if (e != cudaSuccess) rc = fail(std::string("cudaGraphAddKernelNode: ") + cudaGetErrorString(e));
   }
   if (!rc) {
-    const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    const cudaError_t e = cudaGraphInstantiate(&g->exec, g->graph, 0);
     if (e != cudaSuccess) rc = fail(std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
   }
-  if (graph) cudaGraphDestroy(graph);
-  cudaStreamDestroy(st);
-  if (!rc) *graph_exec = exec;
-  return rc;
+  if (rc) {
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+    return rc;
+  }
+  *graph_exec = g;
+  return 0;
 }
 
-int32_t xmg_graph_launch(void* graph_exec, void* stream) {
-  if (!graph_exec) return fail("null graph handle");
-  const cudaError_t e = cudaGraphLaunch((cudaGraphExec_t)graph_exec, (cudaStream_t)stream);
+int32_t xmg_graph_launch(void* handle, void* stream) {
+  if (!handle) return fail("null graph handle");
+  GraphStep* g = static_cast<GraphStep*>(handle);
+  const cudaError_t e = cudaGraphLaunch(g->exec, (cudaStream_t)stream);
   return e == cudaSuccess ? 0 : fail(std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
 }
 
-int32_t xmg_graph_destroy(void* graph_exec) {
-  if (graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)graph_exec);
+int32_t xmg_graph_step(void* handle, const uint8_t* src, uint8_t* staging, int64_t n, void* stream) {
+  if (!handle) return fail("null graph handle");
+  GraphStep* g = static_cast<GraphStep*>(handle);
+  const uint8_t* want = src ? src : staging;
+  if (n != g->n) return fail("xmg_graph_step: n differs from the graph's");
+  if (want != g->actions) {  // re-point the node at this step's actions (host-side update, no copy)
+    g->actions = want;
+    const cudaError_t e = cudaGraphExecKernelNodeSetParams(g->exec, g->node, &g->params);
+    if (e != cudaSuccess) return fail(std::string("cudaGraphExecKernelNodeSetParams: ") + cudaGetErrorString(e));
+  }
+  return xmg_graph_launch(handle, stream);
+}
+
+int32_t xmg_graph_destroy(void* handle) {
+  if (handle) {
+    GraphStep* g = static_cast<GraphStep*>(handle);
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+  }
   return 0;
 }
 

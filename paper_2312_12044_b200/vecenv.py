@@ -41,7 +41,14 @@ GRID_PAD = 64  # the step kernel reads 16-byte aligned chunks past the last grid
 STAGE_BITS = 3 << 18  # reset-ahead stage in state word 0 (include/xmg.h)
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+_get_device = getattr(torch._C, "_cuda_getDevice", None) or torch.cuda.current_device
+
+
 def _stream(device: torch.device) -> int:
+    """The current CUDA stream of `device` (raw handle; no Stream object per call)."""
+    if _raw_stream is not None:
+        return _raw_stream(device.index if device.index is not None else _get_device())
     return torch.cuda.current_stream(device).cuda_stream
 
 
@@ -51,7 +58,7 @@ def _on_device(fn):
     VecEnv on cuda:1 must not launch while cuda:0 is current."""
     @functools.wraps(fn)
     def wrapper(self, *args, **kwargs):
-        if torch.cuda.current_device() == self._dev_index:
+        if _get_device() == self._dev_index:
             return fn(self, *args, **kwargs)
         with torch.cuda.device(self._dev_index):
             return fn(self, *args, **kwargs)
@@ -308,6 +315,7 @@ class VecEnv:
             self._ahead_every, self._ahead_classes = int(ev.value), int(cl.value)
         self._roll_clock = 0
         self._desc_ref = C.byref(self._desc)
+        self._L = _lib.lib()
         self._state_ref = C.byref(self._state)
         self._flag_ptr = self._flag.data_ptr()
         self.stats: torch.Tensor | None = None
@@ -320,6 +328,7 @@ class VecEnv:
             self.reuse_outputs = True
             self._gflag = torch.zeros(4, dtype=torch.int32, device=dev)
             self._gact = torch.zeros(n + 16, dtype=torch.uint8, device=dev)[:n]
+            self._gact_ptr = self._gact.data_ptr()
             self._graphs: dict = {}
             self._gchecked = 0
 
@@ -419,7 +428,7 @@ class VecEnv:
         if self.graph:
             return self._step_graph(actions, compute_obs)
         n = self.num_envs
-        L = _lib.lib()
+        L = self._L
         stream = _stream(self.device)
         flag_ptr = None
         if isinstance(actions, torch.Tensor) and actions.is_cuda:
@@ -431,10 +440,8 @@ class VecEnv:
                 dt = _lib.ACT_I64
             if not actions.is_contiguous():
                 actions = actions.contiguous()
-            if validate:
+            if validate:  # the validation kernel is launched by xmg_step_validated below
                 flag_ptr = self._flag_ptr
-                _lib.check(L.xmg_validate_actions(actions.data_ptr(), dt, n, (self.epoch + 1) & 0xFFFFFFFF, flag_ptr,
-                                                  stream), "xmg_validate_actions")
                 self.launches += 1
         else:
             a = np.asarray(actions)
@@ -451,8 +458,14 @@ class VecEnv:
             if self.reuse_outputs:
                 self._out_cache = {id(outs): o}
         self.epoch += 1
-        _lib.check(L.xmg_step(self._desc_ref, self._state_ref, actions.data_ptr(), dt, n, o[1], flag_ptr,
-                              self.epoch & 0xFFFFFFFF, stream), "xmg_step")
+        if flag_ptr is not None:  # one library call: validation, then the step that awaits its verdict
+            rc = L.xmg_step_validated(self._desc_ref, self._state_ref, actions.data_ptr(), dt, n, o[1], flag_ptr,
+                                      self.epoch & 0xFFFFFFFF, stream)
+        else:
+            rc = L.xmg_step(self._desc_ref, self._state_ref, actions.data_ptr(), dt, n, o[1], None,
+                            self.epoch & 0xFFFFFFFF, stream)
+        if rc:
+            _lib.check(rc, "xmg_step")
         self.launches += 2 + self._batches_in(self.epoch - 1, self.epoch)  # streaming + rare passes (+ batch)
         if self.strict and flag_ptr is not None:
             self.check()
@@ -493,7 +506,11 @@ class VecEnv:
         """step() in graph mode: the same transition (bit-identical, the fused
         kernel at T = 1), one kernel per step replayed from a CUDA graph
         (captured once per record layout by libxmg: xmg_graph_create)."""
-        if actions is not self._gact:
+        src = None  # u8 device actions are copied into the staging buffer by libxmg with the launch
+        if isinstance(actions, torch.Tensor) and actions.is_cuda and actions.dtype == torch.uint8 \
+                and actions.shape == (self.num_envs,) and actions.is_contiguous():
+            src = actions.data_ptr()
+        elif actions is not self._gact:
             self._stage_actions(actions)
         if self.reset_ahead:
             self._roll_clock += 1
@@ -512,7 +529,9 @@ class VecEnv:
                                                    self.num_envs, C.byref(o), self._gflag.data_ptr(), C.byref(h)),
                        "xmg_graph_create")
             ent = self._graphs[key] = (h, o, VecTimeStep(*outs))
-        _lib.check(_lib.lib().xmg_graph_launch(ent[0], _stream(self.device)), "xmg_graph_launch")
+        rc = self._L.xmg_graph_step(ent[0], src, self._gact_ptr, self.num_envs, _stream(self.device))
+        if rc:
+            _lib.check(rc, "xmg_graph_step")
         self.launches += 1
         if self.strict:
             self.check()
