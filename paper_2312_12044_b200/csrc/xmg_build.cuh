@@ -307,39 +307,14 @@ __device__ void rank_place(const WarpScratch& ws, int lane, int F, int W, int mo
 
 // Every key a trial reset consumes, derived from the episode key ek:
 // ref:vecenv.py:224-227 (ks = split(ek, 0), next state key st = split(ek, 1))
-// and ref:scenarios.py:55,106,125,138 (k0, k1, k2 = split(ks, 3)); see
-// warp_trial_keys.
+// and ref:scenarios.py:55,106,125,138 (k0, k1, k2 = split(ks, 3)); and in
+// resample mode (an extension, not in the reference) the task word
+// draw0(split(ek, 2)) of Benchmark.sample_ruleset (ref:benchio.py:57-58).
 struct TrialKeys {
   uint64_t st_hi, st_lo, k0h, k0l, k1h, k1l, k2h, k2l, task_word;
 };
 
-__device__ __noinline__ void derive_trial_keys(uint64_t ek_hi, uint64_t ek_lo, bool resample, TrialKeys* out) {
-  TrialKeys k;
-  const Words4 ks = philox<2>(0, 0, kDomSplit, 0, ek_hi, ek_lo);
-  const Words4 st = philox<2>(1, 0, kDomSplit, 0, ek_hi, ek_lo);
-  k.st_hi = st.w0;
-  k.st_lo = st.w1;
-  uint64_t sub[6];
-#pragma unroll 1
-  for (int i = 0; i < 3; ++i) {
-    const Words4 w = philox<2>((uint64_t)i, 0, kDomSplit, 0, ks.w0, ks.w1);
-    sub[2 * i] = w.w0;
-    sub[2 * i + 1] = w.w1;
-  }
-  k.k0h = sub[0]; k.k0l = sub[1];
-  k.k1h = sub[2]; k.k1l = sub[3];
-  k.k2h = sub[4]; k.k2l = sub[5];
-  k.task_word = 0;
-  if (resample) {
-    // extension (not in the reference): a fresh task per trial, drawn as
-    // Benchmark.sample_ruleset(split(ek, 2)) = rows[word0 % M] (ref:benchio.py:57-58)
-    const Words4 tk = philox<2>(2, 0, kDomSplit, 0, ek_hi, ek_lo);
-    k.task_word = philox<2>(0, 0, kDomDraw, 0, tk.w0, tk.w1).w0;
-  }
-  *out = k;
-}
-
-// The same keys for up to 16 envs at once, spread over the lanes in two
+// The keys of up to 16 envs at once, spread over the lanes in two
 // dependent rounds instead of five blocks in series per env: round 1 derives
 // ks = split(ek, 0) and st = split(ek, 1) (+ split(ek, 2) for resample) of
 // every env, round 2 the three children of ks (+ the resample draw).  Env
