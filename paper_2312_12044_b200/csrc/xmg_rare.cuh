@@ -496,8 +496,10 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRar
 #ifdef XMG_TRACE
       if (i0 == j) XMG_TR(gw, 6, gtime());
 #endif
-      // ---- trials the PUT_DOWN finished: keys derived one env per lane, then
-      // the envs rebuilt by the whole warp
+      // ---- trials the PUT_DOWN finished: keys derived lane-parallel, then
+      // the envs rebuilt by the whole warp (copying a pre-built successor here
+      // instead measured ~1 us/step slower in steady state: step_rare's
+      // register pressure)
       if (lastm) {
         ulonglong2 ek = make_ulonglong2(0, 0);
         if ((lastm >> lane) & 1) ek = reinterpret_cast<const ulonglong2*>(s.rng)[e_l];
