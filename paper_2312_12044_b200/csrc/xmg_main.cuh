@@ -291,7 +291,7 @@ __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_
   uint32_t qflags = 0;
   float rew = 0.f;
   bool last = false, consume = false;
-  const bool ahead = ahead_on(s);
+  const bool ahead = ahead_on(s);  // (the copy path costs ~1 us/step of steady state at C3: measured)
   if (valid) {
     // ---- stage the post-action window (MOVE: both candidate poses) and,
     // for actions that can raise an event, the env's rule row
