@@ -16,10 +16,12 @@ from .test_parity_gpu import _assert_state
 pytestmark = pytest.mark.gpu
 
 
-def _pair(env_name, config, n, resample=False, table_rows=None):
+def _pair(env_name, config, n, resample=False, table_rows=None, **param_changes):
     from paper_2312_12044_b200 import VecEnv, load_benchmark, make
     from paper_2312_12044_b200.ruleset import TaskTable
     _, params = make(env_name)
+    if param_changes:
+        params = params.replace(**param_changes)
     if config:
         bm = load_benchmark(benchmark_file(config, table_rows))
         on = VecEnv(params, n, bm, reset_ahead=True, resample_tasks=resample)
@@ -32,18 +34,20 @@ def _pair(env_name, config, n, resample=False, table_rows=None):
     return params, on, off, ora
 
 
-@pytest.mark.parametrize("env_name,config,n,budgets,resample", [
-    ("MiniGrid-Empty-5x5", None, 4096, 3.2, False),          # goals reached early and often
-    ("MiniGrid-DoorKey-5x5", None, 4096, 3.2, False),
-    ("MiniGrid-Unlock", None, 2048, 2.2, False),             # the goal is rewritten per reset
-    ("XLand-MiniGrid-R1-9x9", "trivial", 8192, 3.1, False),  # ~27% of trials end by goal
-    ("XLand-MiniGrid-R4-13x13", "medium", 4096, 2.1, False),
-    ("XLand-MiniGrid-R4-13x13", "medium", 2048, 2.1, True),  # resample: the next task comes with the record
-    ("XLand-MiniGrid-R9-25x25", "high", 1024, 1.1, False),
+@pytest.mark.parametrize("env_name,config,n,budgets,resample,see", [
+    ("MiniGrid-Empty-5x5", None, 4096, 3.2, False, True),          # goals reached early and often
+    ("MiniGrid-DoorKey-5x5", None, 4096, 3.2, False, True),
+    ("MiniGrid-Unlock", None, 2048, 2.2, False, True),             # the goal is rewritten per reset
+    ("XLand-MiniGrid-R1-9x9", "trivial", 8192, 3.1, False, True),  # ~27% of trials end by goal
+    ("XLand-MiniGrid-R4-13x13", "medium", 4096, 2.1, False, True),
+    ("XLand-MiniGrid-R4-13x13", "medium", 2048, 2.1, True, True),  # resample: the next task comes with the record
+    ("XLand-MiniGrid-R4-13x13", "medium", 2048, 2.1, False, False),  # occluded: the record's first observation
+    ("XLand-MiniGrid-R9-25x25", "high", 1024, 1.1, False, True),
 ])
-def test_reset_ahead_matches_rebuild_and_oracle(env_name, config, n, budgets, resample):
+def test_reset_ahead_matches_rebuild_and_oracle(env_name, config, n, budgets, resample, see):
     from paper_2312_12044_b200 import key_from_seed, policy_keys, random_actions
-    params, on, off, ora = _pair(env_name, config, n, resample)
+    changes = {} if see else {"see_through_walls": False}
+    params, on, off, ora = _pair(env_name, config, n, resample, **changes)
     root = key_from_seed(21)
     a0, b0 = on.reset(root), off.reset(root)
     assert torch.equal(a0.observations, b0.observations)
@@ -119,10 +123,10 @@ def test_reset_ahead_across_rollouts_and_blocks():
 
 
 def test_reset_ahead_stage_lifecycle():
-    """Every env is queued once per trial at step count >= 1 + e mod
-    (budget - 2) (csrc/xmg_main.cuh prebuild_slot), so at the synchronized
-    budget end every env whose trial ran the whole budget holds a pre-built
-    trial (stage 2), and the new trials start at stage 0."""
+    """Every env's class (e mod classes) gets one batch in every cycle of
+    every * classes <= budget - 2 steps (xmg_ahead_plan), so at the
+    synchronized budget end every env whose trial ran the whole budget holds a
+    pre-built trial (stage 2), and the new trials start at stage 0."""
     from paper_2312_12044_b200 import key_from_seed, policy_keys, random_actions
     params, on, _, _ = _pair("XLand-MiniGrid-R4-13x13", "medium", 2048)
     on.reset(key_from_seed(1))
