@@ -45,6 +45,16 @@ constexpr uint32_t kQPut = 1u << 31, kQReset = 1u << 30, kQEnv = (1u << 30) - 1;
 // efficiency once per K steps, without touching the step_rare / step_main
 // overlap.
 constexpr uint64_t kStageReady = 2ull << 18, kStageMask = 3ull << 18;
+// Double-buffered grids: bit 20 of state word 0 says which of the two grid
+// buffers (state.grids = 0, state.next_grids = 1) holds the running trial;
+// a pre-build writes the other one, so the auto-reset that consumes it only
+// flips the bit (no grid copy).  Queue entries carry the bit in bit 30 (env
+// indices are < 2^30), so step_rare addresses the grid without the state word.
+constexpr uint64_t kBufBit = 1ull << 20;
+constexpr uint32_t kEntBuf = 1u << 30;
+__device__ __forceinline__ uint8_t* grid_ptr(const xmg_state& s, int64_t e, int HW, uint32_t buf) {
+  return (buf ? s.next_grids : s.grids) + e * (int64_t)HW;
+}
 __device__ __forceinline__ bool ahead_on(const xmg_state& s) { return s.next_grids != nullptr; }
 
 // capacity of one sub-queue: every env of the step_main CTAs (128 envs each)
@@ -218,13 +228,14 @@ __device__ __forceinline__ void warp_copy_cg(uint8_t* dst, const uint8_t* src, i
 #define XMG_CONSUME_INLINE __forceinline__  // inlined: fewer spills in step_main than a call
 #endif
 // The auto-resets of the envs in `cm` (lanes of the warp's 32-env chunk
-// starting at w0) from their pre-built records: state word and rng per lane,
-// then grid bytes and first observations (into the warp's observation stage)
-// copied by the whole warp, one contiguous run of envs at a time (a burst of
-// budget ends is one run of 32).
+// starting at w0) from their pre-built records: state word (whose buffer bit
+// now names the other grid buffer, where the pre-build put the new grid: no
+// grid copy) and rng per lane, then the first observations copied into the
+// warp's observation stage by the whole warp, one contiguous run of envs at a
+// time (a burst of budget ends is one run of 32).
 __device__ XMG_CONSUME_INLINE void consume_next(const xmg_state s, uint32_t cm, int64_t w0, int HW, int ob,
                                           uint8_t* obs_stage, int lane) {
-  __syncwarp();  // the lanes' own grid writes of this step precede the copy
+  __syncwarp();  // every lane is done with its rule row (the observation stage aliases it)
   if ((cm >> lane) & 1) {
     const ulonglong2* ns = reinterpret_cast<const ulonglong2*>(s.next_state) + 2 * (w0 + lane);
     const ulonglong2 a = __ldcg(ns), b = __ldcg(ns + 1);
@@ -236,7 +247,6 @@ __device__ XMG_CONSUME_INLINE void consume_next(const xmg_state s, uint32_t cm, 
     const uint32_t gap = ~m & ~((1u << a) - 1u);
     const int b = gap ? __ffs(gap) - 1 : 32;
     m = b < 32 ? m & (~0u << b) : 0u;
-    warp_copy_cg(s.grids + (w0 + a) * HW, s.next_grids + (w0 + a) * HW, (b - a) * HW, lane);
     if (obs_stage != nullptr) warp_copy_cg(obs_stage + a * ob, s.next_obs + (w0 + a) * ob, (b - a) * ob, lane);
   }
   __syncwarp();
@@ -268,7 +278,7 @@ __device__ __forceinline__ bool batch_rejected(const uint32_t* flag, uint32_t ep
 // thread's env, its action, the chunk wait done): window staging, action,
 // rules, goal, counters, queues, reset-ahead copies, statistics and the
 // observation.
-template <int MAXCH, bool FULL>
+template <int MAXCH>
 __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_state& s, const xmg_out& o,
                                                uint32_t epoch, int64_t n, int64_t tile, int tid, int lane, int warp,
                                                const MainGeo& geo, WView& vw, uint32_t* rbuf, uint8_t* obs_stage,
@@ -287,16 +297,18 @@ __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_
   uint32_t sc = (uint32_t)(ag.x >> 32);
   const uint32_t goal_word = (uint32_t)ag.y;
   const int task = (int)(ag.y >> 32);
+  const uint32_t buf = (uint32_t)(ag.x >> 20) & 1u;  // which grid buffer holds the running trial
+  vw.g = grid_ptr(s, valid ? e : 0, HW, buf);
 
   uint32_t qflags = 0;
   float rew = 0.f;
   bool last = false, consume = false;
-  const bool ahead = ahead_on(s);  // (the copy path costs ~1 us/step of steady state at C3: measured)
+  const bool ahead = ahead_on(s);  // (the consume path costs ~1 us/step of steady state at C3: measured)
   if (valid) {
     // ---- stage the post-action window (MOVE: both candidate poses) and,
     // for actions that can raise an event, the env's rule row
     const int nd = act == 1 ? ((dir + 3) & 3) : (act == 2 ? ((dir + 1) & 3) : dir);
-    if (!FULL) {
+    {
       int lo, hi;
       window_span(r, c, nd, act == 0 ? 1 : 0, act == 3 ? 1 : 0, H, W, V, lo, hi);
 #if XMG_L2HINT_GRID
@@ -376,9 +388,9 @@ __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_
     }
     if (!consume) {
 #if XMG_L2HINT
-      st_hint_u64(s.agent + 2 * e, pack_agent(r, c, dir | (stage << 2), pocket, sc), pol_keep);
+      st_hint_u64(s.agent + 2 * e, pack_agent(r, c, dir | (stage << 2) | (int)(buf << 4), pocket, sc), pol_keep);
 #else
-      s.agent[2 * e] = pack_agent(r, c, dir | (stage << 2), pocket, sc);
+      s.agent[2 * e] = pack_agent(r, c, dir | (stage << 2) | (int)(buf << 4), pocket, sc);
 #endif
     }
   }
@@ -403,7 +415,8 @@ __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_
       base = __shfl_sync(0xffffffffu, base, leader);
       if (qflags == want) {
         XMG_ASSERT(base + __popc(km & ((1u << lane) - 1)) < queue_cap(n));
-        s.work[queue_base(n, epoch, kind, k) + base + __popc(km & ((1u << lane) - 1))] = (uint32_t)e;
+        s.work[queue_base(n, epoch, kind, k) + base + __popc(km & ((1u << lane) - 1))] =
+            (uint32_t)e | (buf << 30);
       }
     }
   }
@@ -452,9 +465,7 @@ __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_
   }
 }
 
-// FULL: small grids are staged whole, issued before the state word arrives
-// (one DRAM round trip per env instead of two: state word -> view window).
-template <int MAXCH, bool FULL>
+template <int MAXCH>
 __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_desc d, const xmg_state s,
                                                                 const xmg_out o, const void* actions, int act_dtype,
                                                                 const uint32_t* abort_flag, uint32_t epoch,
@@ -477,12 +488,10 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
 
   uint8_t* rb_base = smem + kThreads * geo.stg;
   uint8_t* obs_stage = rb_base + warp * 32 * geo.rb;  // aliases the warp's rule rows
-  WView vw;
-  vw.g = s.grids + (valid ? e : 0) * (int64_t)HW;
+  WView vw;  // (its grid pointer is set from the state word: the env's current buffer)
   vw.stage = smem + tid * geo.stg;
   vw.sbase = vw.slo = vw.shi = 0;
   uint32_t* rbuf = reinterpret_cast<uint32_t*>(rb_base + tid * geo.rb);
-  if (FULL && valid) stage_issue<MAXCH>(vw, 0, HW, HW);
 
   // ---- load: the 16-byte state word and the action
   ulonglong2 ag = make_ulonglong2(0, 0);
@@ -520,10 +529,7 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
   // lets this grid launch); this step appends to the other parity
   if (blockIdx.x == 0)
     for (int i = tid; i < 2 * kQueues; i += blockDim.x) s.work[count_index(epoch + 1, 0, 0) + i] = 0;
-  if (batch_rejected(abort_flag, epoch)) {
-    if (FULL) cp_async_wait_all();  // no copy may still target shared memory at exit
-    return;
-  }
+  if (batch_rejected(abort_flag, epoch)) return;
   if (was_dirty == epoch - 1 && e0 + warp * 32 < n) {
     // the previous step queued envs of this chunk: wait until its step_rare has
     // released them all, then reload the state word it may have rewritten
@@ -537,11 +543,8 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
     }
     __syncwarp();
     if (valid) ag = ld_cg_u64x2(reinterpret_cast<const ulonglong2*>(s.agent) + e);
-    if (FULL && valid) {  // the early grid copy may predate step_rare's writes
-      cp_async_wait_all();
-      stage_issue<MAXCH>(vw, 0, HW, HW);
-    }
-  }  main_tile_body<MAXCH, FULL>(d, s, o, epoch, n, tile, tid, lane, warp, geo, vw, rbuf, obs_stage, ag, act,
+  }
+  main_tile_body<MAXCH>(d, s, o, epoch, n, tile, tid, lane, warp, geo, vw, rbuf, obs_stage, ag, act,
 #if XMG_L2HINT
                               pol_keep, pol_stream);
 #else

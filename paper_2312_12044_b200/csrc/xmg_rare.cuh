@@ -273,20 +273,22 @@ __host__ __device__ inline RareGeo make_rare_geo(int H, int W, int R) {
 }
 
 // Rebuild env e's trial (ref:vecenv.py:359-361 -> :224-291), whole warp.
-// pre (reset-ahead): the same build from the same keys, written to the
-// env's next_* records (grid, state word, rng, first observation) for the
-// auto-reset that will end the running trial; nothing of the running trial
-// is touched.
+// The grid goes to the env's current buffer `buf` (xmg_main.cuh kBufBit),
+// which the new state word keeps.  pre (reset-ahead): the same build from the
+// same keys, written to the OTHER buffer and to the env's next_* records
+// (state word naming that buffer, rng, first observation) for the auto-reset
+// that will end the running trial; nothing of the running trial is touched.
 __device__ __forceinline__ void warp_reset_env(const xmg_env_desc& d, const xmg_env_desc* sd, const xmg_state& s,
                                                const xmg_out& o, uint8_t* wbase, const RareGeo& geo, int lane,
                                                int64_t e, const TrialKeys* key, int task, bool reset_mode,
-                                               ResetOut* rs, bool pre = false) {
+                                               ResetOut* rs, bool pre = false, uint32_t buf = 0) {
   const int H = d.height, W = d.width, HW = H * W, V = d.view_size, ob = 2 * V * V;
   const WarpScratch ws = make_scratch(wbase, geo.hwp);
   const uint32_t g_in = d.scenario == XMG_SCENARIO_XLAND ? d.task_rows[(int64_t)task * d.row_words] : 0u;
-  warp_build(sd, wbase, geo.hwp, lane, key, task, g_in, (pre ? s.next_grids : s.grids) + e * (int64_t)HW, rs);
+  const uint32_t dst_buf = pre ? buf ^ 1u : buf;
+  warp_build(sd, wbase, geo.hwp, lane, key, task, g_in, grid_ptr(s, e, HW, dst_buf), rs);
   const ResetOut ro = *rs;
-  const ulonglong2 word = make_ulonglong2(pack_agent(ro.r, ro.c, ro.d, 0, 0),
+  const ulonglong2 word = make_ulonglong2(pack_agent(ro.r, ro.c, ro.d | (int)(dst_buf << 4), 0, 0),
                                           (uint64_t)ro.goal | ((uint64_t)(uint32_t)ro.task << 32));
   if (lane == 0) {
     if (pre) {
@@ -314,7 +316,8 @@ __device__ __forceinline__ void warp_reset_env(const xmg_env_desc& d, const xmg_
 __device__ __forceinline__ void warp_reset_group(const xmg_env_desc& d, const xmg_env_desc* sd, const xmg_state& s,
                                                  const xmg_out& o, uint8_t* wbase, const RareGeo& geo,
                                                  TrialKeys* keys, int lane, bool mine, int64_t e,
-                                                 const uint64_t* reset_keys, int gw = 0, bool pre = false) {
+                                                 const uint64_t* reset_keys, int gw = 0, bool pre = false,
+                                                 uint32_t buf = 0) {
   const bool resample = d.resample_tasks && d.scenario == XMG_SCENARIO_XLAND;
   int task = 0;
   ulonglong2 ek = make_ulonglong2(0, 0);
@@ -337,8 +340,9 @@ __device__ __forceinline__ void warp_reset_group(const xmg_env_desc& d, const xm
       const int64_t es = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)e, src);
       const int ts = __shfl_sync(0xffffffffu, task, src);
       const bool ps = __shfl_sync(0xffffffffu, (int)pre, src) != 0;
+      const uint32_t bs = __shfl_sync(0xffffffffu, buf, src);
       warp_reset_env(d, sd, s, o, wbase, geo, lane, es, keys + (src - half), ts, reset_keys != nullptr,
-                     reinterpret_cast<ResetOut*>(make_scratch(wbase, geo.hwp).misc + 40), ps);
+                     reinterpret_cast<ResetOut*>(make_scratch(wbase, geo.hwp).misc + 40), ps, bs);
     }
   }
 }
@@ -437,10 +441,13 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRar
       const int64_t it = i0 + (int64_t)lane * put_w;
       const bool mine = lane < kPutBatch && it < cnt_put;
       int64_t e_l = 0;
+      uint32_t buf_l = 0;
       int off_l = 0;
       if (mine) {
-        e_l = qp[it];
-        const uintptr_t g0 = reinterpret_cast<uintptr_t>(s.grids + e_l * (int64_t)HW);
+        const uint32_t ent = qp[it];
+        e_l = (int64_t)(ent & kQEnv);
+        buf_l = (ent >> 30) & 1u;
+        const uintptr_t g0 = reinterpret_cast<uintptr_t>(grid_ptr(s, e_l, HW, buf_l));
         const uintptr_t a0 = g0 & ~uintptr_t(15);
         off_l = (int)(g0 - a0);
         const int nch = (off_l + HW + 15) >> 4;
@@ -469,7 +476,8 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRar
         const uint32_t* rt = pr + src * (geo.rbw / 4);
         const int nr = R > 0 ? (int)(rt[1] & 0xff) : 0;
         uint8_t* G = pg + src * geo.pgb + off;
-        const int res = warp_put_env(G, s.grids + e * (int64_t)HW, pc, lane, H, W, r, c, rt + kRowHeader, nr,
+        const uint32_t bs = __shfl_sync(0xffffffffu, buf_l, src);
+        const int res = warp_put_env(G, grid_ptr(s, e, HW, bs), pc, lane, H, W, r, c, rt + kRowHeader, nr,
                                      (uint32_t)ag.y);
         const bool last = (res & 1) || sc >= (uint32_t)d.budget;
 #ifdef XMG_TRACE
@@ -509,8 +517,9 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRar
           lastm &= lastm - 1;
           const int64_t es = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)e_l, src);
           const int ts = (int)(pa[src].y >> 32);
+          const uint32_t bs = __shfl_sync(0xffffffffu, buf_l, src);
           warp_reset_env(d, sdesc, s, o, wbase, geo, lane, es, keys + src, ts, false,
-                         reinterpret_cast<ResetOut*>(ws.misc + 40));
+                         reinterpret_cast<ResetOut*>(ws.misc + 40), false, bs);
         }
       }
       if (track) release_envs(s.work + pending_base(n), mine, e_l);
@@ -526,8 +535,9 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRar
     for (int64_t i0 = jr; i0 < cnt_reset; i0 += 32 * (int64_t)rs_w) {
       const int64_t i = i0 + (int64_t)lane * rs_w;
       const bool mine = i < cnt_reset;
-      const int64_t e = mine ? (int64_t)qp[i] : 0;
-      warp_reset_group(d, sdesc, s, o, wbase, geo, keys, lane, mine, e, nullptr, gw);
+      const uint32_t ent = mine ? qp[i] : 0u;
+      const int64_t e = (int64_t)(ent & kQEnv);
+      warp_reset_group(d, sdesc, s, o, wbase, geo, keys, lane, mine, e, nullptr, gw, false, (ent >> 30) & 1u);
       if (track) release_envs(s.work + pending_base(n), mine, e);
     }
   }
@@ -593,7 +603,8 @@ __global__ void __launch_bounds__(kPreWarps * 32, XMG_PRE_MINB * 4 / kPreWarps)
       w0 = s.agent[2 * e];
       need = (w0 & kStageMask) == 0;
     }
-    warp_reset_group(d, sdesc, s, none, wbase, geo, keys, lane, need, e, nullptr, 0, true);
+    warp_reset_group(d, sdesc, s, none, wbase, geo, keys, lane, need, e, nullptr, 0, true,
+                     (uint32_t)(w0 >> 20) & 1u);
     if (need) s.agent[2 * e] = w0 | kStageReady;
   }
   // the last CTA re-arms the counter for the next batch

@@ -64,23 +64,56 @@ __device__ XMG_ROLL_POLICY_INLINE uint32_t policy_block(uint64_t kh, uint64_t kl
          ((uint32_t)(w.w3 % 6) << 24);
 }
 
+// A warp-wide copy with plain loads (either side may be shared memory).
+__device__ __forceinline__ void roll_copy(uint8_t* dst, const uint8_t* src, int nbytes, int lane) {
+  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    for (int i = lane; i < (nbytes >> 4); i += 32)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    for (int i = (nbytes & ~15) + lane; i < nbytes; i += 32) dst[i] = src[i];
+  } else {
+    for (int i = lane; i < nbytes; i += 32) dst[i] = src[i];
+  }
+}
+
+// The warp's grids between HBM and shared memory.  Each env's grid lives in
+// the buffer its state word's bit 20 names (bm: the lanes in buffer 1); runs
+// of consecutive lanes in one buffer are contiguous on both sides, so a warp
+// whose envs share a buffer moves its grids in one run.
+__device__ __forceinline__ void roll_grids_io(const xmg_state& s, int64_t e0, uint32_t vm, uint32_t bm, int HW,
+                                              uint8_t* grids, bool to_hbm, int lane) {
+  for (uint32_t pass = 0; pass < 2; ++pass) {
+    for (uint32_t m = (pass ? bm : ~bm) & vm; m;) {
+      const int a = __ffs(m) - 1;
+      const uint32_t gap = ~m & ~((1u << a) - 1u);
+      const int b = gap ? __ffs(gap) - 1 : 32;
+      m = b < 32 ? m & (~0u << b) : 0u;
+      uint8_t* g = grid_ptr(s, e0 + a, HW, pass);
+      if (to_hbm) roll_copy(g, grids + a * HW, (b - a) * HW, lane);
+      else roll_copy(grids + a * HW, g, (b - a) * HW, lane);
+    }
+  }
+}
+
 // The auto-resets of the lanes in cm from their pre-built records: the grid
-// bytes into the warp's shared grids (runs of consecutive lanes are
-// contiguous in both), and each lane's next state words returned.
-__device__ __noinline__ ulonglong4 roll_consume(const xmg_state s, uint32_t cm, int64_t e0, int HW, uint8_t* grids,
-                                                int lane) {
+// bytes (in the other buffer, bm: the lanes whose current grid is in buffer 1)
+// into the warp's shared grids, and each lane's next state words returned.
+// The lane's buffer bit flips with it (the caller's write-back goes there).
+__device__ __noinline__ ulonglong4 roll_consume(const xmg_state s, uint32_t cm, uint32_t bm, int64_t e0, int HW,
+                                                uint8_t* grids, int lane) {
   ulonglong4 out = make_ulonglong4(0, 0, 0, 0);
   if ((cm >> lane) & 1) {
     const ulonglong2* ns = reinterpret_cast<const ulonglong2*>(s.next_state) + 2 * (e0 + lane);
     const ulonglong2 w = __ldcg(ns), k = __ldcg(ns + 1);
     out = make_ulonglong4(w.x, w.y, k.x, k.y);
   }
-  for (uint32_t m = cm; m;) {
-    const int a = __ffs(m) - 1;
-    const uint32_t gap = ~m & ~((1u << a) - 1u);
-    const int b = gap ? __ffs(gap) - 1 : 32;
-    m = b < 32 ? m & (~0u << b) : 0u;
-    warp_copy_cg(grids + a * HW, s.next_grids + (e0 + a) * HW, (b - a) * HW, lane);
+  for (uint32_t pass = 0; pass < 2; ++pass) {  // records of buffer-0 envs are in buffer 1, and back
+    for (uint32_t m = cm & (pass ? bm : ~bm); m;) {
+      const int a = __ffs(m) - 1;
+      const uint32_t gap = ~m & ~((1u << a) - 1u);
+      const int b = gap ? __ffs(gap) - 1 : 32;
+      m = b < 32 ? m & (~0u << b) : 0u;
+      warp_copy_cg(grids + a * HW, grid_ptr(s, e0 + a, HW, pass ^ 1u), (b - a) * HW, lane);
+    }
   }
   __syncwarp();
   return out;
@@ -152,24 +185,16 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
   const bool see = d.see_through_walls != 0;
   if (lane == 0) *sdesc = d;
 
-  // ---- state in: the 32 grids (contiguous in HBM), state words, rng keys
-  {
-    const uint8_t* src = s.grids + e0 * (int64_t)HW;
-    const int bytes = nvalid * HW;
-    if (((reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
-      for (int i = lane; i < (bytes >> 4); i += 32)
-        reinterpret_cast<uint4*>(grids)[i] = reinterpret_cast<const uint4*>(src)[i];
-      for (int i = (bytes & ~15) + lane; i < bytes; i += 32) grids[i] = src[i];
-    } else {
-      for (int i = lane; i < bytes; i += 32) grids[i] = src[i];
-    }
-  }
+  // ---- state in: state words and rng keys, then the grids (in the buffers the words name)
   ulonglong2 ag = make_ulonglong2(0, 0), rk = make_ulonglong2(0, 0), pk = make_ulonglong2(0, 0);
   if (valid) {
     ag = reinterpret_cast<const ulonglong2*>(s.agent)[e];
     rk = reinterpret_cast<const ulonglong2*>(s.rng)[e];
     if (pkeys) pk = reinterpret_cast<const ulonglong2*>(pkeys)[e];
   }
+  const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+  uint32_t buf = (uint32_t)(ag.x >> 20) & 1u;
+  roll_grids_io(s, e0, vmask, __ballot_sync(0xffffffffu, buf != 0), HW, grids, false, lane);
   int r = (int)(ag.x & 0xff), c = (int)((ag.x >> 8) & 0xff), dir = (int)((ag.x >> 16) & 3);
   int pocket = (int)((ag.x >> 24) & 0xff);
   uint32_t sc = (uint32_t)(ag.x >> 32);
@@ -286,8 +311,9 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
       // loop's code small), state into the lane's registers
       const uint32_t cm = __ballot_sync(0xffffffffu, last && stage == 2);
       if (cm) {
-        const ulonglong4 w = roll_consume(s, cm, e0, HW, grids, lane);
+        const ulonglong4 w = roll_consume(s, cm, __ballot_sync(0xffffffffu, buf != 0), e0, HW, grids, lane);
         if ((cm >> lane) & 1) {
+          buf ^= 1u;
           r = (int)(w.x & 0xff);
           c = (int)((w.x >> 8) & 0xff);
           dir = (int)((w.x >> 16) & 3);
@@ -365,20 +391,10 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
 
   // ---- state out
   __syncwarp();
-  {
-    uint8_t* dst = s.grids + e0 * (int64_t)HW;
-    const int bytes = nvalid * HW;
-    if (((reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
-      for (int i = lane; i < (bytes >> 4); i += 32)
-        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(grids)[i];
-      for (int i = (bytes & ~15) + lane; i < bytes; i += 32) dst[i] = grids[i];
-    } else {
-      for (int i = lane; i < bytes; i += 32) dst[i] = grids[i];
-    }
-  }
+  roll_grids_io(s, e0, vmask, __ballot_sync(0xffffffffu, buf != 0), HW, grids, true, lane);
   if (valid) {
     reinterpret_cast<ulonglong2*>(s.agent)[e] =
-        make_ulonglong2(pack_agent(r, c, dir | (stage << 2), pocket, sc),
+        make_ulonglong2(pack_agent(r, c, dir | (stage << 2) | (int)(buf << 4), pocket, sc),
                         (uint64_t)goal_word | ((uint64_t)(uint32_t)task << 32));
     reinterpret_cast<ulonglong2*>(s.rng)[e] = rk;
   }

@@ -217,11 +217,9 @@ int device_attrs(int dev) {
   DevInfo& di = g_dev[dev];
   if (!di.done) {
     cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
-    set_attr(di, step_main<6, false>, "step_main") && set_attr(di, step_main<8, false>, "step_main") &&
-        set_attr(di, step_main<12, false>, "step_main") && set_attr(di, step_main<16, false>, "step_main") &&
-        set_attr(di, step_main<32, false>, "step_main") && set_attr(di, step_main<6, true>, "step_main") &&
-        set_attr(di, step_main<8, true>, "step_main") && set_attr(di, step_main<12, true>, "step_main") &&
-
+    set_attr(di, step_main<6>, "step_main") && set_attr(di, step_main<8>, "step_main") &&
+        set_attr(di, step_main<12>, "step_main") && set_attr(di, step_main<16>, "step_main") &&
+        set_attr(di, step_main<32>, "step_main") &&
         set_attr(di, step_rare, "step_rare") && set_attr(di, prebuild_kernel, "prebuild_kernel") &&
         set_attr(di, rollout_kernel, "rollout_kernel");
     di.done = true;
@@ -252,7 +250,7 @@ bool pdl_enabled() {
   return on == 1;
 }
 
-template <int MAXCH, bool FULL>
+template <int MAXCH>
 int launch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
                 const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st, bool pdl) {
   const MainGeo geo = make_main_geo(d->view_size, MAXCH, d->rule_width);
@@ -270,7 +268,7 @@ int launch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, con
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t err = cudaLaunchKernelEx(&cfg, step_main<MAXCH, FULL>, *d, *s, *o, actions, dtype, flag, epoch, n);
+  const cudaError_t err = cudaLaunchKernelEx(&cfg, step_main<MAXCH>, *d, *s, *o, actions, dtype, flag, epoch, n);
   if (err != cudaSuccess) return fail(std::string("step_main: ") + cudaGetErrorString(err));
   return check_launch("step_main");
 }
@@ -343,34 +341,14 @@ int validate_desc(const xmg_env_desc* d, const xmg_state* s, int64_t n) {
   return 0;
 }
 
-// whole-grid staging: 16-byte chunks of a grid at any alignment
-inline int full_chunks(int hw) { return (hw + 30) / 16; }
-
-bool use_full(const xmg_env_desc* d) {
-  static int mode = -1;  // XMG_STAGE=full (<= 12 chunks) | window (default: measured faster at C3)
-  if (mode < 0) {
-    const char* m = getenv("XMG_STAGE");
-    mode = (m && !strcmp(m, "full")) ? 1 : 0;
-  }
-  return mode == 1 && full_chunks(d->height * d->width) <= 12;
-}
-
 int dispatch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
                   const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st, bool pdl = true) {
-
-
-  if (use_full(d)) {
-    const int fc = full_chunks(d->height * d->width);
-    if (fc <= 6) return launch_main<6, true>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
-    if (fc <= 8) return launch_main<8, true>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
-    return launch_main<12, true>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
-  }
   switch (pick_maxch(d)) {
-    case 6: return launch_main<6, false>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
-    case 8: return launch_main<8, false>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
-    case 12: return launch_main<12, false>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
-    case 16: return launch_main<16, false>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
-    default: return launch_main<32, false>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
+    case 6: return launch_main<6>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
+    case 8: return launch_main<8>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
+    case 12: return launch_main<12>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
+    case 16: return launch_main<16>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
+    default: return launch_main<32>(d, s, o, actions, dtype, flag, epoch, n, st, pdl);
   }
 }
 

@@ -39,6 +39,8 @@ from .ruleset import Benchmark, Ruleset, TaskTable, pack_rulesets
 
 GRID_PAD = 64  # the step kernel reads 16-byte aligned chunks past the last grid
 STAGE_BITS = 3 << 18  # reset-ahead stage in state word 0 (include/xmg.h)
+BUF_BIT = 1 << 20  # the grid buffer holding the env's grid (0: grids, 1: next_grids)
+META_BITS = STAGE_BITS | BUF_BIT
 
 
 _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
@@ -333,9 +335,32 @@ class VecEnv:
             self._gchecked = 0
 
     # -- views
+    def _grid_buffers(self):
+        n, hw = self.num_envs, self._hw
+        g0 = self.grids_flat[: n * hw].view(n, hw)
+        g1 = None if self._next_grids is None else self._next_grids[: n * hw].view(n, hw)
+        return g0, g1
+
     @property
     def grids(self) -> torch.Tensor:
-        return self.grids_flat[: self.num_envs * self._hw].view(self.num_envs, self._hw)
+        """(N, H*W) u8 cells of every env.  With reset-ahead each env's grid
+        lives in one of two buffers (bit 20 of its state word; a pre-built
+        trial is written to the other one and taken over by flipping the bit):
+        this gathers them into a new tensor (write cells with set_grid)."""
+        g0, g1 = self._grid_buffers()
+        if g1 is None:
+            return g0
+        buf = ((self.agent[:, 0] >> 20) & 1).bool()
+        return torch.where(buf[:, None], g1, g0)
+
+    def set_grid(self, i: int, cells) -> None:
+        """Overwrite env i's cells (in the buffer its state word names)."""
+        g0, g1 = self._grid_buffers()
+        cells = torch.as_tensor(cells, dtype=torch.uint8).to(self.device)
+        if g1 is not None and int(self.agent[i, 0].item()) & BUF_BIT:
+            g1[i] = cells
+        else:
+            g0[i] = cells
 
     def agent_fields(self) -> torch.Tensor:
         """(N, 5) int64: row, col, dir, pocket, step_count."""
@@ -344,11 +369,11 @@ class VecEnv:
                             (a >> 32) & 0xFFFFFFFF], dim=1)
 
     def state_words(self) -> torch.Tensor:
-        """(N, 2) state words without the reset-ahead stage bits (18-19 of
-        word 0: scheduling metadata, not env state): the env state proper,
-        comparable across step / steps / rollout paths."""
+        """(N, 2) state words without the reset-ahead bits (stage, 18-19 of
+        word 0, and the grid buffer, 20: scheduling metadata, not env state):
+        the env state proper, comparable across step / steps / rollout paths."""
         a = self.agent.clone()
-        a[:, 0] &= ~STAGE_BITS
+        a[:, 0] &= ~META_BITS
         return a
 
     @property

@@ -199,6 +199,6 @@ def test_resample_on_reset_uses_sample_ruleset():
     ref = VecEnv(params, n, bm, task_ids=want)
     rts = ref.reset_with_keys(ek[:, 0], ek[:, 1])
     np.testing.assert_array_equal(vec.grids.cpu().numpy()[last], ref.grids.cpu().numpy()[last])
-    np.testing.assert_array_equal(vec.agent.cpu().numpy()[last], ref.agent.cpu().numpy()[last])
+    np.testing.assert_array_equal(vec.state_words().cpu().numpy()[last], ref.state_words().cpu().numpy()[last])
     np.testing.assert_array_equal(vec.rng.cpu().numpy()[last], ref.rng.cpu().numpy()[last])
     np.testing.assert_array_equal(ts.observations.cpu().numpy()[last], rts.observations.cpu().numpy()[last])

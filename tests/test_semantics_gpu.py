@@ -34,10 +34,10 @@ def _merge_env(max_steps):
             cells[j * 6 + i] = WALL
     cells[3 * 6 + 1] = a  # purple square, west of the agent
     cells[1 * 6 + 3] = b  # yellow square, by the north wall
-    vec.grids[0] = torch.from_numpy(cells).cuda()
     goal = rs.goal[0] | (rs.goal[1] << 8) | (rs.goal[2] << 16) | (rs.goal[3] << 24)
     word = np.array([_pack(3, 2, 3), goal], np.uint64).view(np.int64)  # (3, 2) facing LEFT, task 0
     vec.agent[0] = torch.from_numpy(word).cuda()
+    vec.set_grid(0, cells)
     return vec, a, b, out
 
 
