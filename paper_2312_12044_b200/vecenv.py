@@ -353,14 +353,14 @@ class VecEnv:
         buf = ((self.agent[:, 0] >> 20) & 1).bool()
         return torch.where(buf[:, None], g1, g0)
 
+    def _live_grid(self, i: int) -> torch.Tensor:
+        """View of env i's cells in the buffer its state word names."""
+        g0, g1 = self._grid_buffers()
+        return g1[i] if g1 is not None and int(self.agent[i, 0].item()) & BUF_BIT else g0[i]
+
     def set_grid(self, i: int, cells) -> None:
         """Overwrite env i's cells (in the buffer its state word names)."""
-        g0, g1 = self._grid_buffers()
-        cells = torch.as_tensor(cells, dtype=torch.uint8).to(self.device)
-        if g1 is not None and int(self.agent[i, 0].item()) & BUF_BIT:
-            g1[i] = cells
-        else:
-            g0[i] = cells
+        self._live_grid(i).copy_(torch.as_tensor(cells, dtype=torch.uint8).to(self.device))
 
     def agent_fields(self) -> torch.Tensor:
         """(N, 5) int64: row, col, dir, pocket, step_count."""
@@ -728,7 +728,7 @@ class VecEnv:
 
     def env_state(self, i: int) -> EnvState:
         """The i-th env as a scalar EnvState (ref vecenv.py:511-521)."""
-        g = self.grids[i].cpu().numpy().tobytes()
+        g = self._live_grid(i).cpu().numpy().tobytes()
         a = int(self.agent[i, 0].item()) & ((1 << 64) - 1)
         k = self.rng[i].cpu().numpy().view(np.uint64)
         agent = AgentState(Position(a & 0xFF, (a >> 8) & 0xFF), Direction((a >> 16) & 3), (a >> 24) & 0xFF)
