@@ -196,6 +196,18 @@ struct WView : View {
   }
 };
 
+// four signed bytes packed into a word (byte k = v_k), and the replication
+// factor that copies a VV-bit group into all VV row groups of a VV*VV mask
+__host__ __device__ constexpr uint32_t sbytes4(int a, int b, int c, int d) {
+  return (uint32_t)(a & 0xff) | ((uint32_t)(b & 0xff) << 8) | ((uint32_t)(c & 0xff) << 16) |
+         ((uint32_t)(d & 0xff) << 24);
+}
+__host__ __device__ constexpr uint32_t rep_groups(int vv) {
+  uint32_t m = 0;
+  for (int i = 0; i < vv; ++i) m |= 1u << (i * vv);
+  return m;
+}
+
 // Stage grid bytes [lo, hi) of this thread's env with 16-byte cp.async
 // chunks (aligned on the global address; the grid buffer is padded).
 template <int MAXCH>
@@ -324,22 +336,44 @@ __device__ __forceinline__ void obs_see(const uint8_t* stage, int sbase, uint8_t
   const int V = VV ? VV : Vrt;
   const int h = V / 2;
   // origin (view cell (0, 0)) and the world steps of i (rows) and j
-  // (columns), select-based (lanes facing different ways stay converged)
-  const bool d0 = d == 0, d1 = d == 1, d2 = d == 2;
-  const int r0 = d0 ? r - (V - 1) : d2 ? r + (V - 1) : d1 ? r - h : r + h;
-  const int c0 = d0 ? c - h : d2 ? c + h : d1 ? c + (V - 1) : c - (V - 1);
-  const int dri = d0 ? 1 : d2 ? -1 : 0, dci = d1 ? -1 : (d0 || d2) ? 0 : 1;
-  const int drj = d1 ? 1 : (d0 || d2) ? 0 : -1, dcj = d0 ? 1 : d2 ? -1 : 0;
-  // the facing makes i move along one world axis and j along the other:
-  // validity is a product of a bit range over i and one over j
-  auto range_mask = [V](int b, int st, int lim) {  // t in [0, V) with 0 <= b + t*st < lim
-    int lo = st > 0 ? -b : b - lim + 1, hi = st > 0 ? lim - b : b + 1;
+  // (columns).  The j step is (-dci, dri): the view's columns run to the
+  // agent's right.
+  int r0, c0, dri, dci;
+  if constexpr (VV != 0) {
+    // per-facing constants as signed bytes (facing d in byte d), picked with
+    // one sign-extending byte permute each (lanes facing different ways stay
+    // converged, no select chains)
+    constexpr int F = VV - 1, HH = VV / 2;
+    constexpr uint32_t kR0 = sbytes4(-F, -HH, F, HH), kC0 = sbytes4(-HH, F, HH, -F);
+    constexpr uint32_t kRI = sbytes4(1, 0, -1, 0), kCI = sbytes4(0, -1, 0, 1);
+    const uint32_t sel = (uint32_t)d * 0x1111u + 0x8880u;
+    r0 = r + (int)__byte_perm(kR0, 0, sel);
+    c0 = c + (int)__byte_perm(kC0, 0, sel);
+    dri = (int)__byte_perm(kRI, 0, sel);
+    dci = (int)__byte_perm(kCI, 0, sel);
+  } else {
+    const bool d0 = d == 0, d1 = d == 1, d2 = d == 2;
+    r0 = d0 ? r - (V - 1) : d2 ? r + (V - 1) : d1 ? r - h : r + h;
+    c0 = d0 ? c - h : d2 ? c + h : d1 ? c + (V - 1) : c - (V - 1);
+    dri = d0 ? 1 : d2 ? -1 : 0;
+    dci = d1 ? -1 : (d0 || d2) ? 0 : 1;
+  }
+  const int drj = -dci, dcj = dri;
+  // the facing makes i move along one world axis and j along the other
+  // (i along rows iff the facing is vertical): validity is a product of a
+  // range [lo, hi) over i and one over j
+  const bool vert = (d & 1) == 0;
+  auto range = [V](int b, int st, int lim, int& lo, int& hi) {  // t in [0, V) with 0 <= b + t*st < lim
+    lo = st > 0 ? -b : b - lim + 1;
+    hi = st > 0 ? lim - b : b + 1;
     lo = max(lo, 0);
     hi = min(hi, V);
-    return hi > lo ? ((1u << hi) - 1u) & ~((1u << lo) - 1u) : 0u;
   };
-  const uint32_t mi = dri ? range_mask(r0, dri, H) : range_mask(c0, dci, W);
-  const uint32_t mj = drj ? range_mask(r0, drj, H) : range_mask(c0, dcj, W);
+  int loi, hii, loj, hij;
+  range(vert ? r0 : c0, vert ? dri : dci, vert ? H : W, loi, hii);
+  range(vert ? c0 : r0, vert ? dcj : drj, vert ? W : H, loj, hij);
+  const uint32_t mi = hii > loi ? ((1u << hii) - 1u) & ~((1u << loi) - 1u) : 0u;
+  const uint32_t mj = hij > loj ? ((1u << hij) - 1u) & ~((1u << loj) - 1u) : 0u;
   const int di = dri * W + dci, dj = drj * W + dcj;  // flat steps
   const uint8_t* p0 = stage - sbase + (r0 * W + c0);
   // (tile, color) byte pairs as 16-bit values; written as one u16 plus
@@ -353,9 +387,13 @@ __device__ __forceinline__ void obs_see(const uint8_t* stage, int sbase, uint8_t
 #pragma unroll
     for (int j = 0; j < VV; ++j) jo[j] = j * dj;
     static_assert(VV * VV <= 32, "the cell mask is one 32-bit word");
-    uint32_t m25 = 0;  // validity of every view cell: bit i*VV + j = mi bit i and mj bit j
-#pragma unroll
-    for (int i = 0; i < VV; ++i) m25 |= (((mi >> i) & 1u) ? mj : 0u) << (i * VV);
+    // validity of every view cell: bit i*VV + j = mi bit i and mj bit j —
+    // mj copied into every row group by one multiply, the rows [loi, hii) as
+    // one bit range
+    constexpr uint32_t kRep = rep_groups(VV);
+    const uint32_t rows = hii > loi ? ((1u << (VV * hii)) - 1u) & ~((1u << (VV * loi)) - 1u) : 0u;
+    const uint32_t m25 = rows & (mj * kRep);
+    (void)mi;
     const uint8_t* pi = p0;
 #pragma unroll
     for (int i = 0; i < VV; ++i) {
