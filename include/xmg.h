@@ -289,7 +289,7 @@ int32_t xmg_image_atlas(int32_t view, const uint8_t* atlas, uint8_t* aligned, vo
 int32_t xmg_image_obs_aligned(const uint8_t* obs /*[n][v][v][2]*/, int64_t n, int32_t view, const uint8_t* aligned,
                               uint8_t* out /*[n][224][224][3]*/, void* stream);
 
-/* Size in u32 words of xmg_state.work for n envs. */
+/* Size in u32 words of xmg_state.work for n envs (-1 unless 0 <= n < 2^30). */
 int64_t xmg_work_words(int64_t n);
 
 /* Bytes of dynamic shared memory per 128-env CTA the step/reset kernels use

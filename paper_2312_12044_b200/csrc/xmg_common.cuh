@@ -202,6 +202,14 @@ __host__ __device__ constexpr uint32_t sbytes4(int a, int b, int c, int d) {
   return (uint32_t)(a & 0xff) | ((uint32_t)(b & 0xff) << 8) | ((uint32_t)(c & 0xff) << 16) |
          ((uint32_t)(d & 0xff) << 24);
 }
+// byte (sel & 7) of k, sign-extended: prmt with the sign-replicate bit set
+// in the upper three selectors (sel = d * 0x1111 + 0x8880 picks byte d).  PTX
+// directly: the __byte_perm intrinsic takes 3-bit selectors only.
+__device__ __forceinline__ int sbyte_of(uint32_t k, uint32_t sel) {
+  uint32_t v;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(v) : "r"(k), "r"(sel));
+  return (int)v;
+}
 __host__ __device__ constexpr uint32_t rep_groups(int vv) {
   uint32_t m = 0;
   for (int i = 0; i < vv; ++i) m |= 1u << (i * vv);
@@ -347,10 +355,10 @@ __device__ __forceinline__ void obs_see(const uint8_t* stage, int sbase, uint8_t
     constexpr uint32_t kR0 = sbytes4(-F, -HH, F, HH), kC0 = sbytes4(-HH, F, HH, -F);
     constexpr uint32_t kRI = sbytes4(1, 0, -1, 0), kCI = sbytes4(0, -1, 0, 1);
     const uint32_t sel = (uint32_t)d * 0x1111u + 0x8880u;
-    r0 = r + (int)__byte_perm(kR0, 0, sel);
-    c0 = c + (int)__byte_perm(kC0, 0, sel);
-    dri = (int)__byte_perm(kRI, 0, sel);
-    dci = (int)__byte_perm(kCI, 0, sel);
+    r0 = r + sbyte_of(kR0, sel);
+    c0 = c + sbyte_of(kC0, sel);
+    dri = sbyte_of(kRI, sel);
+    dci = sbyte_of(kCI, sel);
   } else {
     const bool d0 = d == 0, d1 = d == 1, d2 = d == 2;
     r0 = d0 ? r - (V - 1) : d2 ? r + (V - 1) : d1 ? r - h : r + h;
@@ -382,7 +390,7 @@ __device__ __forceinline__ void obs_see(const uint8_t* stage, int sbase, uint8_t
   const bool odd = (reinterpret_cast<uintptr_t>(dst) & 2) != 0;
   if constexpr (VV != 0) {
     constexpr int NC = VV * VV;
-    uint32_t cd[NC + 1];  // entity codes, view cell order (+ a zero pad)
+    uint32_t cd[NC + 3];  // entity codes, view cell order (+ zero pads to a multiple of 4)
     int jo[VV];           // column offsets, once per view (not per cell)
 #pragma unroll
     for (int j = 0; j < VV; ++j) jo[j] = j * dj;
@@ -405,16 +413,19 @@ __device__ __forceinline__ void obs_see(const uint8_t* stage, int sbase, uint8_t
       }
       pi += di;
     }
-    cd[NC] = 0;
-    // two cells -> one (tile, color, tile, color) word: pack the codes, split
-    // nibbles, interleave (3 byte_perms + 3 ALU ops per pair)
-    auto pair = [](uint32_t a, uint32_t b) {
-      const uint32_t x = __byte_perm(a, b, 0x0040);
-      return __byte_perm((x >> 4) & 0x0F0Fu, x & 0x0F0Fu, 0x5140);
-    };
-    uint32_t ev[(NC + 1) / 2];  // even-aligned words: cells (2k, 2k+1)
 #pragma unroll
-    for (int k = 0; k < (NC + 1) / 2; ++k) ev[k] = pair(cd[2 * k], cd[2 * k + 1]);
+    for (int k = NC; k < NC + 3; ++k) cd[k] = 0;
+    // four cells -> two (tile, color, tile, color) words: pack the codes
+    // (3 byte_perms), split the nibbles (3 ALU ops), interleave (2 byte_perms)
+    uint32_t ev[(NC + 3) / 2];  // even-aligned words: cells (2k, 2k+1)
+#pragma unroll
+    for (int q = 0; q < (NC + 3) / 4; ++q) {
+      const uint32_t x = __byte_perm(__byte_perm(cd[4 * q], cd[4 * q + 1], 0x0040),
+                                     __byte_perm(cd[4 * q + 2], cd[4 * q + 3], 0x0040), 0x5410);
+      const uint32_t hi = (x >> 4) & 0x0F0F0F0Fu, lo = x & 0x0F0F0F0Fu;
+      ev[2 * q] = __byte_perm(hi, lo, 0x5140);
+      ev[2 * q + 1] = __byte_perm(hi, lo, 0x7362);
+    }
     // an odd-offset record leads with cell 0 as a u16, then words of cells
     // (2k+1, 2k+2) = the even words shifted by one cell; an even one ends
     // with cell NC-1 as a u16

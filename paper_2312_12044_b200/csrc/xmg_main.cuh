@@ -61,28 +61,26 @@ __device__ __forceinline__ bool ahead_on(const xmg_state& s) { return s.next_gri
 // feeding it.  Unsigned arithmetic: n < 2^30 (validate_desc), and signed
 // 64-bit divisions cost a sign fix-up in every kernel prologue.
 __host__ __device__ inline int64_t queue_cap(int64_t n) {
-  const uint64_t blocks = ((uint64_t)n + kThreads - 1) / kThreads;
+  const uint32_t blocks = ((uint32_t)n + kThreads - 1) / kThreads;
   return (int64_t)((blocks + kQueues - 1) / kQueues * kThreads);
 }
 
 // Entry slots of sub-queue (parity, kind, q): double-buffered like the counts,
 // so step t + 1's step_main appends while step t's step_rare still drains.
 __host__ __device__ inline int64_t queue_base(int64_t n, uint32_t parity, int kind, int q) {
-  return (int64_t)(kWorkHeader + ((uint64_t)(parity & 1) * 2 * kQueues + (uint64_t)(kind * kQueues + q)) *
-                                     (uint64_t)queue_cap(n));
+  return (int64_t)kWorkHeader + (int64_t)((parity & 1) * 2 * kQueues + (uint32_t)(kind * kQueues + q)) *
+                                    queue_cap(n);
 }
 
 // Chunk bookkeeping after the queues (chunk = the 32 envs of one step_main warp):
 //   pending[nchunks]  queued envs of the chunk step_rare has not finished yet
 //   dirty[nchunks]    epoch of the last step that queued envs of the chunk
 // Only the chunk's own warp reads and writes its dirty word, so the tag needs
-// no clearing.
+// no clearing.  (32-bit arithmetic below: n < 2^30, validate_desc.)
 __host__ __device__ inline int64_t num_chunks(int64_t n) {
-  return (int64_t)(((uint64_t)n + kThreads - 1) / kThreads * kWarps);
+  return (int64_t)(((uint32_t)n + kThreads - 1) / kThreads * kWarps);
 }
-__host__ __device__ inline int64_t pending_base(int64_t n) {
-  return (int64_t)(kWorkHeader + 4ull * kQueues * (uint64_t)queue_cap(n));
-}
+__host__ __device__ inline int64_t pending_base(int64_t n) { return kWorkHeader + 4 * kQueues * queue_cap(n); }
 __host__ __device__ inline int64_t dirty_base(int64_t n) { return pending_base(n) + num_chunks(n); }
 // then the two counter words of the reset-ahead batches (prebuild_kernel)
 __host__ __device__ inline int64_t prebuild_ctr_base(int64_t n) { return dirty_base(n) + num_chunks(n); }
@@ -465,11 +463,20 @@ __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_
   }
 }
 
+// The two L2 policies as values (createpolicy once per device, policy_kernel):
+// kernel parameters live in the constant bank, so the step does not
+// rematerialise them (six uniform-datapath instructions per use).
+__global__ void policy_kernel(uint64_t* out) {
+  out[0] = l2_policy_last();
+  out[1] = l2_policy_first();
+}
+
 template <int MAXCH>
 __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_desc d, const xmg_state s,
                                                                 const xmg_out o, const void* actions, int act_dtype,
                                                                 const uint32_t* abort_flag, uint32_t epoch,
-                                                                int64_t n) {
+                                                                int64_t n, uint64_t pol_keep_in,
+                                                                uint64_t pol_stream_in) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // Launched as a programmatic dependent of the previous kernel (the previous
@@ -498,7 +505,10 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
   int act = 1;
   const uint32_t was_dirty = e0 + warp * 32 < n ? *dirty : 0u;  // issued together with the state loads
 #if XMG_L2HINT
-  const uint64_t pol_keep = l2_policy_last(), pol_stream = l2_policy_first();
+  const uint64_t pol_keep = pol_keep_in, pol_stream = pol_stream_in;
+#else
+  (void)pol_keep_in;
+  (void)pol_stream_in;
 #endif
   if (valid) {
 #if XMG_L2HINT

@@ -198,6 +198,7 @@ struct DevInfo {
   const char* what = "";
   int64_t rare_smem = -1;  // occupancy cache of step_rare for this scratch size
   int rare_per_sm = 0;
+  uint64_t pol[2] = {0, 0};  // L2 policies (evict_last, evict_first), policy_kernel
 };
 constexpr int kMaxDevices = 64;
 DevInfo g_dev[kMaxDevices];
@@ -222,6 +223,16 @@ int device_attrs(int dev) {
         set_attr(di, step_main<32>, "step_main") &&
         set_attr(di, step_rare, "step_rare") && set_attr(di, prebuild_kernel, "prebuild_kernel") &&
         set_attr(di, rollout_kernel, "rollout_kernel");
+    if (di.err == cudaSuccess) {
+      uint64_t* dp = nullptr;
+      di.what = "policy_kernel";
+      di.err = cudaMalloc(&dp, 2 * sizeof(uint64_t));
+      if (di.err == cudaSuccess) {
+        policy_kernel<<<1, 1>>>(dp);
+        di.err = cudaMemcpy(di.pol, dp, sizeof(di.pol), cudaMemcpyDeviceToHost);
+        cudaFree(dp);
+      }
+    }
     di.done = true;
   }
   if (di.err != cudaSuccess) return fail(std::string(di.what) + " attributes: " + cudaGetErrorString(di.err));
@@ -254,7 +265,8 @@ template <int MAXCH>
 int launch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
                 const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st, bool pdl) {
   const MainGeo geo = make_main_geo(d->view_size, MAXCH, d->rule_width);
-  if (!cur_dev()) return -1;
+  const DevInfo* di = cur_dev();
+  if (!di) return -1;
   const int64_t blocks = (n + kThreads - 1) / kThreads;
   // programmatic dependent of the previous kernel on the stream (the previous
   // step's step_rare, or this step's validation)
@@ -268,7 +280,8 @@ int launch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, con
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t err = cudaLaunchKernelEx(&cfg, step_main<MAXCH>, *d, *s, *o, actions, dtype, flag, epoch, n);
+  const cudaError_t err =
+      cudaLaunchKernelEx(&cfg, step_main<MAXCH>, *d, *s, *o, actions, dtype, flag, epoch, n, di->pol[0], di->pol[1]);
   if (err != cudaSuccess) return fail(std::string("step_main: ") + cudaGetErrorString(err));
   return check_launch("step_main");
 }
@@ -623,7 +636,7 @@ int64_t xmg_step_smem_bytes(const xmg_env_desc* desc) {
   return a > b ? a : b;
 }
 
-int64_t xmg_work_words(int64_t n) { return work_words(n); }
+int64_t xmg_work_words(int64_t n) { return n < 0 || n > (int64_t)kQEnv ? -1 : work_words(n); }
 
 int32_t xmg_prebuild(const xmg_env_desc* desc, const xmg_state* state, int64_t cls, int64_t classes, int64_t n,
                      void* stream) {

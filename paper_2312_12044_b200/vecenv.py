@@ -276,7 +276,10 @@ class VecEnv:
         agent[:, 1] = word1
         self.agent = torch.from_numpy(agent.view(np.int64)).to(dev)
         self.rng = torch.zeros((n, 2), dtype=torch.int64, device=dev)
-        self.work = torch.zeros(int(_lib.lib().xmg_work_words(n)), dtype=torch.int32, device=dev)
+        words = int(_lib.lib().xmg_work_words(n))
+        if words < 0:
+            raise ValueError(f"num_envs={n} is too large for one VecEnv (< 2^30; shard with global_offset)")
+        self.work = torch.zeros(words, dtype=torch.int32, device=dev)
         # reset-ahead records (include/xmg.h): each env's next trial, pre-built
         # while the current one runs, so an auto-reset is a copy
         # (off by default for the Empty scenario, whose trials are all the same

@@ -46,6 +46,7 @@ def test_abi_version_and_error_channel():
     assert L.xmg_reset(C.byref(d), C.byref(st), 1, 8, C.byref(out), None) < 0
     assert b"grid size" in L.xmg_last_error()
     assert L.xmg_work_words(1 << 20) > (1 << 21)
+    assert L.xmg_work_words(1 << 30) == -1 and L.xmg_work_words(-1) == -1
 
 
 def test_host_key_helpers_match_oracle():
