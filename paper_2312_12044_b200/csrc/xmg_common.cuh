@@ -126,6 +126,16 @@ __device__ __forceinline__ void cp_async16_hint(void* smem_dst, const void* gmem
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem_src), "l"(pol)
                : "memory");
 }
+// the same with the shared-memory address already converted (one
+// generic->shared conversion per buffer instead of one per chunk)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async16_s(uint32_t s, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async16_hint_s(uint32_t s, const void* gmem_src, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem_src), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
@@ -229,11 +239,12 @@ __device__ __forceinline__ void stage_issue(View& vw, int lo, int hi, int HW, co
     vw.sbase = (int)(a0 - gb);
     vw.slo = max(vw.sbase, 0);
     vw.shi = min(vw.sbase + 16 * nch, HW);
+    const uint32_t sb = smem_u32(vw.stage);
 #pragma unroll
     for (int k = 0; k < MAXCH; ++k)
       if (k < nch) {
-        if (pol) cp_async16_hint(vw.stage + 16 * k, reinterpret_cast<const void*>(a0 + 16 * k), *pol);
-        else cp_async16(vw.stage + 16 * k, reinterpret_cast<const void*>(a0 + 16 * k));
+        if (pol) cp_async16_hint_s(sb + 16 * k, reinterpret_cast<const void*>(a0 + 16 * k), *pol);
+        else cp_async16_s(sb + 16 * k, reinterpret_cast<const void*>(a0 + 16 * k));
       }
   }
 }
@@ -432,8 +443,9 @@ __device__ __forceinline__ void obs_see(const uint8_t* stage, int sbase, uint8_t
     *reinterpret_cast<uint16_t*>(dst + (odd ? 0 : 2 * (NC - 1))) =
         (uint16_t)(odd ? ev[0] : ev[(NC - 1) / 2]);
     uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + (odd ? 2 : 0));
+    const uint32_t sh = odd ? 16u : 0u;  // a funnel shift by 0 is the word itself
 #pragma unroll
-    for (int k = 0; k < (NC - 1) / 2; ++k) d32[k] = odd ? __funnelshift_r(ev[k], ev[k + 1], 16) : ev[k];
+    for (int k = 0; k < (NC - 1) / 2; ++k) d32[k] = __funnelshift_r(ev[k], ev[k + 1], sh);
   } else {
     uint16_t* o = reinterpret_cast<uint16_t*>(dst);
     for (int i = 0; i < V; ++i)

@@ -319,7 +319,8 @@ __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_
     if (rules_needed) {
       const uint32_t* src = d.task_rows + (int64_t)task * d.row_words;
       const int nq = (kRowHeader + R + 3) >> 2;
-      for (int q = 0; q < nq; ++q) cp_async16(rbuf + 4 * q, src + 4 * q);
+      const uint32_t rs = smem_u32(rbuf);
+      for (int q = 0; q < nq; ++q) cp_async16_s(rs + 16 * q, src + 4 * q);
     }
     cp_async_wait_all();
 
