@@ -311,6 +311,26 @@ __device__ __forceinline__ void warp_reset_env(const xmg_env_desc& d, const xmg_
   XMG_TRB(6);
 }
 
+// The auto-resets of the PUT_DOWN envs in cm (lanes of a step_rare batch,
+// env e_l per lane) from their pre-built records: state word (its buffer bit
+// names the other grid buffer, where the record's grid is) and rng per lane,
+// then each env's first observation copied by the whole warp.
+__device__ __noinline__ void put_consume(const xmg_state s, const xmg_out o, uint32_t cm, int64_t e_l, int ob,
+                                         int lane) {
+  if ((cm >> lane) & 1) {
+    const ulonglong2* ns = reinterpret_cast<const ulonglong2*>(s.next_state) + 2 * e_l;
+    const ulonglong2 a = __ldcg(ns), b = __ldcg(ns + 1);
+    reinterpret_cast<ulonglong2*>(s.agent)[e_l] = a;
+    reinterpret_cast<ulonglong2*>(s.rng)[e_l] = b;
+  }
+  if (o.obs != nullptr)
+    for (uint32_t m = cm; m; m &= m - 1) {
+      const int64_t e = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)e_l, __ffs(m) - 1);
+      warp_copy_cg(o.obs + e * ob, s.next_obs + e * ob, ob, lane);
+    }
+  __syncwarp();
+}
+
 // Resets of a group of up to 32 envs (one per lane, `mine`): each lane
 // derives its env's trial keys, then the warp rebuilds the envs one by one.
 __device__ __forceinline__ void warp_reset_group(const xmg_env_desc& d, const xmg_env_desc* sd, const xmg_state& s,
@@ -504,10 +524,19 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRar
 #ifdef XMG_TRACE
       if (i0 == j) XMG_TR(gw, 6, gtime());
 #endif
-      // ---- trials the PUT_DOWN finished: keys derived lane-parallel, then
-      // the envs rebuilt by the whole warp (copying a pre-built successor here
-      // instead measured ~1 us/step slower in steady state: step_rare's
-      // register pressure)
+      // ---- trials the PUT_DOWN finished: a pre-built successor taken over
+      // (out of line: keeps step_rare's registers), else keys derived
+      // lane-parallel and the envs rebuilt by the whole warp
+      if (lastm && ahead_on(s)) {
+        // trials with a pre-built successor (stage 2, e.g. every PUT_DOWN of a
+        // synchronized budget end) take it over like step_main does
+        const bool ready = ((lastm >> lane) & 1) && ((pa[lane].x & kStageMask) == kStageReady);
+        const uint32_t cm = __ballot_sync(0xffffffffu, ready);
+        if (cm) {
+          put_consume(s, o, cm, e_l, ob, lane);
+          lastm &= ~cm;
+        }
+      }
       if (lastm) {
         ulonglong2 ek = make_ulonglong2(0, 0);
         if ((lastm >> lane) & 1) ek = reinterpret_cast<const ulonglong2*>(s.rng)[e_l];
