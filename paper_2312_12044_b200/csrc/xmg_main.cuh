@@ -320,7 +320,13 @@ __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_
       const uint32_t* src = d.task_rows + (int64_t)task * d.row_words;
       const int nq = (kRowHeader + R + 3) >> 2;
       const uint32_t rs = smem_u32(rbuf);
-      for (int q = 0; q < nq; ++q) cp_async16_s(rs + 16 * q, src + 4 * q);
+      if (nq <= 8) {  // rows of up to 28 rules: straight-line, predicated
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < nq) cp_async16_s(rs + 16 * q, src + 4 * q);
+      } else {
+        for (int q = 0; q < nq; ++q) cp_async16_s(rs + 16 * q, src + 4 * q);
+      }
     }
     cp_async_wait_all();
 
@@ -477,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
                                                                 const xmg_out o, const void* actions, int act_dtype,
                                                                 const uint32_t* abort_flag, uint32_t epoch,
                                                                 int64_t n, uint64_t pol_keep_in,
-                                                                uint64_t pol_stream_in) {
+                                                                uint64_t pol_stream_in, const MainGeo geo) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // Launched as a programmatic dependent of the previous kernel (the previous
@@ -485,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
   // the previous step_rare: with a validation it waits for the verdict, and
   // per 32-env chunk it waits only where the previous step queued envs (below).
   const int H = d.height, W = d.width, HW = H * W, V = d.view_size, R = d.rule_width;
-  const MainGeo geo = make_main_geo(V, MAXCH, R);
+  // geo: make_main_geo(V, MAXCH, R), computed by the launcher (a kernel parameter)
   const int64_t tile = blockIdx.x;
   const int64_t e0 = tile * kThreads;
   const int64_t chunk = tile * kWarps + warp;

@@ -281,7 +281,8 @@ int launch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, con
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const cudaError_t err =
-      cudaLaunchKernelEx(&cfg, step_main<MAXCH>, *d, *s, *o, actions, dtype, flag, epoch, n, di->pol[0], di->pol[1]);
+      cudaLaunchKernelEx(&cfg, step_main<MAXCH>, *d, *s, *o, actions, dtype, flag, epoch, n, di->pol[0], di->pol[1],
+                         geo);
   if (err != cudaSuccess) return fail(std::string("step_main: ") + cudaGetErrorString(err));
   return check_launch("step_main");
 }
