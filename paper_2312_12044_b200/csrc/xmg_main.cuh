@@ -99,10 +99,6 @@ __device__ __forceinline__ ulonglong2 ld_cg_u64x2(const ulonglong2* p) {  // fre
 #ifndef XMG_L2HINT
 #define XMG_L2HINT 1
 #endif
-#ifndef XMG_VAL_GRIDWAIT
-#define XMG_VAL_GRIDWAIT 0  // 1: griddepcontrol.wait on the validation grid (measured 81 -> 94 us/step at C3:
-                            // it waits for the whole programmatic chain, so the drain overlap is lost)
-#endif
 #ifndef XMG_VAL_SLEEP
 #define XMG_VAL_SLEEP 64  // ns between polls of the validation verdict
 #endif
@@ -280,7 +276,8 @@ template <int MAXCH>
 __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_state& s, const xmg_out& o,
                                                uint32_t epoch, int64_t n, int64_t tile, int tid, int lane, int warp,
                                                const MainGeo& geo, WView& vw, uint32_t* rbuf, uint8_t* obs_stage,
-                                               ulonglong2 ag, int act, uint64_t pol_keep, uint64_t pol_stream) {
+                                               ulonglong2 ag, int act, uint64_t pol_keep, uint64_t pol_stream,
+                                               const uint32_t* abort_flag) {
   const int H = d.height, W = d.width, HW = H * W, V = d.view_size, R = d.rule_width;
   const int64_t e0 = tile * kThreads;
   const int64_t chunk = tile * kWarps + warp;
@@ -302,10 +299,10 @@ __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_
   float rew = 0.f;
   bool last = false, consume = false;
   const bool ahead = ahead_on(s);  // (the consume path costs ~1 us/step of steady state at C3: measured)
+  const int nd = act == 1 ? ((dir + 3) & 3) : (act == 2 ? ((dir + 1) & 3) : dir);
   if (valid) {
     // ---- stage the post-action window (MOVE: both candidate poses) and,
     // for actions that can raise an event, the env's rule row
-    const int nd = act == 1 ? ((dir + 3) & 3) : (act == 2 ? ((dir + 1) & 3) : dir);
     {
       int lo, hi;
       window_span(r, c, nd, act == 0 ? 1 : 0, act == 3 ? 1 : 0, H, W, V, lo, hi);
@@ -328,6 +325,22 @@ __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_
         for (int q = 0; q < nq; ++q) cp_async16_s(rs + 16 * q, src + 4 * q);
       }
     }
+  }
+  // this epoch's validation verdict (published by the last validation CTA),
+  // awaited while the window is in flight: nothing is written before it
+  if (abort_flag != nullptr) {
+    if (lane == 0)
+      for (uint32_t spins = 0; ld_acquire(abort_flag + 1) != epoch; ++spins) {
+        if (spins > (1u << 25)) __trap();
+        __nanosleep(XMG_VAL_SLEEP);
+      }
+    __syncwarp();
+    if (batch_rejected(abort_flag, epoch)) {
+      cp_async_wait_all();  // (no copy outlives the CTA)
+      return;
+    }
+  }
+  if (valid) {
     cp_async_wait_all();
 
     // ---- action, ref:vecenv.py:306-342 / ref:env.py:148-191
@@ -525,28 +538,11 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
 #endif
     act = load_action(actions, act_dtype, e);
   }
-  // the loads above are in flight while the verdict is awaited (reads only:
-  // a rejected batch writes nothing; state step_rare may still rewrite is
-  // reloaded below)
-  if (abort_flag != nullptr) {  // this epoch's validation verdict (published by its last CTA)
-#if XMG_VAL_GRIDWAIT
-    // step_main is the programmatic dependent of the validation grid: wait for
-    // that grid's completion in hardware (no polling traffic against the
-    // validation's own atomics), then the verdict is visible
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
-    if (lane == 0)
-      for (uint32_t spins = 0; ld_acquire(abort_flag + 1) != epoch; ++spins) {
-        if (spins > (1u << 25)) __trap();
-        __nanosleep(XMG_VAL_SLEEP);
-      }
-    __syncwarp();
-  }
   // the previous step_rare has read these counts (it reads them before it
   // lets this grid launch); this step appends to the other parity
   if (blockIdx.x == 0)
     for (int i = tid; i < 2 * kQueues; i += blockDim.x) s.work[count_index(epoch + 1, 0, 0) + i] = 0;
-  if (batch_rejected(abort_flag, epoch)) return;
+  // (a rejected batch returns in main_tile_body, before its first write)
   if (was_dirty == epoch - 1 && e0 + warp * 32 < n) {
     // the previous step queued envs of this chunk: wait until its step_rare has
     // released them all, then reload the state word it may have rewritten
@@ -563,8 +559,9 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
   }
   main_tile_body<MAXCH>(d, s, o, epoch, n, tile, tid, lane, warp, geo, vw, rbuf, obs_stage, ag, act,
 #if XMG_L2HINT
-                              pol_keep, pol_stream);
+                              pol_keep, pol_stream,
 #else
-                              0, 0);
+                              0, 0,
 #endif
+                              abort_flag);
 }
