@@ -34,16 +34,16 @@ constexpr uint32_t kQPut = 1u << 31, kQReset = 1u << 30, kQEnv = (1u << 30) - 1;
 // (ref:vecenv.py:224-233 via :359-361), both fixed while the trial runs.  So
 // every K-th step (host side, xmg_step) a plain launch of prebuild_kernel
 // builds the next trial of one class of envs (e mod B == class, B = the
-// classes that fit in budget - 2 steps) into state.next_* and marks them
-// stage 2 (state word 0 bits 18-19); the kernels after it see the records.
-// When a trial ends at stage 2, step_main copies the records (grid, state
-// word, rng, first observation) instead of queueing a rebuild; otherwise (a
-// goal reached before the env's class came up, a PUT_DOWN that ends the
-// trial) the in-place rebuild runs.  Every trial that runs to the budget
-// passes one batch of its class, so the synchronized budget resets are all
-// copies; the build work moves out of the burst and is done at full-GPU
-// efficiency once per K steps, without touching the step_rare / step_main
-// overlap.
+// classes that fit in budget - 2 steps) into state.next_state / next_obs and
+// the env's other grid buffer, and marks them stage 2 (state word 0 bits
+// 18-19); the kernels after it see the records.  When a trial ends at stage
+// 2, step_main (or step_rare, for a PUT_DOWN) takes the record over (state
+// word with the buffer bit flipped, rng, first observation) instead of
+// rebuilding; otherwise (a goal reached before the env's class came up) the
+// in-place rebuild runs.  Every trial that runs to the budget passes one batch
+// of its class, so the synchronized budget resets are all take-overs; the
+// build work moves out of the burst and is done at full-GPU efficiency once
+// per K steps, without touching the step_rare / step_main overlap.
 constexpr uint64_t kStageReady = 2ull << 18, kStageMask = 3ull << 18;
 // Double-buffered grids: bit 20 of state word 0 says which of the two grid
 // buffers (state.grids = 0, state.next_grids = 1) holds the running trial;
@@ -270,7 +270,7 @@ __device__ __forceinline__ bool batch_rejected(const uint32_t* flag, uint32_t ep
 
 // The step of one 128-env tile after its loads (state word `ag` of this
 // thread's env, its action, the chunk wait done): window staging, action,
-// rules, goal, counters, queues, reset-ahead copies, statistics and the
+// rules, goal, counters, queues, reset-ahead take-overs, statistics and the
 // observation.
 template <int MAXCH>
 __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_state& s, const xmg_out& o,
