@@ -56,14 +56,18 @@ def test_reset_ahead_matches_rebuild_and_oracle(env_name, config, n, budgets, re
     steps = int(budgets * params.step_budget) + 3
     acts = random_actions(policy_keys(key_from_seed(22), n, device=on.device), 0, steps)
     ah = acts.cpu().numpy()
-    copied = rebuilt = 0
+    copied = rebuilt = put_taken = 0
     for t in range(steps):
         stage = on.reset_ahead_stage.cpu().numpy()
+        holding = on.agent_fields()[:, 3].cpu().numpy() != 0
         ta, tb = on.step(acts[t]), off.step(acts[t])
         st = ta.step_types.cpu().numpy()
         last = st == 2
         copied += int((last & (stage == 2)).sum())
         rebuilt += int((last & (stage != 2)).sum())
+        # PUT_DOWN while holding something, ending a trial with a record:
+        # step_rare's take-over path (xmg_rare.cuh put_consume)
+        put_taken += int((last & (stage == 2) & holding & (ah[t] == 4)).sum())
         assert torch.equal(ta.observations, tb.observations), f"obs t={t}"
         assert torch.equal(ta.rewards, tb.rewards) and torch.equal(ta.discounts, tb.discounts), f"t={t}"
         assert torch.equal(ta.step_types, tb.step_types), f"step_type t={t}"
@@ -84,6 +88,7 @@ def test_reset_ahead_matches_rebuild_and_oracle(env_name, config, n, budgets, re
     assert rebuilt > 0 or env_name.startswith("XLand-MiniGrid-R9"), "no trial ended before its pre-build"
     # the budget burst is served from the records: nearly every budget end copies
     assert copied > rebuilt or env_name.startswith("MiniGrid-Empty")
+    assert put_taken > 0 or not env_name.startswith("XLand"), "no PUT_DOWN ended a trial that had a record"
 
 
 def test_reset_ahead_across_rollouts_and_blocks():
