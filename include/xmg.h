@@ -111,8 +111,8 @@ typedef struct xmg_out {
     float* reward;      /* [n]  float32(1.0 - 0.9*(sc/budget)) evaluated in fp64 */
     float* discount;    /* [n] */
     int8_t* step_type;  /* [n]  FIRST 0 / MID 1 / LAST 2 */
-    /* nullable episode statistics, one slot per 128-env CTA (no atomics
-     * contention): stats[3*cta + 0] += sum of rewards, [+1] += finished
+    /* nullable episode statistics, one slot per 128 envs (little atomics
+     * contention): stats[3*(e/128) + 0] += sum of rewards, [+1] += finished
      * trials, [+2] += their lengths (ref RolloutStats, harness.py:103-143) */
     double* stats;
 } xmg_out;
@@ -258,7 +258,7 @@ int32_t xmg_graph_launch(void* graph_exec, void* stream);
 int32_t xmg_graph_step(void* graph_exec, const uint8_t* src, uint8_t* staging, int64_t n, void* stream);
 int32_t xmg_graph_destroy(void* graph_exec);
 
-/* Dynamic shared memory per 128-env CTA of the rollout kernel (<0: unsupported). */
+/* Dynamic shared memory per CTA (4 warps) of the rollout kernel (<0: unsupported). */
 int64_t xmg_rollout_smem_bytes(const xmg_env_desc* desc);
 
 /* ---- observation images (ref render.py) ---------------- */
@@ -292,7 +292,7 @@ int32_t xmg_image_obs_aligned(const uint8_t* obs /*[n][v][v][2]*/, int64_t n, in
 /* Size in u32 words of xmg_state.work for n envs (-1 unless 0 <= n < 2^30). */
 int64_t xmg_work_words(int64_t n);
 
-/* Bytes of dynamic shared memory per 128-env CTA the step/reset kernels use
+/* Bytes of dynamic shared memory per CTA the step/reset kernels use
  * for this description (host query, for capacity checks). <0 if unsupported. */
 int64_t xmg_step_smem_bytes(const xmg_env_desc* desc);
 

@@ -77,7 +77,11 @@ __device__ __forceinline__ int dir_dc(int d) { return d == 1 ? 1 : (d == 3 ? -1 
 __device__ __forceinline__ int near_dr(int k) { return k == 0 ? -1 : (k == 3 ? 1 : 0); }
 __device__ __forceinline__ int near_dc(int k) { return k == 1 ? -1 : (k == 2 ? 1 : 0); }
 
-constexpr int kThreads = 128;  // envs per CTA
+#ifndef XMG_THREADS
+#define XMG_THREADS 64  // 64-env CTAs: C3 78.2 -> 76.9, C4 54.1 -> 51.5 us/step vs 128 (256: slower)
+#endif
+constexpr int kThreads = XMG_THREADS;  // envs per step_main CTA
+constexpr int kStatEnvs = 128;         // envs per episode-statistics slot (include/xmg.h xmg_out.stats)
 constexpr int kRowHeader = 4;  // task row: goal, counts, MOVE slot mask, PICK_UP slot mask
 constexpr int kMaxDynSmem = 227 * 1024 - 1024;  // leave room for the static shared desc copy
 constexpr int kWarps = kThreads / 32;
@@ -102,7 +106,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define XMG_TRB(k)
 #endif
 #ifndef XMG_MINB
-#define XMG_MINB 8  // min resident CTAs per SM the register allocation targets (64 registers; measured best at C3)
+#define XMG_MINB (1024 / XMG_THREADS)  // min resident CTAs per SM the register allocation targets (64 registers; measured best at C3)
 #endif
 #ifndef XMG_MINB_RARE
 #define XMG_MINB_RARE 6  // step_rare: <= 80 registers, so the next step's kernels fit beside it

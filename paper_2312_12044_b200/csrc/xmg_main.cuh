@@ -57,7 +57,7 @@ __device__ __forceinline__ uint8_t* grid_ptr(const xmg_state& s, int64_t e, int 
 }
 __device__ __forceinline__ bool ahead_on(const xmg_state& s) { return s.next_grids != nullptr; }
 
-// capacity of one sub-queue: every env of the step_main CTAs (128 envs each)
+// capacity of one sub-queue: every env of the step_main CTAs (kThreads envs each)
 // feeding it.  Unsigned arithmetic: n < 2^30 (validate_desc), and signed
 // 64-bit divisions cost a sign fix-up in every kernel prologue.
 __host__ __device__ inline int64_t queue_cap(int64_t n) {
@@ -268,7 +268,7 @@ __device__ __forceinline__ bool batch_rejected(const uint32_t* flag, uint32_t ep
   return flag != nullptr && *reinterpret_cast<volatile const uint32_t*>(flag) == epoch;
 }
 
-// The step of one 128-env tile after its loads (state word `ag` of this
+// The step of one kThreads-env tile after its loads (state word `ag` of this
 // thread's env, its action, the chunk wait done): window staging, action,
 // rules, goal, counters, queues, reset-ahead take-overs, statistics and the
 // observation.
@@ -444,7 +444,7 @@ __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_
   if (cm) consume_next(s, cm, e0 + warp * 32, HW, 2 * V * V, o.obs != nullptr ? obs_stage : nullptr, lane);
 
   // ---- episode statistics of the trials decided here
-  if (o.stats != nullptr) warp_stats_step(o.stats, (int)tile, rew, last, sc);
+  if (o.stats != nullptr) warp_stats_step(o.stats, (int)(e0 / kStatEnvs), rew, last, sc);
 
 
   // ---- observation: assembled in smem, one TMA bulk store per warp

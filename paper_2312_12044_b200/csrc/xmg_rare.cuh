@@ -375,7 +375,7 @@ __device__ __forceinline__ void warp_reset_group(const xmg_env_desc& d, const xm
 // reset_keys != nullptr: reset mode (ref VecEnv.reset_with_keys,
 // vecenv.py:205-222), every env [0, n) rebuilt from keys[e] with a FIRST
 // record.
-__global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRareWarps) step_rare(const xmg_env_desc d, const xmg_state s,
+__global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * 4 / kRareWarps) step_rare(const xmg_env_desc d, const xmg_state s,
                                                                      const xmg_out o, const uint64_t* reset_keys,
                                                                      const uint32_t* abort_flag, uint32_t epoch,
                                                                      int64_t n, int track) {
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * kWarps / kRar
           o.discount[e] = last ? 0.f : 1.f;
           o.step_type[e] = last ? 2 : 1;
           if (o.stats != nullptr && (rew != 0.f || last)) {
-            const int slot = (int)(e / kThreads);
+            const int slot = (int)(e / kStatEnvs);
             atomicAdd(o.stats + 3 * slot, (double)rew);
             if (last) {
               atomicAdd(o.stats + 3 * slot + 1, 1.0);

@@ -398,6 +398,6 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
                         (uint64_t)goal_word | ((uint64_t)(uint32_t)task << 32));
     reinterpret_cast<ulonglong2*>(s.rng)[e] = rk;
   }
-  if (o.stats != nullptr) warp_stats(o.stats, (int)(e0 / kThreads), st_ret, st_trials, st_len);
+  if (o.stats != nullptr) warp_stats(o.stats, (int)(e0 / kStatEnvs), st_ret, st_trials, st_len);
   if (lane == 0 && o.obs != nullptr) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }

@@ -8,7 +8,7 @@
 //   (:359-361 -> :224-291) -> egocentric observation (:481-500).
 //
 // Kernels:
-//  * step_main — one thread per env, 128 envs per CTA: one 16-byte state word
+//  * step_main — one thread per env, 64 envs per CTA: one 16-byte state word
 //    per env, the grid bytes of the view window staged global->shared with
 //    16-byte cp.async, the action, MOVE / PICK_UP rules and goals per lane
 //    (select-based), counters and reward, the observation assembled in shared
