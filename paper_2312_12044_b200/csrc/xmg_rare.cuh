@@ -602,8 +602,13 @@ __host__ __device__ inline int pre_warp_bytes(int H, int W) {
   return warp_scratch_bytes(hwp) + kKeySlots * (int)sizeof(TrialKeys) + round16((int)sizeof(xmg_env_desc));
 }
 
+// epoch != 0 (the batch of xmg_step / xmg_steps epoch `epoch`): launched as a
+// programmatic dependent, so it may run while the previous step's step_rare
+// still drains; an env of a chunk that step queued is read only after that
+// step_rare has released the chunk (the protocol of step_main).
 __global__ void __launch_bounds__(kPreWarps * 32, XMG_PRE_MINB * 4 / kPreWarps)
-    prebuild_kernel(const xmg_env_desc d, const xmg_state s, int64_t cls, int64_t B, int64_t n, uint32_t* ctr) {
+    prebuild_kernel(const xmg_env_desc d, const xmg_state s, int64_t cls, int64_t B, int64_t n, uint32_t* ctr,
+                    uint32_t epoch) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t count = cls < n ? (n - cls + B - 1) / B : 0;
@@ -629,7 +634,19 @@ __global__ void __launch_bounds__(kPreWarps * 32, XMG_PRE_MINB * 4 / kPreWarps)
     uint64_t w0 = 0;
     bool need = false;
     if (lane < kPreGroup && i < count) {
-      w0 = s.agent[2 * e];
+      if (epoch != 0) {
+        const int64_t chunk = e >> 5;
+        if (s.work[dirty_base(n) + chunk] == epoch - 1) {
+          const uint32_t* pending = s.work + pending_base(n) + chunk;
+          for (uint32_t spins = 0; ld_acquire(pending) != 0; ++spins) {
+            if (spins > (1u << 25)) __trap();
+            __nanosleep(128);
+          }
+        }
+        w0 = ld_cg_u64x2(reinterpret_cast<const ulonglong2*>(s.agent) + e).x;
+      } else {
+        w0 = s.agent[2 * e];
+      }
       need = (w0 & kStageMask) == 0;
     }
     warp_reset_group(d, sdesc, s, none, wbase, geo, keys, lane, need, e, nullptr, 0, true,

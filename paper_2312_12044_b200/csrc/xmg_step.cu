@@ -395,7 +395,7 @@ AheadPlan ahead_plan(const xmg_env_desc* d, int64_t n, int sms) {
 }
 
 int launch_prebuild(const xmg_env_desc* d, const xmg_state* s, int64_t cls, int64_t classes, int64_t n,
-                    cudaStream_t st) {
+                    cudaStream_t st, uint32_t epoch = 0) {
   const int64_t smem = (int64_t)kPreWarps * pre_warp_bytes(d->height, d->width);
   const DevInfo* di = cur_dev();
   if (!di) return -1;
@@ -407,8 +407,21 @@ int launch_prebuild(const xmg_env_desc* d, const xmg_state* s, int64_t cls, int6
   const int64_t count = (n - cls + classes - 1) / classes;
   const int64_t need = (count + (int64_t)kPreWarps * kPreGroup - 1) / ((int64_t)kPreWarps * kPreGroup);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * di->sms, need));
-  prebuild_kernel<<<(unsigned)blocks, kPreWarps * 32, (size_t)smem, st>>>(*d, *s, cls, classes, n,
-                                                                          s->work + prebuild_ctr_base(n));
+  // a step's batch (epoch != 0) may overlap the previous step's step_rare
+  // (programmatic dependent; prebuild_kernel waits per chunk)
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = epoch != 0 && pdl_enabled() ? 1 : 0;
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(kPreWarps * 32);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t err = cudaLaunchKernelEx(&cfg, prebuild_kernel, *d, *s, cls, classes, n,
+                                             s->work + prebuild_ctr_base(n), epoch);
+  if (err != cudaSuccess) return fail(std::string("prebuild_kernel: ") + cudaGetErrorString(err));
   return check_launch("prebuild_kernel");
 }
 
@@ -423,7 +436,7 @@ int maybe_prebuild(const xmg_env_desc* d, const xmg_state* s, uint32_t epoch, in
   if (epoch % (uint64_t)p.every != 0) return 0;
   const int64_t cls = (int64_t)((epoch / (uint64_t)p.every) % (uint64_t)p.classes);
   if (cls >= n) return 0;
-  return launch_prebuild(d, s, cls, p.classes, n, st) ? -1 : 1;
+  return launch_prebuild(d, s, cls, p.classes, n, st, epoch == 0 ? 0u : epoch) ? -1 : 1;
 }
 
 // envs per warp of the one-kernel step (xmg_step_fused): 32; XMG_FUSED_EPW
