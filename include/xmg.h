@@ -24,7 +24,9 @@
  *   agent  u64 [n][2]     word 0: r | c<<8 | dir<<16 | pocket<<24 | step_count<<32,
  *                         bits 18-19 = the reset-ahead stage (scheduling metadata,
  *                         not env state: 0 none, 1 next trial queued for pre-build
- *                         this step, 2 pre-built; see next_* below)
+ *                         this step, 2 pre-built; see next_* below),
+ *                         bit 20 = the grid buffer holding the env's grid
+ *                         (0: grids, 1: next_grids; always 0 without reset-ahead)
  *                         word 1: goal | task<<32, where goal = encoding bytes
  *                         (kind, a1, a2, a3) little-endian and task = the row
  *                         of the task table this env runs (one 16-byte load)
@@ -98,9 +100,11 @@ typedef struct xmg_state {
      * on the env's rng key and task (ref vecenv.py:224-233, 359-361), both
      * fixed while the trial runs, so xmg_step pre-builds it during the trial
      * (one env in (budget - 2) per step) and the auto-reset that ends the
-     * trial becomes a copy of these records instead of a build.  16-byte
-     * aligned; contents are scratch owned by the library. */
-    uint8_t* next_grids;   /* [n][H*W] (+64 B pad, like grids) the next trial's grid */
+     * trial takes these records over instead of building.  The grids are
+     * double-buffered: a pre-build writes the buffer the env's state word
+     * does not name, and the take-over flips bit 20 (no grid copy).  16-byte
+     * aligned; next_state / next_obs are scratch owned by the library. */
+    uint8_t* next_grids;   /* [n][H*W] (+64 B pad, like grids) the second grid buffer */
     uint64_t* next_state;  /* [n][4]: next state word 0, word 1, next rng (hi, lo) */
     uint8_t* next_obs;     /* [n][v][v][2] the next trial's first observation */
 } xmg_state;
