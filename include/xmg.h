@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define XMG_ABI_VERSION 2
+#define XMG_ABI_VERSION 3
 
 /* scenario ids: ref scenarios.py:177-185 (SCENARIOS) */
 enum {
@@ -87,6 +87,13 @@ typedef struct xmg_env_desc {
     const int16_t* seg_off;      /* [num_segments+1] offsets into seg_cells */
     const int16_t* seg_cells;    /* flat cell indices of each door segment */
     const uint32_t* task_rows;   /* [num_tasks][row_words] */
+    /* ABI 3: optional compact rows of the rules a MOVE / PICK_UP can fire
+     * (AGENT_HOLD, the AGENT_NEAR family), [num_tasks][agent_row_words]:
+     * word 0 = count | MOVE slot mask << 8 | PICK_UP slot mask << 20 (12-bit
+     * masks over these slots), then the rule words in stored order, padded
+     * to 16 bytes.  NULL / 0: the step reads the whole task row. */
+    int32_t agent_row_words;
+    const uint32_t* agent_rows;
 } xmg_env_desc;
 
 typedef struct xmg_state {

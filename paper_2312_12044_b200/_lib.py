@@ -23,7 +23,7 @@ HEADER = os.path.join(ROOT, "include", "xmg.h")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xptxas", "-v", "-shared", "-Xcompiler", "-fPIC"]
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # scenario ids of include/xmg.h (ref scenarios.py:177-185)
 SCENARIO_IDS = {"xland": 0, "empty": 1, "empty_random": 2, "door_key": 3, "four_rooms": 4,
@@ -49,7 +49,8 @@ class EnvDesc(C.Structure):
                 ("fixed_doors", C.c_int32), ("rule_width", C.c_int32), ("obj_width", C.c_int32),
                 ("row_words", C.c_int32), ("num_tasks", C.c_int32), ("resample_tasks", C.c_int32),
                 ("base_cells", C.c_void_p),
-                ("seg_off", C.c_void_p), ("seg_cells", C.c_void_p), ("task_rows", C.c_void_p)]
+                ("seg_off", C.c_void_p), ("seg_cells", C.c_void_p), ("task_rows", C.c_void_p),
+                ("agent_row_words", C.c_int32), ("agent_rows", C.c_void_p)]
 
 
 class State(C.Structure):

@@ -251,13 +251,15 @@ struct MainGeo {
   int64_t total;
 };
 
-__host__ __device__ inline MainGeo make_main_geo(int V, int maxch, int R) {
+// arw: words of the compact agent-rule rows (xmg_env_desc.agent_rows), 0
+// when the step fetches whole task rows
+__host__ __device__ inline MainGeo make_main_geo(int V, int maxch, int R, int arw) {
   MainGeo g;
   g.ob = 2 * V * V;
   g.stg = 16 * maxch + 16;
   // per-lane rule row; after the rule pass the warp's 32 rule rows hold its
   // 32 observation records (the staging area of the bulk store)
-  g.rb = max(16 * ((kRowHeader + R + 3) / 4), round16(g.ob));
+  g.rb = max(arw > 0 ? 4 * arw : 16 * ((kRowHeader + R + 3) / 4), round16(g.ob));
   g.total = (int64_t)kThreads * (g.stg + g.rb);
   return g;
 }
@@ -314,8 +316,12 @@ __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_
     }
     const bool rules_needed = R > 0 && (act == 0 || act == 3);
     if (rules_needed) {
-      const uint32_t* src = d.task_rows + (int64_t)task * d.row_words;
-      const int nq = (kRowHeader + R + 3) >> 2;
+      // the compact agent-rule row when the table has one (MOVE / PICK_UP
+      // fire nothing else), else the whole task row
+      const bool compact = d.agent_rows != nullptr;
+      const uint32_t* src = compact ? d.agent_rows + (int64_t)task * d.agent_row_words
+                                    : d.task_rows + (int64_t)task * d.row_words;
+      const int nq = compact ? d.agent_row_words >> 2 : (kRowHeader + R + 3) >> 2;
       const uint32_t rs = smem_u32(rbuf);
       if (nq <= 8) {  // rows of up to 28 rules: straight-line, predicated
 #pragma unroll
@@ -366,8 +372,10 @@ __device__ __forceinline__ void main_tile_body(const xmg_env_desc& d, const xmg_
     bool goal = false;
     if (ev == 0 || ev == 1) {
       Nbrs nb = load_nbrs(vw, H, W, r, c);
-      const int nr = R > 0 ? (int)(rbuf[1] & 0xff) : 0;
-      if (nr) {
+      if (d.agent_rows != nullptr) {  // compact row: count | MOVE mask << 8 | PICK_UP mask << 20
+        const uint32_t slots = R > 0 ? (rbuf[0] >> (8 + 12 * ev)) & 0xFFFu : 0u;
+        if (slots) pocket = agent_rules(vw, nb, rbuf + 1, slots, pocket);
+      } else if (const int nr = R > 0 ? (int)(rbuf[1] & 0xff) : 0) {
         if (R <= 32) {
           const uint32_t slots = rbuf[2 + ev];
           if (slots) pocket = agent_rules(vw, nb, rbuf + kRowHeader, slots, pocket);

@@ -261,10 +261,13 @@ bool pdl_enabled() {
   return on == 1;
 }
 
+// words per compact agent-rule row step_main fetches (0: whole task rows)
+inline int agent_words(const xmg_env_desc* d) { return d->agent_rows != nullptr ? d->agent_row_words : 0; }
+
 template <int MAXCH>
 int launch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
                 const uint32_t* flag, uint32_t epoch, int64_t n, cudaStream_t st, bool pdl) {
-  const MainGeo geo = make_main_geo(d->view_size, MAXCH, d->rule_width);
+  const MainGeo geo = make_main_geo(d->view_size, MAXCH, d->rule_width, agent_words(d));
   const DevInfo* di = cur_dev();
   if (!di) return -1;
   const int64_t blocks = (n + kThreads - 1) / kThreads;
@@ -345,11 +348,14 @@ int validate_desc(const xmg_env_desc* d, const xmg_state* s, int64_t n) {
   if (d->num_segments > 12) return fail("too many door segments");
   if (d->rule_width < 0 || d->rule_width > 255 || d->obj_width < 0 || d->obj_width > 255) return fail("bad widths");
   if (d->row_words < 4 || (d->row_words & 3)) return fail("row_words must be a positive multiple of 4");
+  if (d->agent_rows != nullptr &&
+      (d->agent_row_words < 4 || d->agent_row_words > 16 || (d->agent_row_words & 3)))
+    return fail("agent_row_words must be 4, 8, 12 or 16 (<= 12 compact rules)");
   if (d->num_tasks < 1) return fail("empty task table");
   if (!d->base_cells || !d->task_rows) return fail("null base_cells / task_rows");
   if (pick_maxch(d) == 0) return fail("view window too wide for this build (v*W + v > 482)");
   if (!grid_fits(d)) return fail("grid too large for this build (H*W <= 1024)");
-  if (make_main_geo(d->view_size, pick_maxch(d), d->rule_width).total > kMaxDynSmem - 1024 ||
+  if (make_main_geo(d->view_size, pick_maxch(d), d->rule_width, agent_words(d)).total > kMaxDynSmem - 1024 ||
       make_rare_geo(d->height, d->width, d->rule_width).total > kMaxDynSmem - 1024)
     return fail("grid too large for the shared-memory scratch of this build (H*W <= ~3000)");
   return 0;
@@ -645,7 +651,7 @@ int32_t xmg_profile_read(double* main_ms, double* rare_ms, int64_t* steps) {
 
 int64_t xmg_step_smem_bytes(const xmg_env_desc* desc) {
   if (!desc) return -1;
-  const int64_t a = make_main_geo(desc->view_size, pick_maxch(desc), desc->rule_width).total;
+  const int64_t a = make_main_geo(desc->view_size, pick_maxch(desc), desc->rule_width, agent_words(desc)).total;
   const int64_t b = make_rare_geo(desc->height, desc->width, desc->rule_width).total;
   return a > b ? a : b;
 }

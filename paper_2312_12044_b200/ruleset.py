@@ -127,6 +127,14 @@ class TaskTable:
     rule_width: int           # R
     obj_width: int            # O
     max_objects_used: int     # max active objects over rows (GridFull check)
+    # (M, agent_row_words) uint32 or None: per task only the rules a MOVE /
+    # PICK_UP can fire (AGENT_HOLD and the AGENT_NEAR family), in stored order:
+    # word 0 = count | MOVE slot mask << 8 | PICK_UP slot mask << 20 (masks
+    # over these compact slots), then the rule words as in `rows`; rows padded
+    # to 16 bytes.  step_main fetches it instead of the whole row (C3: 32 B
+    # instead of 64 B per MOVE / PICK_UP action).  None when a task has more
+    # than AGENT_ROW_MAX such rules.
+    agent_rows: np.ndarray | None = None
 
     @property
     def num_tasks(self) -> int:
@@ -140,9 +148,17 @@ class TaskTable:
     def goals(self) -> np.ndarray:
         return self.rows[:, 0]
 
+    @property
+    def agent_row_words(self) -> int:
+        return 0 if self.agent_rows is None else self.agent_rows.shape[1]
+
     def to_device(self, device):
         import torch
         return torch.from_numpy(self.rows.view(np.int32)).to(device)
+
+    def agent_rows_to_device(self, device):
+        import torch
+        return None if self.agent_rows is None else torch.from_numpy(self.agent_rows.view(np.int32)).to(device)
 
 
 def _left_pack(active: np.ndarray, values: np.ndarray) -> np.ndarray:
@@ -190,11 +206,39 @@ def pack_raw_rows(raw: np.ndarray, max_rules: int, max_objects: int) -> TaskTabl
                                                    (0x2841 >> (4 * np.clip(kinds - 8, 0, 3))) & 0xF, 0))
         rules[..., 2] = np.where(agent_near, allow, rules[..., 2]).astype(np.uint8)
         words[:, HEADER_WORDS:HEADER_WORDS + R] = np.ascontiguousarray(rules).view(np.uint32)[..., 0]
+        agent_rows = _pack_agent_rows(words[:, HEADER_WORDS:HEADER_WORDS + R], kinds)
+    else:
+        agent_rows = None
     if O:
         ob = np.zeros((m, 4 * ow), np.uint8)
         ob[:, :O] = objs
         words[:, HEADER_WORDS + R:HEADER_WORDS + R + ow] = ob.view(np.uint32)
-    return TaskTable(words, R, O, O)
+    return TaskTable(words, R, O, O, agent_rows)
+
+
+AGENT_ROW_MAX = 12  # compact agent rules per task (12-bit slot masks)
+
+
+def _pack_agent_rows(rule_words: np.ndarray, kinds: np.ndarray) -> np.ndarray | None:
+    """TaskTable.agent_rows from the packed rule words (M, R) and their kinds."""
+    near = (kinds == 2) | ((kinds >= 8) & (kinds <= 11))   # gated on MOVE and PICK_UP
+    fam = near | (kinds == 1)                              # + AGENT_HOLD: PICK_UP only
+    count = fam.sum(axis=1)
+    a = int(count.max(initial=0))
+    if a > AGENT_ROW_MAX:
+        return None
+    m = rule_words.shape[0]
+    out = np.zeros((m, (1 + a + 3) // 4 * 4), np.uint32)
+    if a:
+        compact = _left_pack(fam, rule_words)[:, :a]
+        near_c = _left_pack(fam, near)[:, :a]
+        live = np.arange(a)[None, :] < count[:, None]
+        bits = np.uint64(1) << np.arange(a, dtype=np.uint64)
+        move = ((near_c & live).astype(np.uint64) * bits).sum(axis=1)
+        pick = (live.astype(np.uint64) * bits).sum(axis=1)
+        out[:, 1:1 + a] = np.where(live, compact, 0)
+        out[:, 0] = (count.astype(np.uint64) | (move << np.uint64(8)) | (pick << np.uint64(20))).astype(np.uint32)
+    return out
 
 
 def pack_rulesets(rulesets: Sequence[Ruleset]) -> TaskTable:

@@ -268,6 +268,12 @@ class VecEnv:
         self._seg_off = torch.from_numpy(seg_off.astype(np.int16)).to(dev)
         self._seg_cells = torch.from_numpy(seg_cells.astype(np.int16)).to(dev)
         self._table = torch.from_numpy(table.rows.view(np.int32).copy()).to(dev)
+        # compact MOVE / PICK_UP rule rows (ruleset.TaskTable.agent_rows), xland only
+        agent_rows = getattr(table, "agent_rows", None) if scen == 0 and table.rule_width > 0 else None
+        if os.environ.get("XMG_AGENT_ROWS", "1") == "0":
+            agent_rows = None
+        self._agent_rows = None if agent_rows is None else \
+            torch.from_numpy(np.ascontiguousarray(agent_rows).view(np.int32)).to(dev)
         self.grids_flat = torch.zeros(n * self._hw + GRID_PAD, dtype=torch.uint8, device=dev)
         # 16-byte state word per env: [pose | pocket | step count, goal | task << 32]
         goals = table.rows[ids, 0].astype(np.uint64) if scen == 0 else np.zeros(n, np.uint64)
@@ -301,7 +307,9 @@ class VecEnv:
         self._desc = _lib.EnvDesc(h, w, v, params.step_budget, scen, int(params.see_through_walls), nseg, fixed,
                                   table.rule_width if scen == 0 else 0, table.obj_width, table.row_words,
                                   table.num_tasks, int(resample_tasks and scen == 0), self._base.data_ptr(),
-                                  self._seg_off.data_ptr(), self._seg_cells.data_ptr(), self._table.data_ptr())
+                                  self._seg_off.data_ptr(), self._seg_cells.data_ptr(), self._table.data_ptr(),
+                                  0 if self._agent_rows is None else self._agent_rows.shape[1],
+                                  _ptr(self._agent_rows))
         self._state = _lib.State(self.grids_flat.data_ptr(), self.agent.data_ptr(), self.rng.data_ptr(),
                                  self.work.data_ptr(), _ptr(self._next_grids), _ptr(self._next_state),
                                  _ptr(self._next_obs))

@@ -36,7 +36,7 @@ def test_abi_version_and_error_channel():
     L = _lib.lib()
     assert L.xmg_abi_version() == _lib.ABI_VERSION
     # a bad description is rejected on the host, before any CUDA call
-    d = _lib.EnvDesc(9, 9, 4, 243, 0, 1, 0, 0, 0, 0, 4, 1, 0, 1, 1, 1, 1)
+    d = _lib.EnvDesc(9, 9, 4, 243, 0, 1, 0, 0, 0, 0, 4, 1, 0, 1, 1, 1, 1, 0, None)
     st = _lib.State(1, 1, 1, 1)
     out = _lib.Out(None, 1, 1, 1, None)
     rc = L.xmg_step(C.byref(d), C.byref(st), 1, 0, 8, C.byref(out), None, 1, None)

@@ -128,5 +128,33 @@ def test_task_table_left_packs_like_the_reference():
     assert t.row_words % 4 == 0
 
 
+def test_agent_rows_are_the_move_pickup_rules_in_stored_order():
+    """TaskTable.agent_rows (the compact rows step_main fetches for MOVE /
+    PICK_UP): the AGENT_HOLD / AGENT_NEAR-family rule words of each row in
+    stored order, with the row's MOVE / PICK_UP masks re-indexed onto them."""
+    rs = Ruleset(goal=(4, 85, 102, 0), rules=((0, 0, 0, 0), (3, 85, 102, 150), (0, 0, 0, 0), (2, 86, 0, 57),
+                                             (1, 151, 0, 57)), init_objects=(0, 85, 0, 102, 86))
+    t = pack_rulesets([rs])
+    a = t.agent_rows[0]
+    assert t.agent_row_words == 4
+    assert a[0] & 0xFF == 2 and (a[0] >> 8) & 0xFFF == 0b01 and (a[0] >> 20) & 0xFFF == 0b11
+    assert a[1:3].tolist() == t.rows[0, HEADER_WORDS + 1:HEADER_WORDS + 3].tolist()
+    for cfg in ("medium", "high"):
+        tt = load_benchmark(benchmark_file(cfg)).task_table()
+        rows, ar = tt.rows, tt.agent_rows
+        assert ar is not None and tt.agent_row_words % 4 == 0
+        rng = np.random.default_rng(0)
+        for i in rng.choice(tt.num_tasks, 500, replace=False):
+            nr = int(rows[i, 1] & 0xFF)
+            words = rows[i, HEADER_WORDS:HEADER_WORDS + nr]
+            fam = [j for j in range(nr) if int(words[j] & 0xFF) in (1, 2, 8, 9, 10, 11)]
+            n = int(ar[i, 0] & 0xFF)
+            assert n == len(fam) and ar[i, 1:1 + n].tolist() == words[fam].tolist()
+            move, pick = int(ar[i, 0] >> 8) & 0xFFF, int(ar[i, 0] >> 20)
+            assert [(int(rows[i, 2]) >> j) & 1 for j in fam] == [(move >> k) & 1 for k in range(n)]
+            assert [(int(rows[i, 3]) >> j) & 1 for j in fam] == [(pick >> k) & 1 for k in range(n)]
+            assert move >> n == 0 and pick >> n == 0
+
+
 def test_golden_fixtures_present():
     assert len([f for f in os.listdir(GOLDEN) if f.endswith(".npz")]) >= 20
