@@ -208,13 +208,14 @@ __global__ void __launch_bounds__(kRollWarps * 32, XMG_ROLL_MINB) rollout_kernel
   uint32_t* rbuf = rules_s + lane * (geo.rbw / 4);
   auto load_row = [&](int who, int tk) {  // whole warp: task row header + rules of lane `who`
     if (R == 0) return;
-    const uint32_t* src = d.task_rows + (int64_t)tk * d.row_words;
-    uint32_t* dst = rules_s + who * (geo.rbw / 4);
-    for (int i = lane; i < kRowHeader + R; i += 32) dst[i] = src[i];
+    // rows and the shared row slots are 16-byte aligned and rbw bytes long
+    const uint4* src = reinterpret_cast<const uint4*>(d.task_rows + (int64_t)tk * d.row_words);
+    uint4* dst = reinterpret_cast<uint4*>(rules_s + who * (geo.rbw / 4));
+    for (int i = lane; i < geo.rbw / 16; i += 32) dst[i] = src[i];
   };
   if (R > 0 && valid) {
-    const uint32_t* src = d.task_rows + (int64_t)task * d.row_words;
-    for (int i = 0; i < kRowHeader + R; ++i) rbuf[i] = src[i];
+    const uint4* src = reinterpret_cast<const uint4*>(d.task_rows + (int64_t)task * d.row_words);
+    for (int i = 0; i < geo.rbw / 16; ++i) reinterpret_cast<uint4*>(rbuf)[i] = src[i];
   }
   __syncwarp();
 
