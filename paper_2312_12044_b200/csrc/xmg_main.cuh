@@ -572,4 +572,8 @@ __global__ void __launch_bounds__(kThreads, XMG_MINB) step_main(const xmg_env_de
                               0, 0,
 #endif
                               abort_flag);
+  // this CTA is done: the step's step_rare (a programmatic dependent that
+  // waits for this grid's completion before it reads the queues) may be
+  // scheduled as the last CTAs drain, instead of after the grid boundary
+  griddep_launch();
 }

@@ -395,6 +395,9 @@ __global__ void __launch_bounds__(kRareWarps * 32, XMG_MINB_RARE * 4 / kRareWarp
   // not both
   int put_w = per_q, jp = j, jr = -1, rs_w = 0;
   if (!reset_mode) {
+    // launched as a programmatic dependent of this step's step_main: the
+    // queues are complete once that grid has completed
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     cnt_put = s.work[count_index(epoch, 0, q)];
     cnt_reset = s.work[count_index(epoch, 1, q)];
     if (cnt_reset > 0 && per_q < 2) {  // a single warp per sub-queue does both

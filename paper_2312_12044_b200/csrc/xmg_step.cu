@@ -251,6 +251,9 @@ DevInfo* cur_dev() {
   return &g_dev[dev];
 }
 
+// XMG_RARE_PDL=0: step_rare as a plain launch after step_main
+bool rare_pdl();
+
 // XMG_PDL=0 turns the programmatic (overlapped) launches off
 bool pdl_enabled() {
   static int on = -1;
@@ -263,6 +266,15 @@ bool pdl_enabled() {
 
 // words per compact agent-rule row step_main fetches (0: whole task rows)
 inline int agent_words(const xmg_env_desc* d) { return d->agent_rows != nullptr ? d->agent_row_words : 0; }
+
+bool rare_pdl() {
+  static int on = -1;
+  if (on < 0) {
+    const char* v = getenv("XMG_RARE_PDL");
+    on = (v && !strcmp(v, "0")) ? 0 : 1;
+  }
+  return on == 1 && pdl_enabled();
+}
 
 template <int MAXCH>
 int launch_main(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, const void* actions, int dtype,
@@ -326,8 +338,21 @@ int launch_rare(const xmg_env_desc* d, const xmg_state* s, const xmg_out* o, con
   const int64_t need = ((n + kRareWarps * 64 - 1) / (kRareWarps * 64) + unit - 1) / unit * unit;  // <= a warp / 64 envs
   if (blocks > need) blocks = need;
   if (blocks < unit) blocks = unit;
-  step_rare<<<(unsigned)blocks, kRareWarps * 32, (size_t)geo.total, st>>>(*d, *s, *o, keys, flag, epoch, n,
-                                                                                track);
+  // the step's drain: a programmatic dependent of its step_main (which
+  // triggers as its CTAs finish; step_rare waits for that grid before reading
+  // the queues), so its launch overlaps step_main's last CTAs
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = keys == nullptr && rare_pdl() ? 1 : 0;
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(kRareWarps * 32);
+  cfg.dynamicSmemBytes = (size_t)geo.total;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t err = cudaLaunchKernelEx(&cfg, step_rare, *d, *s, *o, keys, flag, epoch, n, track);
+  if (err != cudaSuccess) return fail(std::string("step_rare: ") + cudaGetErrorString(err));
   return check_launch("step_rare");
 }
 
