@@ -193,11 +193,11 @@ def test_shards_reproduce_the_global_batch():
                 assert torch.equal(p.grids, whole.grids[sl])
 
 
-@pytest.mark.parametrize("knobs", [{"XMG_AHEAD": "0"}, {"XMG_AGENT_ROWS": "0"}, {"XMG_PDL": "0"}, {"XMG_RARE_CTAS": "2"}])
+@pytest.mark.parametrize("knobs", [{"XMG_AHEAD": "0"}, {"XMG_AGENT_ROWS": "0"}, {"XMG_PDL": "0"}, {"XMG_RARE_PDL": "0"}, {"XMG_RARE_CTAS": "2"}])
 def test_tuning_knobs_keep_parity(knobs):
     """The library's tuning switches (reset-ahead off, whole task rows instead of
     the compact agent-rule rows, no programmatic
-    overlap, a small step_rare grid) change scheduling only: a fresh process
+    overlap at all or none for step_rare, a small step_rare grid) change scheduling only: a fresh process
     with each switch reproduces the oracle bit for bit (switches are read once
     per process)."""
     import os
