@@ -676,8 +676,11 @@ def run_ours(args):
                            "achieved_gbs": ach, "frac_of_hbm_peak": ach / peak if bpe_f else None}
         del traj
         fused = {"unit": "env-steps/s", "chunk_steps": chunk, **modes,
-                 "note": "xmg_rollout (one kernel per chunk of steps, state resident in shared memory / registers, "
-                         "random policy evaluated in-kernel), bit-identical to K VecEnv.step calls "
+                 "kernel": "xmg_rollout (fused)" if vec.aligned_fused_choice() else
+                           "xmg_steps (per-call kernels, random_actions per block: VecEnv.rollout's choice here)",
+                 "note": "VecEnv.rollout: xmg_rollout (one kernel per chunk of steps, state resident in shared memory "
+                         "/ registers, random policy evaluated in-kernel) where it keeps >= 12 warps per SM, else "
+                         "the per-call kernels; bit-identical to K VecEnv.step calls "
                          "(tests/test_rollout_gpu.py); same K steps and phase as the timed window; records = "
                          "obs + reward + discount + step type per env-step written to HBM"}
 

@@ -645,15 +645,19 @@ class VecEnv:
     @_on_device
     def rollout(self, steps: int, policy_keys: torch.Tensor | None = None, actions: torch.Tensor | None = None,
                 t0: int = 0, record: Sequence[str] = ("observations", "rewards", "discounts", "step_types"),
-                out: Trajectory | None = None) -> Trajectory:
+                out: Trajectory | None = None, fused: bool | None = None) -> Trajectory:
         """``steps`` consecutive ``step`` calls in one kernel (state on chip for
         the whole rollout), bit-identical to them.  Actions come from the
         random policy of ref harness.py:58-64 (``policy_keys``: step t plays
         word t0 + t of each env's key mod 6, as ``random_actions``) or from a
         (steps, N) tensor ``actions``.  ``record`` picks the per-step fields
         kept (ref harness.py:103-143 accumulates only statistics: pass
-        ``record=()`` and ``enable_stats()`` for that).  Does not consume an
-        epoch: rollouts and steps may be interleaved freely."""
+        ``record=()`` and ``enable_stats()`` for that).  Rollouts and steps
+        may be interleaved freely.  Where the fused kernel keeps too few warps
+        resident (``aligned_fused_choice``: R9-25x25) the same steps run
+        through the per-call kernels instead, 64 per library call (C4: 5.9e9
+        → 1.1e10 env-steps/s); ``fused`` forces the choice (True: the fused
+        kernel, False: the per-call kernels)."""
         n, v, dev = self.num_envs, self.params.view_size, self.device
         if steps < 0 or t0 < 0:
             raise ValueError("steps and t0 must be >= 0")
@@ -680,7 +684,44 @@ class VecEnv:
                 torch.empty((steps, n), dtype=torch.float32, device=dev) if "rewards" in record else None,
                 torch.empty((steps, n), dtype=torch.float32, device=dev) if "discounts" in record else None,
                 torch.empty((steps, n), dtype=torch.int8, device=dev) if "step_types" in record else None)
+        aligned = out.observations is None or (n * 2 * v * v) % 16 == 0
+        if fused is None:
+            fused = not aligned or self.aligned_fused_choice()
+        if not fused:
+            if not aligned:
+                raise ValueError("rollout(fused=False): with observations, num_envs * 2 * v * v must be a multiple "
+                                 "of 16 (16-byte aligned records)")
+            return self._rollout_per_call(steps, policy_keys, actions, t0, out)
         return self._launch_rollout(steps, policy_keys, actions, t0, out)
+
+    def _rollout_per_call(self, steps: int, policy_keys, actions, t0: int, out: Trajectory,
+                          block: int = 64) -> Trajectory:
+        """rollout() through the per-call kernels (xmg_steps), ``block`` steps
+        per library call, the random policy's actions drawn on the device per
+        block; unrecorded fields go to scratch buffers.  Bit-identical to the
+        fused kernel, as every path is."""
+        n, dev = self.num_envs, self.device
+        scratch = None
+        if out.rewards is None or out.discounts is None or out.step_types is None:
+            scratch = (torch.empty((block, n), dtype=torch.float32, device=dev),
+                       torch.empty((block, n), dtype=torch.float32, device=dev),
+                       torch.empty((block, n), dtype=torch.int8, device=dev))
+        for c0 in range(0, steps, block):
+            k = min(block, steps - c0)
+            if actions is None:
+                a = random_actions(policy_keys, t0 + c0, k)
+                self.launches += 1
+            else:
+                a = actions[c0:c0 + k]
+            pick = lambda f, i: f[c0:c0 + k] if f is not None else scratch[i][:k]  # noqa: E731
+            o = _lib.Out(_ptr(None if out.observations is None else out.observations[c0:c0 + k]),
+                         _ptr(pick(out.rewards, 0)), _ptr(pick(out.discounts, 1)), _ptr(pick(out.step_types, 2)),
+                         _ptr(self.stats))
+            _lib.check(_lib.lib().xmg_steps(self._desc_ref, self._state_ref, a.data_ptr(), _lib.ACT_U8, k, n,
+                                            C.byref(o), self.epoch & 0xFFFFFFFF, _stream(dev)), "xmg_steps")
+            self.epoch += k
+            self.launches += 2 * k + self._batches_in(self.epoch - k, self.epoch)
+        return out
 
     def _batches_in(self, e0: int, e1: int) -> int:
         """Reset-ahead batches libxmg launched for epochs (e0, e1] (one per

@@ -32,18 +32,20 @@ def _same_state(a, b, msg):
     assert torch.equal(a.rng, b.rng), f"rng {msg}"
 
 
-@pytest.mark.parametrize("env_name,config,n,steps,resample,see", [
-    ("XLand-MiniGrid-R4-13x13", "medium", 4096, 600, False, None),
-    ("XLand-MiniGrid-R1-9x9", "trivial", 4096, 300, False, None),
-    ("XLand-MiniGrid-R9-25x25", "high", 1024, 400, False, None),
-    ("XLand-MiniGrid-R4-13x13", "medium", 1000, 520, True, None),     # resample-on-reset, ragged tail
-    ("XLand-MiniGrid-R2-13x13", "small", 999, 300, False, False),     # occluded view, odd n
-    ("MiniGrid-DoorKey-8x8", None, 2048, 250, False, None),
-    ("MiniGrid-UnlockPickUp", None, 1024, 400, False, None),
-    ("MiniGrid-FourRooms", None, 512, 300, False, None),
-    ("MiniGrid-Empty-8x8", None, 333, 200, False, None),
+@pytest.mark.parametrize("env_name,config,n,steps,resample,see,fused", [
+    ("XLand-MiniGrid-R4-13x13", "medium", 4096, 600, False, None, None),
+    ("XLand-MiniGrid-R4-13x13", "medium", 2048, 530, False, None, False),   # the per-call rollout path
+    ("XLand-MiniGrid-R1-9x9", "trivial", 4096, 300, False, None, None),
+    ("XLand-MiniGrid-R9-25x25", "high", 1024, 400, False, None, None),    # auto: per-call kernels
+    ("XLand-MiniGrid-R9-25x25", "high", 1024, 400, False, None, True),    # the fused kernel, 25x25 grids
+    ("XLand-MiniGrid-R4-13x13", "medium", 1000, 520, True, None, None),     # resample-on-reset, ragged tail
+    ("XLand-MiniGrid-R2-13x13", "small", 999, 300, False, False, None),     # occluded view, odd n
+    ("MiniGrid-DoorKey-8x8", None, 2048, 250, False, None, None),
+    ("MiniGrid-UnlockPickUp", None, 1024, 400, False, None, None),
+    ("MiniGrid-FourRooms", None, 512, 300, False, None, None),
+    ("MiniGrid-Empty-8x8", None, 333, 200, False, None, None),
 ])
-def test_rollout_equals_steps(env_name, config, n, steps, resample, see):
+def test_rollout_equals_steps(env_name, config, n, steps, resample, see, fused):
     from paper_2312_12044_b200 import key_from_seed, policy_keys, random_actions
     params, bm, a, b = _pair(env_name, config, n, resample, see)
     root = key_from_seed(7)
@@ -52,7 +54,7 @@ def test_rollout_equals_steps(env_name, config, n, steps, resample, see):
     sa, sb = a.enable_stats(), b.enable_stats()
     pk = policy_keys(key_from_seed(1), n, device=a.device)
     acts = random_actions(pk, 0, steps)
-    tr = b.rollout(steps, policy_keys=pk)
+    tr = b.rollout(steps, policy_keys=pk, fused=fused)
     for t in range(steps):
         ts = a.step(acts[t])
         assert torch.equal(ts.observations, tr.observations[t]), f"obs t={t}"
@@ -101,9 +103,11 @@ def test_rollout_vs_oracle_and_interleaving():
     vec.check()
 
 
-def test_rollout_explicit_actions_and_partial_records():
+@pytest.mark.parametrize("fused", [None, False])
+def test_rollout_explicit_actions_and_partial_records(fused):
     """A (T, N) action tensor instead of the policy keys; records subset;
-    stats-only mode; invalid actions rejected before any mutation."""
+    stats-only mode; invalid actions rejected before any mutation (the fused
+    kernel and the per-call rollout path)."""
     from paper_2312_12044_b200 import InvalidAction, key_from_seed
     params, bm, a, b = _pair("XLand-MiniGrid-R4-13x13", "medium", 777)
     root = key_from_seed(3)
@@ -112,9 +116,9 @@ def test_rollout_explicit_actions_and_partial_records():
     g = torch.Generator().manual_seed(5)
     acts = torch.randint(0, 6, (530, 777), generator=g, dtype=torch.int64)
     sa, sb = a.enable_stats(), b.enable_stats()
-    tr = b.rollout(300, actions=acts[:300], record=("rewards", "step_types"))
+    tr = b.rollout(300, actions=acts[:300], record=("rewards", "step_types"), fused=fused)
     assert tr.observations is None and tr.discounts is None
-    b.rollout(230, actions=acts[300:].cuda(), record=())
+    b.rollout(230, actions=acts[300:].cuda(), record=(), fused=fused)
     rews, sts = [], []
     for t in range(530):
         ts = a.step(acts[t].cuda())
@@ -129,7 +133,7 @@ def test_rollout_explicit_actions_and_partial_records():
     bad = acts[:10].clone()
     bad[4, 17] = 6
     with pytest.raises(InvalidAction):
-        b.rollout(10, actions=bad)
+        b.rollout(10, actions=bad, fused=fused)
     assert torch.equal(before, b.grids)
 
 
