@@ -149,3 +149,14 @@ def test_reset_ahead_stage_lifecycle():
     assert last[full].all()
     assert (on.reset_ahead_stage.cpu().numpy()[full] == 0).all()
     assert (on.agent_fields()[:, 4].cpu().numpy()[full] == 0).all()
+    # the take-overs flipped those envs to the second grid buffer: the
+    # accessors follow the buffer bit
+    flipped = ((on.agent[:, 0] >> 20) & 1).cpu().numpy().astype(bool)
+    assert flipped[full].all()
+    i = int(np.flatnonzero(flipped)[0])
+    g = on.grids
+    assert on.env_state(i).grid.cells == g[i].cpu().numpy().tobytes()
+    cells = g[i].clone()
+    cells[0] = 0x77
+    on.set_grid(i, cells)
+    assert torch.equal(on.grids[i], cells) and on._next_grids[i * cells.numel()].item() == 0x77
